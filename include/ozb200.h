@@ -1,0 +1,167 @@
+/*
+ * ozb200.h — C ABI of the B200-native Ozaki-INT8 HPL hot path.
+ *
+ * Plain pointers, sizes and an opaque cudaStream_t (passed as void*).  No
+ * torch types cross this boundary.  Every entry point returns an oz_status;
+ * oz_last_error() returns a thread-local message for the most recent failure
+ * on the calling thread.  The Python drop-in (paper_2509_23565_b200/_lib.py)
+ * maps the codes onto the reference exception hierarchy
+ * (/root/reference/pkg/src/ozemu/errors.py:4-41).
+ *
+ * Matrix conventions
+ *   - FP64 matrices are addressed by (row_stride, col_stride) in elements, so
+ *     row-major (numpy C order) and column-major (LAPACK/HPL order) views are
+ *     both accepted without copies.
+ *   - Slice stacks are int8, "K-major": slice s, vector v, inner index t lives
+ *     at slices[s*slice_stride + v*slice_ld + t].  slice_ld is a multiple of 16
+ *     bytes (TMA global-stride rule); bytes in [K, slice_ld) are written as 0.
+ *   - The emulated GEMM writes its output column-major with respect to its own
+ *     (m, n): out[col*ldc + row].  A row-major caller swaps the operands.
+ *
+ * Device pointers are CUDA global memory on the current device; `stream` is a
+ * cudaStream_t (NULL = legacy default stream).
+ */
+#ifndef OZB200_H
+#define OZB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (errors.py:4-41 mapping in paper_2509_23565_b200/_lib.py). */
+enum oz_status {
+  OZ_OK = 0,
+  OZ_INVALID_PARAMS = 1,   /* InvalidParamsError      errors.py:8   */
+  OZ_NON_FINITE = 2,       /* NonFiniteEntryError     errors.py:16  */
+  OZ_SHAPE = 3,            /* ShapeMismatchError      errors.py:20  */
+  OZ_ACC_OVERFLOW = 4,     /* AccumulatorOverflowError errors.py:28 */
+  OZ_SINGULAR_PIVOT = 5,   /* SingularPivotError      errors.py:32  */
+  OZ_CUDA_ERROR = 6,       /* runtime / driver / cuBLAS failure      */
+  OZ_UNSUPPORTED = 7       /* configuration not supported on device  */
+};
+
+/* Orientation / ScalingMode (split.py:31-46). */
+enum oz_orientation { OZ_ROW_SCALED = 0, OZ_COL_SCALED = 1 };
+enum oz_scaling { OZ_PER_VECTOR = 0, OZ_GLOBAL = 1 };
+
+/* Matrix generators (matgen.py:133-171). */
+enum oz_gen_kind {
+  OZ_GEN_UNIFORM = 0,            /* hpl_uniform: u - 0.5             matgen.py:164-171 */
+  OZ_GEN_PARAWILK = 1,           /* deterministic pattern            matgen.py:133-146 */
+  OZ_GEN_PARAWILK_RANDOMIZED = 2 /* pattern, zeros <- 2*u*u          matgen.py:149-161 */
+};
+
+const char* oz_last_error(void);
+int oz_version(void);
+/* Number of SMs of the current device (used by host-side schedulers). */
+int oz_sm_count(int* out);
+
+/* Scratch needed by oz_split (device bytes). */
+size_t oz_split_aux_bytes(void);
+
+/*
+ * split_matrix (split.py:109-160): per-vector (or global) frexp exponent of
+ * max|x|, then num_slices truncated slice_bits-bit signed slices.
+ * Bit-exact with the reference.  `aux` is device scratch of
+ * oz_split_aux_bytes() bytes; after the call aux[0] (int32) is nonzero iff a
+ * NaN/Inf was seen (the Python layer raises NonFiniteEntryError).
+ * slice_bits must be <= 7 (int8 slices).
+ */
+int oz_split(const double* src, int64_t rows, int64_t cols,
+             int64_t row_stride, int64_t col_stride,
+             int orientation, int mode, int num_slices, int slice_bits,
+             int8_t* slices, int64_t slice_ld, int64_t slice_stride,
+             int32_t* exps, void* aux, void* stream);
+
+/*
+ * Emulated product + epilogue (gemm.py:190-229 and :266-270):
+ *   P_p  = A_slice[pa[p]] . B_slice[pb[p]]^T        exact INT32 (tcgen05 kind::i8)
+ *   acc  = sum_p P_p * 2^-(shift[p])  in the given order, one FP64 rounding per pair
+ *   ab   = acc * 2^(expA[row] + expB[col])
+ *   out  = alpha*ab ; if (c_is_input && beta != 0) out = out + beta*c
+ * Pairs are 0-based slice indices; shift[p] = (i+j)*q with 1-based i, j.
+ * Requires inner * (2^q - 1)^2 < 2^31 (exact INT32 accumulation).
+ * growth_max (optional, device uint64): atomicMax of the IEEE bits of |out|.
+ */
+int oz_gemm_emu(int64_t m, int64_t n, int64_t inner,
+                const int8_t* a_slices, int64_t a_ld, int64_t a_sstride, int a_nslices,
+                const int32_t* a_exps,
+                const int8_t* b_slices, int64_t b_ld, int64_t b_sstride, int b_nslices,
+                const int32_t* b_exps,
+                int npairs, const int32_t* pair_a, const int32_t* pair_b,
+                const int32_t* pair_shift,
+                double alpha, double beta, double* c, int64_t ldc, int c_is_input,
+                unsigned long long* growth_max, void* stream);
+
+/* One slice-pair product as raw INT32 (debug/parity: test_gemm.py:218-240). */
+int oz_gemm_pair_i32(int64_t m, int64_t n, int64_t inner,
+                     const int8_t* a_slice, int64_t a_ld,
+                     const int8_t* b_slice, int64_t b_ld,
+                     int32_t* out, int64_t ldo, void* stream);
+
+/* Native FP64 GEMM comparator (gemm.py:259-262) through cuBLAS DGEMM,
+ * column-major: C = alpha*A*B + beta*C. */
+int oz_dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha,
+             const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
+             double* c, int64_t ldc, void* stream);
+
+/*
+ * Blocked right-looking LU with partial pivoting (solve.py:66-140) on a
+ * column-major n x n matrix, in place.  backend 0 = native FP64 Schur update
+ * (cuBLAS DGEMM), 1 = Ozaki-INT8 emulated Schur update with the given pair
+ * table.  ipiv (device int32[n]) receives LAPACK-style 0-based row
+ * interchanges; `stats` (device double[4]) receives {observed max, max|A|, -, -}
+ * for the growth factor; `info` (device int32) = first zero-pivot column + 1 or 0.
+ */
+size_t oz_lu_workspace_bytes(int64_t n, int64_t nb, int num_slices);
+int oz_lu_factor(double* a, int64_t n, int64_t lda, int64_t nb,
+                 int backend, int num_slices, int slice_bits,
+                 int npairs, const int32_t* pair_a, const int32_t* pair_b,
+                 const int32_t* pair_shift,
+                 int32_t* ipiv, double* stats, int32_t* info,
+                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* Host helper: LAPACK ipiv -> permutation vector (pivots[i] = original row). */
+int oz_ipiv_to_perm(const int32_t* ipiv_host, int64_t n, int64_t* perm_host);
+
+/* lu_solve (solve.py:143-156): x = U^-1 L^-1 b[perm] on device. */
+int oz_lu_solve(const double* lu, int64_t n, int64_t lda, const int64_t* perm,
+                const double* b, double* x, void* workspace, size_t workspace_bytes,
+                void* stream);
+size_t oz_lu_solve_workspace_bytes(int64_t n);
+
+/* scaled_residual inputs (solve.py:181-214): out[0]=||Ax-b||_inf,
+ * out[1]=||A||_inf, out[2]=||x||_inf, out[3]=||b||_inf.  A addressed by
+ * strides; summation order is fixed (deterministic). */
+int oz_residual_norms(const double* a, int64_t n, int64_t row_stride, int64_t col_stride,
+                      const double* x, const double* b, double* out, void* stream);
+
+/* b = A @ ones(n) (harness.py:126), A addressed by strides. */
+int oz_row_sums(const double* a, int64_t n, int64_t row_stride, int64_t col_stride,
+                double* out, void* stream);
+
+/* max |A| over an m x n strided matrix into out[0] (device double). */
+int oz_max_abs(const double* a, int64_t m, int64_t n, int64_t row_stride,
+               int64_t col_stride, double* out, void* stream);
+
+/*
+ * Generators (matgen.py:133-171), bit-exact with numpy's PCG64
+ * default_rng(seed).random((n, n)).  (state, inc) are the 128-bit PCG64 state
+ * after seeding, split in hi/lo words.  Output element (i, j) is written at
+ * out[i*row_stride + j*col_stride].
+ */
+int oz_generate(int kind, int64_t n, int64_t depth, int64_t block, double alpha,
+                uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                double* out, int64_t row_stride, int64_t col_stride, void* stream);
+
+/* Out-of-place strided copy (layout change), e.g. row-major -> column-major. */
+int oz_copy2d(const double* src, int64_t rows, int64_t cols, int64_t src_rs, int64_t src_cs,
+              double* dst, int64_t dst_rs, int64_t dst_cs, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OZB200_H */

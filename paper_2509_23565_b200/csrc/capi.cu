@@ -1,0 +1,105 @@
+// capi.cu — host-side plumbing of the C ABI: error strings, device queries,
+// the cuBLAS DGEMM comparator (gemm.py:259-262 "native" path) and small host
+// helpers.  No kernels of consequence live here.
+#include <cublas_v2.h>
+#include <stdarg.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+
+namespace oz {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+const char* last_error() { return g_err; }
+
+int sm_count() {
+  static std::mutex mu;
+  static std::unordered_map<int, int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+    n = 148;
+  cache[dev] = n;
+  return n;
+}
+
+// One cuBLAS handle per (device, host thread): handles are not thread-safe to
+// share while switching streams, and the reference harness may call from a
+// thread pool (harness.py:56-72).
+static cublasHandle_t cublas_handle() {
+  static thread_local std::unordered_map<int, cublasHandle_t> handles;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto it = handles.find(dev);
+  if (it != handles.end()) return it->second;
+  cublasHandle_t h = nullptr;
+  if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
+  handles[dev] = h;
+  return h;
+}
+
+int dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha, const double* a,
+          int64_t lda, const double* b, int64_t ldb, double beta, double* c, int64_t ldc,
+          cudaStream_t st) {
+  if (m == 0 || n == 0) return OZ_OK;
+  cublasHandle_t h = cublas_handle();
+  OZ_REQUIRE(h != nullptr, OZ_CUDA_ERROR, "cublasCreate failed");
+  OZ_REQUIRE(cublasSetStream(h, st) == CUBLAS_STATUS_SUCCESS, OZ_CUDA_ERROR,
+             "cublasSetStream failed");
+  cublasStatus_t s = cublasDgemm(h, transa ? CUBLAS_OP_T : CUBLAS_OP_N,
+                                 transb ? CUBLAS_OP_T : CUBLAS_OP_N, (int)m, (int)n, (int)k,
+                                 &alpha, a, (int)lda, b, (int)ldb, &beta, c, (int)ldc);
+  OZ_REQUIRE(s == CUBLAS_STATUS_SUCCESS, OZ_CUDA_ERROR, "cublasDgemm failed (%d)", (int)s);
+  return OZ_OK;
+}
+
+}  // namespace oz
+
+extern "C" const char* oz_last_error(void) { return oz::last_error(); }
+
+extern "C" int oz_version(void) { return 100; }
+
+extern "C" int oz_sm_count(int* out) {
+  *out = oz::sm_count();
+  return OZ_OK;
+}
+
+extern "C" int oz_dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha,
+                        const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
+                        double* c, int64_t ldc, void* stream) {
+  return oz::dgemm(transa, transb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc,
+                   oz::as_stream(stream));
+}
+
+// LAPACK-style interchanges -> permutation vector: pivots[i] is the original
+// row index that ends at position i (solve.py:80-82 perm bookkeeping).
+extern "C" int oz_ipiv_to_perm(const int32_t* ipiv, int64_t n, int64_t* perm) {
+  for (int64_t i = 0; i < n; ++i) perm[i] = i;
+  for (int64_t t = 0; t < n; ++t) {
+    const int64_t p = ipiv[t];
+    if (p < 0 || p >= n) {
+      oz::set_error("ipiv[%lld]=%lld out of range", (long long)t, (long long)p);
+      return OZ_INVALID_PARAMS;
+    }
+    if (p != t) {
+      const int64_t tmp = perm[t];
+      perm[t] = perm[p];
+      perm[p] = tmp;
+    }
+  }
+  return OZ_OK;
+}

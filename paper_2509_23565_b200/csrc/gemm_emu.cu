@@ -1,0 +1,472 @@
+// gemm_emu.cu — K3+K4+K5 of SURVEY §2.2: the Ozaki-INT8 emulated DGEMM.
+//
+// Reference semantics (/root/reference/pkg/src/ozemu/gemm.py):
+//   pairs (i,j) with i+j <= t, ordered by (i+j, i)               :157-178
+//   out = 0; for (i,j): out += ldexp(A_i @ B_j, eA+eB-(i+j)q)   :214-222
+//   out = alpha*out; out = out + beta*c                          :266-270
+// The integer products A_i @ B_j are exact (INT32 on the tensor cores), the
+// FP64 accumulation is done per element in the reference pair order with one
+// rounding per pair (fma(P, 2^-(i+j)q, acc)), and the row/column exponent is
+// applied once at the end (exact power-of-two scaling) — bit-identical to the
+// reference whenever no intermediate over/underflows.
+//
+// Kernel design (sm_100a):
+//   * persistent CTAs (one per SM), grouped raster over 128x128 output tiles;
+//   * loop order tile -> pair -> K: one INT32 product per pair lands in a TMEM
+//     accumulator (tcgen05.mma.cta_group::1.kind::i8, M=128, N=128, K=32),
+//     double-buffered so the epilogue of pair p overlaps the MMAs of pair p+1;
+//   * operands are K-major int8 slice tiles (128 rows x 128 bytes) staged by
+//     TMA (cp.async.bulk.tensor.3d, 128B swizzle) through a 6-stage mbarrier ring;
+//   * warp roles: w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
+//     w4..w11 epilogue (each owns 32 TMEM lanes x 64 columns and keeps its
+//     64 FP64 accumulators in registers for the whole pair loop);
+//   * the FP64 recombine, alpha/beta epilogue (C read once, written once) and
+//     the optional growth max (solve.py:135) are fused in the epilogue.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace oz {
+namespace emu {
+
+constexpr int BM = 128;
+constexpr int BN = 128;
+constexpr int BK = 128;  // bytes of K per stage (one 128B swizzle atom)
+constexpr int STAGES = 6;
+constexpr int NUM_ACC = 2;
+constexpr int TMEM_COLS = 256;
+constexpr int NUM_THREADS = 384;
+constexpr int EPI_WARP0 = 4;
+constexpr int MAX_PAIRS = 256;
+constexpr int TILE_BYTES = BM * BK;  // == BN * BK
+constexpr int STAGE_BYTES = 2 * TILE_BYTES;
+constexpr int GROUP_M = 16;
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + 256;
+
+// instruction descriptor: D=S32, A=B=signed int8, both K-major, M=128, N=128
+constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+
+struct Params {
+  int m, n, inner;
+  int num_m_tiles, num_n_tiles, num_tiles;
+  int nkb;
+  int npairs;
+  const int32_t* expA;
+  const int32_t* expB;
+  double* c;
+  int64_t ldc;
+  int c_is_input;
+  double alpha, beta;
+  unsigned long long* growth;
+  int32_t* debug_out;  // pair-debug mode: raw INT32 product
+  int64_t ldo;
+  uint8_t pa[MAX_PAIRS];
+  uint8_t pb[MAX_PAIRS];
+  uint16_t shift[MAX_PAIRS];
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// K-major, 128B-swizzled shared-memory matrix descriptor (8-row groups 1024B apart).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;            // leading byte offset (unused for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;  // stride byte offset
+  d |= (uint64_t)1 << 46;            // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+
+// exact int32 -> double on the FP64 pipe (magic-number trick)
+__device__ __forceinline__ double i32_to_f64(uint32_t v) {
+  const double d = __hiloint2double(0x43300000, (int)(v ^ 0x80000000u));
+  return __dsub_rn(d, 4503601774854144.0);  // 2^52 + 2^31
+}
+
+__device__ __forceinline__ void tile_coords(const Params& p, int t, int& mt, int& nt) {
+  const int per_group = GROUP_M * p.num_n_tiles;
+  const int g = t / per_group;
+  const int first_m = g * GROUP_M;
+  int gm = p.num_m_tiles - first_m;
+  gm = gm < GROUP_M ? gm : GROUP_M;
+  const int r = t - g * per_group;
+  mt = first_m + r % gm;
+  nt = r / gm;
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    emu_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                    const __grid_constant__ CUtensorMap tmB, const __grid_constant__ Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + STAGES * TILE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = bars + 2 * STAGES + NUM_ACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 2 * NUM_ACC);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int b = 0; b < NUM_ACC; ++b) {
+      mbar_init(smem_u32(&tfull[b]), 1);
+      mbar_init(smem_u32(&tempty[b]), (NUM_THREADS / 32 - EPI_WARP0));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp < EPI_WARP0) {
+    // warpgroup 0 (producer / MMA / allocator) donates registers to the epilogue
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+  }
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        int mt, nt;
+        tile_coords(p, t, mt, nt);
+        for (int q = 0; q < p.npairs; ++q) {
+          const int sa = p.pa[q], sb = p.pb[q];
+          for (int kb = 0; kb < p.nkb; ++kb) {
+            mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+            const uint32_t fb = smem_u32(&full[stage]);
+            mbar_expect_tx(fb, STAGE_BYTES);
+            tma_load_3d(smem_u32(smA + stage * TILE_BYTES), &tmA, fb, kb * BK, mt * BM, sa);
+            tma_load_3d(smem_u32(smB + stage * TILE_BYTES), &tmB, fb, kb * BK, nt * BN, sb);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t it = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        for (int q = 0; q < p.npairs; ++q, ++it) {
+          const uint32_t buf = it & 1, aph = (it >> 1) & 1;
+          mbar_wait(smem_u32(&tempty[buf]), aph ^ 1);
+          tc_fence_after();
+          const uint32_t dtmem = tmem_base + buf * BN;
+          for (int kb = 0; kb < p.nkb; ++kb) {
+            mbar_wait(smem_u32(&full[stage]), phase);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(smA + stage * TILE_BYTES);
+            const uint32_t b0 = smem_u32(smB + stage * TILE_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < BK / 32; ++kk) {
+              tc_mma_i8(dtmem, sdesc(a0 + kk * 32), sdesc(b0 + kk * 32), IDESC,
+                        (kb | kk) != 0 ? 1u : 0u);
+            }
+            tc_commit(smem_u32(&empty[stage]));
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          tc_commit(smem_u32(&tfull[buf]));
+        }
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // --------------------------------------------------------------- epilogue
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+    const int ew = warp - EPI_WARP0;  // 0..7
+    const int quad = warp & 3;        // TMEM lane quadrant this warp may access
+    const int half = ew >> 2;         // column half (0: cols 0-63, 1: 64-127)
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    double gmax = 0.0;
+    uint32_t it = 0;
+    const bool debug = p.debug_out != nullptr;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      int mt, nt;
+      tile_coords(p, t, mt, nt);
+      double acc[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) acc[i] = 0.0;
+      const int row = mt * BM + quad * 32 + lane;
+      const int col0 = nt * BN + half * 64;
+      for (int q = 0; q < p.npairs; ++q, ++it) {
+        const uint32_t buf = it & 1, aph = (it >> 1) & 1;
+        mbar_wait(smem_u32(&tfull[buf]), aph);
+        tc_fence_after();
+        const double s = pow2(-(int)p.shift[q]);
+        const uint32_t taddr = tmem_base + lane_base + buf * BN + half * 64;
+#pragma unroll
+        for (int c = 0; c < 64; c += 16) {
+          uint32_t v[16];
+          tmem_ld16(taddr + c, v);
+          tmem_wait_ld();
+          if (debug) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int col = col0 + c + i;
+              if (row < p.m && col < p.n) p.debug_out[(int64_t)col * p.ldo + row] = (int32_t)v[i];
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[c + i] = fma(i32_to_f64(v[i]), s, acc[c + i]);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
+      }
+      if (debug) continue;
+      // final scale, alpha/beta epilogue, column-major store (coalesced per column)
+      if (row < p.m) {
+        const int er = p.expA[row];
+        const bool use_c = p.c_is_input && p.beta != 0.0;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const int col = col0 + i;
+          if (col < p.n) {
+            const double ab = ldexp_exact(acc[i], er + p.expB[col]);
+            double out = __dmul_rn(p.alpha, ab);
+            double* dst = p.c + (int64_t)col * p.ldc + row;
+            if (use_c) out = __dadd_rn(out, __dmul_rn(p.beta, *dst));
+            *dst = out;
+            gmax = fmax(gmax, fabs(out));
+          }
+        }
+      }
+    }
+    if (p.growth != nullptr) {
+      gmax = warp_max(gmax);
+      if (lane == 0 && gmax > 0.0) atomic_max_abs(p.growth, gmax);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult qres;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qres) ==
+            cudaSuccess &&
+        qres == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+int make_slice_map(CUtensorMap* map, const int8_t* base, int64_t inner, int64_t rows,
+                   int64_t ld, int64_t sstride, int nslices) {
+  auto fn = encode_fn();
+  OZ_REQUIRE(fn != nullptr, OZ_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  OZ_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15) == 0, OZ_INVALID_PARAMS,
+             "slice buffer must be 16-byte aligned");
+  OZ_REQUIRE(ld % 16 == 0 && sstride % 16 == 0, OZ_INVALID_PARAMS,
+             "slice strides must be multiples of 16 bytes");
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)nslices};
+  cuuint64_t strides[2] = {(cuuint64_t)ld, (cuuint64_t)sstride};
+  cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)BM, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  OZ_REQUIRE(r == CUDA_SUCCESS, OZ_CUDA_ERROR, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return OZ_OK;
+}
+
+int launch(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    OZ_CHECK_CUDA(cudaFuncSetAttribute(emu_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)SMEM_BYTES));
+    attr_set = true;
+  }
+  p.num_m_tiles = (int)ceil_div(p.m, BM);
+  p.num_n_tiles = (int)ceil_div(p.n, BN);
+  p.num_tiles = p.num_m_tiles * p.num_n_tiles;
+  p.nkb = (int)ceil_div(p.inner, BK);
+  int grid = sm_count();
+  if (grid > p.num_tiles) grid = p.num_tiles;
+  emu_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ta, tb, p);
+  OZ_CHECK_LAUNCH();
+  return OZ_OK;
+}
+
+}  // namespace emu
+
+int gemm_emu_launch(int64_t m, int64_t n, int64_t inner, const int8_t* a_slices, int64_t a_ld,
+                    int64_t a_sstride, int a_nslices, const int32_t* a_exps,
+                    const int8_t* b_slices, int64_t b_ld, int64_t b_sstride, int b_nslices,
+                    const int32_t* b_exps, int npairs, const int32_t* pair_a,
+                    const int32_t* pair_b, const int32_t* pair_shift, double alpha, double beta,
+                    double* c, int64_t ldc, int c_is_input, unsigned long long* growth,
+                    cudaStream_t st) {
+  using namespace emu;
+  OZ_REQUIRE(m >= 1 && n >= 1 && inner >= 1, OZ_INVALID_PARAMS, "empty GEMM");
+  OZ_REQUIRE(m < (1ll << 31) && n < (1ll << 31), OZ_INVALID_PARAMS, "dimension too large");
+  OZ_REQUIRE(inner * 127ll * 127ll < (1ll << 31), OZ_ACC_OVERFLOW,
+             "inner dimension %lld breaks exact INT32 accumulation of int8 slices",
+             (long long)inner);
+  OZ_REQUIRE(npairs >= 1 && npairs <= MAX_PAIRS, OZ_INVALID_PARAMS, "npairs out of range");
+  OZ_REQUIRE(ldc >= m, OZ_INVALID_PARAMS, "ldc < m");
+  Params p{};
+  p.m = (int)m;
+  p.n = (int)n;
+  p.inner = (int)inner;
+  p.npairs = npairs;
+  for (int i = 0; i < npairs; ++i) {
+    OZ_REQUIRE(pair_a[i] >= 0 && pair_a[i] < a_nslices && pair_b[i] >= 0 &&
+                   pair_b[i] < b_nslices && pair_shift[i] >= 0 && pair_shift[i] < 1000,
+               OZ_INVALID_PARAMS, "bad pair table entry %d", i);
+    p.pa[i] = (uint8_t)pair_a[i];
+    p.pb[i] = (uint8_t)pair_b[i];
+    p.shift[i] = (uint16_t)pair_shift[i];
+  }
+  p.expA = a_exps;
+  p.expB = b_exps;
+  p.c = c;
+  p.ldc = ldc;
+  p.c_is_input = c_is_input;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.growth = growth;
+  CUtensorMap ta, tb;
+  OZ_TRY(make_slice_map(&ta, a_slices, inner, m, a_ld, a_sstride, a_nslices));
+  OZ_TRY(make_slice_map(&tb, b_slices, inner, n, b_ld, b_sstride, b_nslices));
+  return launch(ta, tb, p, st);
+}
+
+}  // namespace oz
+
+extern "C" int oz_gemm_emu(int64_t m, int64_t n, int64_t inner, const int8_t* a_slices,
+                           int64_t a_ld, int64_t a_sstride, int a_nslices, const int32_t* a_exps,
+                           const int8_t* b_slices, int64_t b_ld, int64_t b_sstride, int b_nslices,
+                           const int32_t* b_exps, int npairs, const int32_t* pair_a,
+                           const int32_t* pair_b, const int32_t* pair_shift, double alpha,
+                           double beta, double* c, int64_t ldc, int c_is_input,
+                           unsigned long long* growth_max, void* stream) {
+  return oz::gemm_emu_launch(m, n, inner, a_slices, a_ld, a_sstride, a_nslices, a_exps, b_slices,
+                             b_ld, b_sstride, b_nslices, b_exps, npairs, pair_a, pair_b,
+                             pair_shift, alpha, beta, c, ldc, c_is_input, growth_max,
+                             oz::as_stream(stream));
+}
+
+extern "C" int oz_gemm_pair_i32(int64_t m, int64_t n, int64_t inner, const int8_t* a_slice,
+                                int64_t a_ld, const int8_t* b_slice, int64_t b_ld, int32_t* out,
+                                int64_t ldo, void* stream) {
+  using namespace oz;
+  using namespace oz::emu;
+  OZ_REQUIRE(m >= 1 && n >= 1 && inner >= 1, OZ_INVALID_PARAMS, "empty GEMM");
+  OZ_REQUIRE(inner * 127ll * 127ll < (1ll << 31), OZ_ACC_OVERFLOW, "inner too large");
+  OZ_REQUIRE(ldo >= m, OZ_INVALID_PARAMS, "ldo < m");
+  Params p{};
+  p.m = (int)m;
+  p.n = (int)n;
+  p.inner = (int)inner;
+  p.npairs = 1;
+  p.debug_out = out;
+  p.ldo = ldo;
+  p.alpha = 1.0;
+  CUtensorMap ta, tb;
+  OZ_TRY(make_slice_map(&ta, a_slice, inner, m, a_ld, round_up(m * a_ld, 16), 1));
+  OZ_TRY(make_slice_map(&tb, b_slice, inner, n, b_ld, round_up(n * b_ld, 16), 1));
+  return launch(ta, tb, p, as_stream(stream));
+}

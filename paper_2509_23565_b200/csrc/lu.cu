@@ -1,0 +1,840 @@
+// lu.cu — K7..K12 of SURVEY §2.2: the FP64 side of the HPL-style LU.
+//
+// Reference: /root/reference/pkg/src/ozemu/solve.py
+//   _panel_factor  :66-91   partial pivoting (first max wins ties), whole-row
+//                           swaps, column DIVIDED by the pivot, rank-1 update
+//                           as outer product then subtraction (no FMA)
+//   lu_factor      :94-140  blocked right-looking: panel, trsm (unit lower),
+//                           Schur update through the GEMM backend, growth
+//   lu_solve       :143-156 perm gather, unit-lower then upper substitution
+//   scaled_residual:181-214 ||Ax-b|| / ((||A|| ||x|| + ||b||) n eps)
+//
+// Storage is column-major (LAPACK/HPL order) with leading dimension lda.
+//
+// Panel design: the nb-wide panel is factored in windows of w <= 64 columns.
+// Each window runs as ONE cooperative persistent kernel: every CTA keeps a
+// slab of rows x w columns resident in shared memory for all w column steps;
+// per step the CTAs publish their best pivot candidate (|value|, position,
+// row data) to global memory, meet at a single grid barrier, and all reduce
+// the candidates identically.  Rows never move inside the kernel — each row
+// keeps a logical position, and the interchanges are applied afterwards by a
+// gather (compose_swaps + laswp_gather), which turns LAPACK's sequential
+// interchanges into one read-all/write-all pass per column.  The rest of the
+// panel is updated with trsm + cuBLAS DGEMM; the Schur update is cuBLAS DGEMM
+// (native comparator) or the Ozaki-INT8 tcgen05 GEMM (gemm_emu.cu).
+#include <vector>
+
+#include "common.cuh"
+
+namespace oz {
+
+int dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha, const double* a,
+          int64_t lda, const double* b, int64_t ldb, double beta, double* c, int64_t ldc,
+          cudaStream_t st);
+int split_launch(const double* src, int64_t rows, int64_t cols, int64_t row_stride,
+                 int64_t col_stride, int orientation, int mode, int k, int q, int8_t* slices,
+                 int64_t slice_ld, int64_t slice_stride, int32_t* exps, void* aux_v,
+                 cudaStream_t st);
+int gemm_emu_launch(int64_t m, int64_t n, int64_t inner, const int8_t* a_slices, int64_t a_ld,
+                    int64_t a_sstride, int a_nslices, const int32_t* a_exps,
+                    const int8_t* b_slices, int64_t b_ld, int64_t b_sstride, int b_nslices,
+                    const int32_t* b_exps, int npairs, const int32_t* pair_a,
+                    const int32_t* pair_b, const int32_t* pair_shift, double alpha, double beta,
+                    double* c, int64_t ldc, int c_is_input, unsigned long long* growth,
+                    cudaStream_t st);
+
+namespace {
+
+constexpr int PANEL_W = 64;  // max window width
+constexpr int PANEL_THREADS = 256;
+constexpr int PANEL_WARPS = PANEL_THREADS / 32;
+constexpr int CAND_STRIDE = 4 + PANEL_W;  // doubles per candidate record
+constexpr int TRSM_W = 64;                // diagonal block of the blocked trsm
+constexpr int TRSM_C = 16;                // right-hand-side columns per CTA
+constexpr int SWAP_MAX = 2048;            // max entries of a composed swap list (2*nb)
+
+// ------------------------------------------------------------------ grid barrier
+struct GridBar {
+  unsigned count;
+  unsigned gen;
+};
+
+__device__ __forceinline__ void grid_sync(GridBar* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = &bar->gen;
+    const unsigned g = *vgen;
+    __threadfence();
+    if (atomicAdd(&bar->count, 1u) == nblocks - 1) {
+      atomicExch(&bar->count, 0u);
+      __threadfence();
+      atomicAdd(&bar->gen, 1u);
+    } else {
+      while (*vgen == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// np.argmax(|col|) order: larger magnitude wins, ties -> smaller logical position
+__device__ __forceinline__ bool better(double a1, int p1, double a2, int p2) {
+  return a1 > a2 || (a1 == a2 && p1 < p2);
+}
+
+struct PanelArgs {
+  double* a;
+  int64_t lda;
+  int64_t r0;  // first row (== first column of the window)
+  int64_t m;   // rows r0..r0+m-1
+  int w;       // window width (<= PANEL_W)
+  int rows_per_cta;
+  int32_t* ipiv;
+  unsigned long long* growth;
+  int32_t* info;
+  GridBar* bar;
+  double* cand;  // [2][gridDim][CAND_STRIDE]
+};
+
+struct PanelShared {
+  double red_a[PANEL_WARPS];
+  int red_p[PANEL_WARPS];
+  int red_r[PANEL_WARPS];
+  int occ[PANEL_W];
+  double urow[PANEL_W];
+  int best;
+};
+
+size_t panel_smem_bytes(int w, int R) {
+  return (size_t)w * R * sizeof(double) + (size_t)R * sizeof(int);
+}
+
+// One window of the panel: solve.py:75-90 for columns r0..r0+w-1 over rows r0..
+__global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArgs p) {
+  extern __shared__ double sm[];  // slab [w][R] column-major, then pos[R]
+  __shared__ PanelShared sh;
+  const int R = p.rows_per_cta;
+  const int w = p.w;
+  const int64_t row_lo = (int64_t)blockIdx.x * R;
+  const int nloc = (int)max((int64_t)0, min((int64_t)R, p.m - row_lo));
+  int* pos = reinterpret_cast<int*>(sm + (size_t)w * R);  // logical position; -1 = pivot used
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double* abase = p.a + p.r0 * p.lda + p.r0 + row_lo;
+
+  for (int c = 0; c < w; ++c)
+    for (int r = tid; r < nloc; r += PANEL_THREADS) sm[c * R + r] = abase[c * p.lda + r];
+  for (int r = tid; r < nloc; r += PANEL_THREADS) pos[r] = (int)(row_lo + r);
+  for (int i = tid; i < PANEL_W; i += PANEL_THREADS) sh.occ[i] = i;
+  __syncthreads();
+
+  double gmax = 0.0;
+  for (int i = tid; i < nloc * w; i += PANEL_THREADS) {
+    const int c = i / nloc, r = i - c * nloc;
+    gmax = fmax(gmax, fabs(sm[c * R + r]));
+  }
+
+  for (int t = 0; t <= w; ++t) {
+    // ---- publish this CTA's pivot candidate for column t (values after step t-1)
+    if (t < w) {
+      const int buf = t & 1;
+      double ba = -1.0;
+      int bp = 0x7fffffff, br = -1;
+      for (int r = tid; r < nloc; r += PANEL_THREADS) {
+        const int pr = pos[r];
+        if (pr < 0) continue;
+        const double v = fabs(sm[t * R + r]);
+        if (better(v, pr, ba, bp)) {
+          ba = v;
+          bp = pr;
+          br = r;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double oa = __shfl_xor_sync(0xffffffffu, ba, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+        const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+        if (better(oa, op, ba, bp)) {
+          ba = oa;
+          bp = op;
+          br = orr;
+        }
+      }
+      if (lane == 0) {
+        sh.red_a[wid] = ba;
+        sh.red_p[wid] = bp;
+        sh.red_r[wid] = br;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double fa = sh.red_a[0];
+        int fp = sh.red_p[0], fr = sh.red_r[0];
+        for (int i = 1; i < PANEL_WARPS; ++i)
+          if (better(sh.red_a[i], sh.red_p[i], fa, fp)) {
+            fa = sh.red_a[i];
+            fp = sh.red_p[i];
+            fr = sh.red_r[i];
+          }
+        sh.best = fr;
+      }
+      __syncthreads();
+      const int br_ = sh.best;
+      double* rec = p.cand + ((size_t)buf * gridDim.x + blockIdx.x) * CAND_STRIDE;
+      long long* irec = reinterpret_cast<long long*>(rec);
+      if (br_ < 0) {
+        if (tid == 0) {
+          rec[0] = -1.0;
+          irec[1] = 0x7fffffff;
+          irec[2] = -1;
+        }
+      } else {
+        if (tid == 0) {
+          rec[0] = fabs(sm[t * R + br_]);
+          irec[1] = pos[br_];
+          irec[2] = row_lo + br_;
+        }
+        for (int c = t + tid; c < w; c += PANEL_THREADS) rec[4 + c] = sm[c * R + br_];
+      }
+    }
+    if (t == w) break;
+
+    // ---- one grid barrier per column, then every CTA reduces all candidates
+    const int buf = t & 1;
+    grid_sync(p.bar, gridDim.x);
+    if (wid == 0) {
+      double ba = -1.0;
+      int bp = 0x7fffffff, bg = 0;
+      for (int g = lane; g < (int)gridDim.x; g += 32) {
+        const double* rec = p.cand + ((size_t)buf * gridDim.x + g) * CAND_STRIDE;
+        const double av = __ldcg(rec);
+        const int pv = (int)__ldcg(reinterpret_cast<const long long*>(rec) + 1);
+        if (better(av, pv, ba, bp)) {
+          ba = av;
+          bp = pv;
+          bg = g;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double oa = __shfl_xor_sync(0xffffffffu, ba, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+        const int og = __shfl_xor_sync(0xffffffffu, bg, o);
+        if (better(oa, op, ba, bp)) {
+          ba = oa;
+          bp = op;
+          bg = og;
+        }
+      }
+      if (lane == 0) sh.best = bg;
+    }
+    __syncthreads();
+    const double* win = p.cand + ((size_t)buf * gridDim.x + sh.best) * CAND_STRIDE;
+    const int ppos = (int)__ldcg(reinterpret_cast<const long long*>(win) + 1);
+    const int64_t prow = __ldcg(reinterpret_cast<const long long*>(win) + 2);
+    for (int c = t + tid; c < w; c += PANEL_THREADS) sh.urow[c] = __ldcg(win + 4 + c);
+    const int rt = sh.occ[t];  // relative physical row currently at position t
+    __syncthreads();
+    const double piv = sh.urow[t];
+    if (tid == 0) {
+      if (blockIdx.x == 0) {
+        p.ipiv[p.r0 + t] = (int32_t)(p.r0 + ppos);
+        if (piv == 0.0) atomicCAS(reinterpret_cast<int*>(p.info), 0, (int)(p.r0 + t + 1));
+      }
+      // interchange bookkeeping (solve.py:80-82): pivot row is final; the row
+      // at position t takes the pivot's old position
+      if (prow >= row_lo && prow < row_lo + nloc) pos[prow - row_lo] = -1;
+      if (rt != prow) {
+        if (rt >= row_lo && rt < row_lo + nloc) pos[rt - row_lo] = ppos;
+        if (ppos < PANEL_W) sh.occ[ppos] = rt;
+      }
+    }
+    __syncthreads();
+    // column scaling by DIVISION (solve.py:84) and rank-1 update (:86) as
+    // product-then-subtract, exactly like np.outer followed by -=
+    for (int r = tid; r < nloc; r += PANEL_THREADS) {
+      if (pos[r] < 0) continue;
+      const double l = sm[t * R + r] / piv;
+      sm[t * R + r] = l;
+      for (int c = t + 1; c < w; ++c) {
+        const double x = __dsub_rn(sm[c * R + r], __dmul_rn(l, sh.urow[c]));
+        sm[c * R + r] = x;
+        gmax = fmax(gmax, fabs(x));
+      }
+    }
+    __syncthreads();
+  }
+  for (int c = 0; c < w; ++c)
+    for (int r = tid; r < nloc; r += PANEL_THREADS) abase[c * p.lda + r] = sm[c * R + r];
+  if (p.growth) {
+    gmax = warp_max(gmax);
+    if (lane == 0 && gmax > 0.0) atomic_max_abs(p.growth, gmax);
+  }
+}
+
+// ------------------------------------------------- interchanges -> gather list
+// Simulates LAPACK's sequential interchanges ipiv[t0..t0+S) on row indices and
+// emits (dst, src) pairs: new_row[dst] = old_row[src].  Single thread; the
+// out-of-block positions live in a small open-addressing table.
+__global__ void compose_swaps_kernel(const int32_t* __restrict__ ipiv, int64_t t0, int S,
+                                     int32_t* dst, int32_t* src, int32_t* count) {
+  constexpr int H = 4096;
+  __shared__ int32_t cur[SWAP_MAX / 2];
+  __shared__ int32_t hkey[H];
+  __shared__ int32_t hval[H];
+  for (int i = threadIdx.x; i < H; i += blockDim.x) hkey[i] = -1;
+  for (int i = threadIdx.x; i < S; i += blockDim.x) cur[i] = (int32_t)(t0 + i);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  auto slot = [&](int32_t key) {
+    unsigned h = ((unsigned)key * 2654435761u) & (H - 1);
+    while (hkey[h] != -1 && hkey[h] != key) h = (h + 1) & (H - 1);
+    return h;
+  };
+  for (int t = 0; t < S; ++t) {
+    const int32_t pr = ipiv[t0 + t];
+    if (pr == t0 + t) continue;
+    const int32_t a = cur[t];
+    int32_t b;
+    if (pr < t0 + S) {
+      b = cur[pr - t0];
+      cur[pr - t0] = a;
+    } else {
+      const unsigned h = slot(pr);
+      b = (hkey[h] == pr) ? hval[h] : pr;
+      hkey[h] = pr;
+      hval[h] = a;
+    }
+    cur[t] = b;
+  }
+  int n = 0;
+  for (int i = 0; i < S; ++i)
+    if (cur[i] != t0 + i) {
+      dst[n] = (int32_t)(t0 + i);
+      src[n] = cur[i];
+      ++n;
+    }
+  for (int h = 0; h < H; ++h)
+    if (hkey[h] != -1 && hval[h] != hkey[h]) {
+      dst[n] = hkey[h];
+      src[n] = hval[h];
+      ++n;
+    }
+  *count = n;
+}
+
+// Apply a gather list to columns [c0a,c1a) U [c0b,c1b): read all, then write.
+__global__ void laswp_gather_kernel(double* __restrict__ a, int64_t lda, const int32_t* dst,
+                                    const int32_t* src, const int32_t* count, int64_t c0a,
+                                    int64_t c1a, int64_t c0b, int64_t c1b) {
+  __shared__ double buf[SWAP_MAX];
+  const int cnt = *count;
+  if (cnt == 0) return;
+  const int64_t na = c1a - c0a, nbb = c1b - c0b;
+  for (int64_t ci = blockIdx.x; ci < na + nbb; ci += gridDim.x) {
+    const int64_t col = ci < na ? c0a + ci : c0b + (ci - na);
+    double* colp = a + col * lda;
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) buf[e] = colp[src[e]];
+    __syncthreads();
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) colp[dst[e]] = buf[e];
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- small trsm
+// B[0:w, c] <- L^{-1} B[0:w, c] with L the unit-lower w x w block (w <= 64).
+__global__ void trsm_unit_lower_kernel(const double* __restrict__ L, int64_t ldl, int w,
+                                       double* __restrict__ B, int64_t ldb, int64_t ncols) {
+  __shared__ double sL[TRSM_W][TRSM_W + 1];
+  __shared__ double sX[TRSM_W][TRSM_C + 1];
+  const int tid = threadIdx.x;
+  const int64_t c0 = (int64_t)blockIdx.x * TRSM_C;
+  for (int i = tid; i < w * w; i += blockDim.x) {
+    const int r = i % w, c = i / w;
+    sL[r][c] = L[c * ldl + r];
+  }
+  for (int i = tid; i < w * TRSM_C; i += blockDim.x) {
+    const int r = i % w, c = i / w;
+    sX[r][c] = (c0 + c < ncols) ? B[(c0 + c) * ldb + r] : 0.0;
+  }
+  __syncthreads();
+  for (int i = 0; i < w - 1; ++i) {
+    for (int e = tid; e < (w - 1 - i) * TRSM_C; e += blockDim.x) {
+      const int r = i + 1 + e % (w - 1 - i), c = e / (w - 1 - i);
+      sX[r][c] = fma(-sL[r][i], sX[i][c], sX[r][c]);
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < w * TRSM_C; i += blockDim.x) {
+    const int r = i % w, c = i / w;
+    if (c0 + c < ncols) B[(c0 + c) * ldb + r] = sX[r][c];
+  }
+}
+
+// --------------------------------------------------------------- reductions
+__global__ void max_abs_kernel(const double* __restrict__ a, int64_t m, int64_t n, int64_t rs,
+                               int64_t cs, int upper_only, int64_t diag_off,
+                               unsigned long long* out) {
+  double mx = 0.0;
+  const int64_t total = m * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i % m, c = i / m;
+    if (upper_only && c + diag_off < r) continue;
+    mx = fmax(mx, fabs(a[r * rs + c * cs]));
+  }
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0 && mx > 0.0) atomic_max_abs(out, mx);
+}
+
+// Row-chunked GEMV partials: part[chunk][i] = sum_{j in chunk} a_ij * x_j (x=null -> 1),
+// apart[chunk][i] = sum |a_ij|.  Deterministic (fixed order, no atomics).
+constexpr int GEMV_CHUNK = 1024;
+__global__ void gemv_partial_kernel(const double* __restrict__ a, int64_t n, int64_t rs,
+                                    int64_t cs, const double* __restrict__ x,
+                                    double* __restrict__ part, double* __restrict__ apart) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t j0 = (int64_t)blockIdx.y * GEMV_CHUNK;
+  if (i >= n) return;
+  const int64_t j1 = min(n, j0 + GEMV_CHUNK);
+  double s = 0.0, sa = 0.0;
+  const double* row = a + i * rs;
+  for (int64_t j = j0; j < j1; ++j) {
+    const double v = row[j * cs];
+    s = fma(v, x ? x[j] : 1.0, s);
+    sa += fabs(v);
+  }
+  part[blockIdx.y * n + i] = s;
+  if (apart) apart[blockIdx.y * n + i] = sa;
+}
+
+// out[i] = sum_chunks part ; residual mode: r_i = out_i - b_i, reduce max|r|, max asum
+__global__ void gemv_finish_kernel(const double* __restrict__ part,
+                                   const double* __restrict__ apart, int nchunks, int64_t n,
+                                   const double* __restrict__ b, double* __restrict__ out,
+                                   unsigned long long* rmax, unsigned long long* amax) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double rr = 0.0, aa = 0.0;
+  if (i < n) {
+    double s = 0.0, sa = 0.0;
+    for (int c = 0; c < nchunks; ++c) {
+      s += part[c * n + i];
+      if (apart) sa += apart[c * n + i];
+    }
+    if (out) out[i] = s;
+    if (b) rr = fabs(s - b[i]);
+    aa = sa;
+  }
+  rr = warp_max(rr);
+  aa = warp_max(aa);
+  if ((threadIdx.x & 31) == 0) {
+    if (rmax && rr > 0.0) atomic_max_abs(rmax, rr);
+    if (amax && aa > 0.0) atomic_max_abs(amax, aa);
+  }
+}
+
+// ------------------------------------------------------------------ triangular solves
+constexpr int TRSV_B = 128;
+// x[blk] <- L_bb^{-1} x[blk] (unit lower) or U_bb^{-1} x[blk] (upper)
+__global__ void trsv_diag_kernel(const double* __restrict__ a, int64_t lda, int64_t r0, int bs,
+                                 int upper, double* __restrict__ x, int32_t* zero_diag) {
+  __shared__ double sx[TRSV_B];
+  const int r = threadIdx.x;
+  if (r < bs) sx[r] = x[r0 + r];
+  __syncthreads();
+  if (!upper) {
+    for (int i = 0; i < bs - 1; ++i) {
+      if (r > i && r < bs) sx[r] = fma(-a[(r0 + i) * lda + r0 + r], sx[i], sx[r]);
+      __syncthreads();
+    }
+  } else {
+    for (int i = bs - 1; i >= 0; --i) {
+      if (r == i) {
+        const double d = a[(r0 + i) * lda + r0 + i];
+        if (d == 0.0 && zero_diag) *zero_diag = 1;
+        sx[i] = sx[i] / d;
+      }
+      __syncthreads();
+      if (r < i) sx[r] = fma(-a[(r0 + i) * lda + r0 + r], sx[i], sx[r]);
+      __syncthreads();
+    }
+  }
+  if (r < bs) x[r0 + r] = sx[r];
+}
+
+// x[rows] -= A[rows, r0:r0+bs] x[r0:r0+bs]
+__global__ void trsv_update_kernel(const double* __restrict__ a, int64_t lda, int64_t row_lo,
+                                   int64_t row_hi, int64_t r0, int bs, double* __restrict__ x) {
+  __shared__ double sx[TRSV_B];
+  if (threadIdx.x < bs) sx[threadIdx.x] = x[r0 + threadIdx.x];
+  __syncthreads();
+  const int64_t i = row_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= row_hi) return;
+  double s = 0.0;
+  for (int j = 0; j < bs; ++j) s = fma(a[(r0 + j) * lda + i], sx[j], s);
+  x[i] -= s;
+}
+
+__global__ void gather_kernel(const double* __restrict__ b, const int64_t* __restrict__ perm,
+                              int64_t n, double* __restrict__ x) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) x[i] = b[perm[i]];
+}
+
+__global__ void copy2d_kernel(const double* __restrict__ src, int64_t rows, int64_t cols,
+                              int64_t srs, int64_t scs, double* __restrict__ dst, int64_t drs,
+                              int64_t dcs) {
+  __shared__ double tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  const bool src_rowmajor = scs == 1;
+  for (int k = ty; k < 32; k += 8) {
+    // read with the contiguous source index on threadIdx.x
+    const int64_t r = src_rowmajor ? r0 + k : r0 + tx;
+    const int64_t c = src_rowmajor ? c0 + tx : c0 + k;
+    if (r < rows && c < cols) {
+      if (src_rowmajor) tile[k][tx] = src[r * srs + c * scs];
+      else tile[tx][k] = src[r * srs + c * scs];
+    }
+  }
+  __syncthreads();
+  const bool dst_rowmajor = dcs == 1;
+  for (int k = ty; k < 32; k += 8) {
+    const int64_t r = dst_rowmajor ? r0 + k : r0 + tx;
+    const int64_t c = dst_rowmajor ? c0 + tx : c0 + k;
+    if (r < rows && c < cols) dst[r * drs + c * dcs] = dst_rowmajor ? tile[k][tx] : tile[tx][k];
+  }
+}
+
+__global__ void finalize_stats_kernel(const unsigned long long* bits, double* stats) {
+  stats[0] = __longlong_as_double((long long)bits[0]);
+  stats[1] = __longlong_as_double((long long)bits[1]);
+}
+
+// ---------------------------------------------------------------- workspace
+struct LuWs {
+  GridBar* bar;
+  double* cand;
+  int32_t* swap_dst;
+  int32_t* swap_src;
+  int32_t* swap_cnt;
+  unsigned long long* bits;  // [0] observed growth, [1] max|A|
+  void* split_aux;
+  int32_t* expA;
+  int32_t* expB;
+  int8_t* slA;
+  int8_t* slB;
+  int64_t ldK;
+};
+
+size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+
+size_t lu_ws_layout(int64_t n, int64_t nb, int k, uint8_t* base, LuWs* ws) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    uint8_t* p = base ? base + off : nullptr;
+    off += align_up(bytes);
+    return p;
+  };
+  const int sms = 1024;  // upper bound on panel CTAs
+  const int64_t ldK = round_up(nb, 16);
+  LuWs w{};
+  w.bar = reinterpret_cast<GridBar*>(take(sizeof(GridBar)));
+  w.cand = reinterpret_cast<double*>(take(sizeof(double) * 2 * sms * CAND_STRIDE));
+  w.swap_dst = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * SWAP_MAX));
+  w.swap_src = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * SWAP_MAX));
+  w.swap_cnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * 4));
+  w.bits = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * 4));
+  w.split_aux = take(64);
+  w.expA = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * n));
+  w.expB = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * n));
+  w.ldK = ldK;
+  if (k > 0) {
+    w.slA = reinterpret_cast<int8_t*>(take((size_t)k * n * ldK));
+    w.slB = reinterpret_cast<int8_t*>(take((size_t)k * n * ldK));
+  }
+  if (ws) *ws = w;
+  return off;
+}
+
+int max_abs(const double* a, int64_t m, int64_t n, int64_t rs, int64_t cs, int upper,
+            int64_t diag_off, unsigned long long* out, cudaStream_t st) {
+  if (m <= 0 || n <= 0) return OZ_OK;
+  int64_t blocks = ceil_div(m * n, 256);
+  if (blocks > sm_count() * 8) blocks = sm_count() * 8;
+  max_abs_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, m, n, rs, cs, upper, diag_off, out);
+  OZ_CHECK_LAUNCH();
+  return OZ_OK;
+}
+
+int apply_swaps(double* a, int64_t lda, const int32_t* ipiv, int64_t t0, int S, const LuWs& ws,
+                int64_t c0a, int64_t c1a, int64_t c0b, int64_t c1b, cudaStream_t st) {
+  if (S <= 0) return OZ_OK;
+  compose_swaps_kernel<<<1, 256, 0, st>>>(ipiv, t0, S, ws.swap_dst, ws.swap_src, ws.swap_cnt);
+  OZ_CHECK_LAUNCH();
+  const int64_t ncols = (c1a - c0a) + (c1b - c0b);
+  if (ncols <= 0) return OZ_OK;
+  int64_t blocks = ncols < sm_count() * 8 ? ncols : sm_count() * 8;
+  laswp_gather_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, lda, ws.swap_dst, ws.swap_src,
+                                                        ws.swap_cnt, c0a, c1a, c0b, c1b);
+  OZ_CHECK_LAUNCH();
+  return OZ_OK;
+}
+
+// U12 <- L11^{-1} A12 for L11 (jb x jb, unit lower) at a[j,j], A12 = rows j..j+jb, ncols
+int trsm_blocked(double* a, int64_t lda, int64_t j, int64_t jb, double* b, int64_t ldb,
+                 int64_t ncols, cudaStream_t st) {
+  if (ncols <= 0) return OZ_OK;
+  for (int64_t i = 0; i < jb; i += TRSM_W) {
+    const int w = (int)(jb - i < TRSM_W ? jb - i : TRSM_W);
+    const double* L = a + (j + i) * lda + (j + i);
+    trsm_unit_lower_kernel<<<(unsigned)ceil_div(ncols, TRSM_C), 256, 0, st>>>(L, lda, w, b + i, ldb,
+                                                                          ncols);
+    OZ_CHECK_LAUNCH();
+    const int64_t below = jb - i - w;
+    if (below > 0)
+      OZ_TRY(dgemm(0, 0, below, ncols, w, -1.0, a + (j + i) * lda + (j + i + w), lda, b + i, ldb,
+                   1.0, b + i + w, ldb, st));
+  }
+  return OZ_OK;
+}
+
+int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int32_t* ipiv,
+                 int32_t* info, const LuWs& ws, cudaStream_t st) {
+  static int max_smem = 0;
+  if (!max_smem) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    OZ_CHECK_CUDA(cudaFuncSetAttribute(panel_window_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       max_smem - (int)sizeof(PanelShared) - 1024));
+  }
+  const int sms = sm_count();
+  const size_t cap = (size_t)max_smem - sizeof(PanelShared) - 1024;
+  int G = (int)ceil_div(m, 256);
+  if (G > sms) G = sms;
+  if (G < 1) G = 1;
+  int R = (int)ceil_div(m, G);
+  while (panel_smem_bytes(w, R) > cap) {
+    OZ_REQUIRE(G < sms, OZ_UNSUPPORTED, "panel of %lld rows x %d cols does not fit on chip",
+               (long long)m, w);
+    ++G;
+    R = (int)ceil_div(m, G);
+  }
+  G = (int)ceil_div(m, R);
+  PanelArgs pa;
+  pa.a = a;
+  pa.lda = lda;
+  pa.r0 = r0;
+  pa.m = m;
+  pa.w = w;
+  pa.rows_per_cta = R;
+  pa.ipiv = ipiv;
+  pa.growth = ws.bits;
+  pa.info = info;
+  pa.bar = ws.bar;
+  pa.cand = ws.cand;
+  void* args[] = {&pa};
+  OZ_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)panel_window_kernel, dim3(G),
+                                            dim3(PANEL_THREADS), args, panel_smem_bytes(w, R),
+                                            st));
+  return OZ_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------- LU driver
+int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k, int q,
+              int npairs, const int32_t* pa, const int32_t* pb, const int32_t* ps,
+              int32_t* ipiv, double* stats, int32_t* info, void* workspace, size_t ws_bytes,
+              cudaStream_t st) {
+  OZ_REQUIRE(n >= 1, OZ_INVALID_PARAMS, "empty matrices are not supported");
+  OZ_REQUIRE(nb >= 1 && nb <= n, OZ_INVALID_PARAMS, "lu_block must be in 1..%lld, got %lld",
+             (long long)n, (long long)nb);
+  OZ_REQUIRE(nb <= SWAP_MAX / 2, OZ_UNSUPPORTED, "lu_block > %d not supported", SWAP_MAX / 2);
+  OZ_REQUIRE(lda >= n, OZ_INVALID_PARAMS, "lda < n");
+  OZ_REQUIRE(backend == 0 || backend == 1, OZ_INVALID_PARAMS, "bad backend");
+  LuWs ws;
+  const size_t need = lu_ws_layout(n, nb, backend == 1 ? k : 0, (uint8_t*)workspace, &ws);
+  OZ_REQUIRE(ws_bytes >= need, OZ_INVALID_PARAMS, "workspace too small (%zu < %zu)", ws_bytes,
+             need);
+  OZ_CHECK_CUDA(cudaMemsetAsync(ws.bar, 0, sizeof(GridBar), st));
+  OZ_CHECK_CUDA(cudaMemsetAsync(ws.bits, 0, 4 * sizeof(unsigned long long), st));
+  OZ_CHECK_CUDA(cudaMemsetAsync(info, 0, sizeof(int32_t), st));
+  OZ_TRY(max_abs(a, n, n, 1, lda, 0, 0, ws.bits + 1, st));
+
+  for (int64_t j = 0; j < n; j += nb) {
+    const int64_t jb = nb < n - j ? nb : n - j;
+    // ---- panel (columns j..j+jb) in windows of <= PANEL_W columns
+    for (int64_t jj = j; jj < j + jb; jj += PANEL_W) {
+      const int w = (int)((j + jb - jj) < PANEL_W ? (j + jb - jj) : PANEL_W);
+      OZ_TRY(panel_window(a, lda, jj, n - jj, w, ipiv, info, ws, st));
+      // interchanges of this window on all panel columns (the window's own included)
+      OZ_TRY(apply_swaps(a, lda, ipiv, jj, w, ws, j, j + jb, 0, 0, st));
+      const int64_t rest = j + jb - (jj + w);
+      if (rest > 0) {
+        OZ_TRY(trsm_blocked(a, lda, jj, w, a + (jj + w) * lda + jj, lda, rest, st));
+        const int64_t below = n - jj - w;
+        if (below > 0)
+          OZ_TRY(dgemm(0, 0, below, rest, w, -1.0, a + jj * lda + jj + w, lda,
+                       a + (jj + w) * lda + jj, lda, 1.0, a + (jj + w) * lda + jj + w, lda, st));
+      }
+    }
+    // ---- panel interchanges on the columns outside the panel (whole-row swaps, :80-82)
+    OZ_TRY(apply_swaps(a, lda, ipiv, j, (int)jb, ws, 0, j, j + jb, n, st));
+    const int64_t rest = n - j - jb;
+    if (rest > 0) {
+      double* a12 = a + (j + jb) * lda + j;
+      double* a21 = a + j * lda + (j + jb);
+      double* a22 = a + (j + jb) * lda + (j + jb);
+      OZ_TRY(trsm_blocked(a, lda, j, jb, a12, lda, rest, st));  // solve.py:123-127
+      if (backend == 0) {                                         // solve.py:130-134 native
+        OZ_TRY(dgemm(0, 0, rest, rest, jb, -1.0, a21, lda, a12, lda, 1.0, a22, lda, st));
+        OZ_TRY(max_abs(a22, rest, rest, 1, lda, 0, 0, ws.bits, st));
+      } else {                                                    // emulated Schur update
+        const int64_t sst = rest * ws.ldK;
+        OZ_TRY(split_launch(a21, rest, jb, 1, lda, OZ_ROW_SCALED, OZ_PER_VECTOR, k, q, ws.slA,
+                            ws.ldK, sst, ws.expA, ws.split_aux, st));
+        OZ_TRY(split_launch(a12, jb, rest, 1, lda, OZ_COL_SCALED, OZ_PER_VECTOR, k, q, ws.slB,
+                            ws.ldK, sst, ws.expB, ws.split_aux, st));
+        OZ_TRY(gemm_emu_launch(rest, rest, jb, ws.slA, ws.ldK, sst, k, ws.expA, ws.slB, ws.ldK,
+                               sst, k, ws.expB, npairs, pa, pb, ps, -1.0, 1.0, a22, lda, 1,
+                               ws.bits, st));
+      }
+    }
+    // finalized U rows of this panel: triu(lu[j:j+jb, j:]) (solve.py:135-137)
+    OZ_TRY(max_abs(a + j * lda + j, jb, n - j, 1, lda, 1, 0, ws.bits, st));
+  }
+  finalize_stats_kernel<<<1, 1, 0, st>>>(ws.bits, stats);
+  OZ_CHECK_LAUNCH();
+  return OZ_OK;
+}
+
+int lu_solve(const double* lu, int64_t n, int64_t lda, const int64_t* perm, const double* b,
+             double* x, int32_t* flag, cudaStream_t st) {
+  gather_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(b, perm, n, x);
+  OZ_CHECK_LAUNCH();
+  // forward: unit lower
+  for (int64_t r0 = 0; r0 < n; r0 += TRSV_B) {
+    const int bs = (int)(n - r0 < TRSV_B ? n - r0 : TRSV_B);
+    trsv_diag_kernel<<<1, TRSV_B, 0, st>>>(lu, lda, r0, bs, 0, x, flag);
+    OZ_CHECK_LAUNCH();
+    const int64_t lo = r0 + bs;
+    if (lo < n) {
+      trsv_update_kernel<<<(unsigned)ceil_div(n - lo, 256), 256, 0, st>>>(lu, lda, lo, n, r0, bs,
+                                                                           x);
+      OZ_CHECK_LAUNCH();
+    }
+  }
+  // backward: upper
+  const int64_t nblk = ceil_div(n, TRSV_B);
+  for (int64_t bi = nblk - 1; bi >= 0; --bi) {
+    const int64_t r0 = bi * TRSV_B;
+    const int bs = (int)(n - r0 < TRSV_B ? n - r0 : TRSV_B);
+    trsv_diag_kernel<<<1, TRSV_B, 0, st>>>(lu, lda, r0, bs, 1, x, flag);
+    OZ_CHECK_LAUNCH();
+    if (r0 > 0) {
+      trsv_update_kernel<<<(unsigned)ceil_div(r0, 256), 256, 0, st>>>(lu, lda, 0, r0, r0, bs, x);
+      OZ_CHECK_LAUNCH();
+    }
+  }
+  return OZ_OK;
+}
+
+int gemv_rows(const double* a, int64_t n, int64_t rs, int64_t cs, const double* x,
+              const double* b, double* out, unsigned long long* rmax, unsigned long long* amax,
+              double* part, cudaStream_t st) {
+  const int nchunks = (int)ceil_div(n, GEMV_CHUNK);
+  double* apart = amax ? part + (size_t)nchunks * n : nullptr;
+  dim3 grid((unsigned)ceil_div(n, 128), (unsigned)nchunks);
+  gemv_partial_kernel<<<grid, 128, 0, st>>>(a, n, rs, cs, x, part, apart);
+  OZ_CHECK_LAUNCH();
+  gemv_finish_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(part, apart, nchunks, n, b, out,
+                                                                 rmax, amax);
+  OZ_CHECK_LAUNCH();
+  return OZ_OK;
+}
+
+}  // namespace oz
+
+// ======================================================================= C ABI
+extern "C" size_t oz_lu_workspace_bytes(int64_t n, int64_t nb, int num_slices) {
+  return oz::lu_ws_layout(n, nb, num_slices, nullptr, nullptr);
+}
+
+extern "C" int oz_lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend,
+                            int num_slices, int slice_bits, int npairs, const int32_t* pair_a,
+                            const int32_t* pair_b, const int32_t* pair_shift, int32_t* ipiv,
+                            double* stats, int32_t* info, void* workspace, size_t ws_bytes,
+                            void* stream) {
+  return oz::lu_factor(a, n, lda, nb, backend, num_slices, slice_bits, npairs, pair_a, pair_b,
+                       pair_shift, ipiv, stats, info, workspace, ws_bytes, oz::as_stream(stream));
+}
+
+extern "C" size_t oz_lu_solve_workspace_bytes(int64_t n) { return 256; }
+
+extern "C" int oz_lu_solve(const double* lu, int64_t n, int64_t lda, const int64_t* perm,
+                           const double* b, double* x, void* workspace, size_t ws_bytes,
+                           void* stream) {
+  OZ_REQUIRE(ws_bytes >= 4, OZ_INVALID_PARAMS, "workspace too small");
+  OZ_CHECK_CUDA(cudaMemsetAsync(workspace, 0, 4, oz::as_stream(stream)));
+  return oz::lu_solve(lu, n, lda, perm, b, x, reinterpret_cast<int32_t*>(workspace),
+                      oz::as_stream(stream));
+}
+
+extern "C" int oz_residual_norms(const double* a, int64_t n, int64_t row_stride,
+                                 int64_t col_stride, const double* x, const double* b,
+                                 double* out, void* stream) {
+  using namespace oz;
+  cudaStream_t st = as_stream(stream);
+  const int nchunks = (int)ceil_div(n, GEMV_CHUNK);
+  double* part = nullptr;
+  unsigned long long* bits = nullptr;
+  OZ_CHECK_CUDA(cudaMallocAsync(&part, sizeof(double) * 2 * nchunks * n, st));
+  OZ_CHECK_CUDA(cudaMallocAsync(&bits, sizeof(unsigned long long) * 4, st));
+  OZ_CHECK_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned long long) * 4, st));
+  int s = gemv_rows(a, n, row_stride, col_stride, x, b, nullptr, bits, bits + 1, part, st);
+  if (s == OZ_OK) s = max_abs(x, n, 1, 1, 1, 0, 0, bits + 2, st);
+  if (s == OZ_OK) s = max_abs(b, n, 1, 1, 1, 0, 0, bits + 3, st);
+  if (s == OZ_OK) {
+    OZ_CHECK_CUDA(cudaMemcpyAsync(out, bits, sizeof(double) * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  cudaFreeAsync(part, st);
+  cudaFreeAsync(bits, st);
+  return s;
+}
+
+extern "C" int oz_row_sums(const double* a, int64_t n, int64_t row_stride, int64_t col_stride,
+                           double* out, void* stream) {
+  using namespace oz;
+  cudaStream_t st = as_stream(stream);
+  const int nchunks = (int)ceil_div(n, GEMV_CHUNK);
+  double* part = nullptr;
+  OZ_CHECK_CUDA(cudaMallocAsync(&part, sizeof(double) * nchunks * n, st));
+  int s = gemv_rows(a, n, row_stride, col_stride, nullptr, nullptr, out, nullptr, nullptr, part,
+                    st);
+  cudaFreeAsync(part, st);
+  return s;
+}
+
+extern "C" int oz_max_abs(const double* a, int64_t m, int64_t n, int64_t row_stride,
+                          int64_t col_stride, double* out, void* stream) {
+  using namespace oz;
+  cudaStream_t st = as_stream(stream);
+  OZ_CHECK_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
+  return max_abs(a, m, n, row_stride, col_stride, 0, 0,
+                 reinterpret_cast<unsigned long long*>(out), st);
+}
+
+extern "C" int oz_copy2d(const double* src, int64_t rows, int64_t cols, int64_t src_rs,
+                         int64_t src_cs, double* dst, int64_t dst_rs, int64_t dst_cs,
+                         void* stream) {
+  using namespace oz;
+  if (rows <= 0 || cols <= 0) return OZ_OK;
+  dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32));
+  copy2d_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(src, rows, cols, src_rs, src_cs, dst,
+                                                            dst_rs, dst_cs);
+  OZ_CHECK_LAUNCH();
+  return OZ_OK;
+}

@@ -1,0 +1,138 @@
+"""GPU parity: split kernel and tcgen05 emulated GEMM vs the reference.
+
+Golden fixtures come from the reference itself (oracle/make_golden.py); the
+larger cases are checked against the CPU oracle restatement on the same seeded
+inputs.  The bar is bit-exactness (np.array_equal) for slices, exponents,
+per-pair INT32 products and the emulated GEMM output.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import ozaki_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _pkg():
+    import paper_2509_23565_b200 as oz
+    return oz
+
+
+def test_split_matches_reference_golden():
+    oz = _pkg()
+    g = load_golden("split")
+    for i in range(int(g["count"][0])):
+        k, q, orient, mode = (int(v) for v in g[f"s{i}_meta"])
+        st = oz.split_matrix(g[f"s{i}_a"], k, q,
+                             oz.Orientation.COL_SCALED if orient else oz.Orientation.ROW_SCALED,
+                             oz.ScalingMode.GLOBAL if mode else oz.ScalingMode.PER_VECTOR)
+        assert np.array_equal(np.stack(st.slices), g[f"s{i}_slices"]), i
+        assert np.array_equal(st.exponents, g[f"s{i}_exps"]), i
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (7, 300), (300, 7), (129, 1000), (2048, 96)])
+@pytest.mark.parametrize("orient", ["row", "col"])
+def test_split_matches_oracle_random(shape, orient):
+    oz = _pkg()
+    rng = np.random.default_rng(hash((shape, orient)) % 2**32)
+    a = (rng.random(shape) - 0.5) * np.ldexp(1.0, rng.integers(-70, 71, size=(shape[0], 1)))
+    for k in (1, 7, 12):
+        st = oz.split_matrix(a, k, 7, oz.Orientation.ROW_SCALED if orient == "row"
+                             else oz.Orientation.COL_SCALED)
+        ref_s, ref_e = orc.split(a, k, 7, orient)
+        assert np.array_equal(np.stack(st.slices), ref_s)
+        assert np.array_equal(st.exponents, ref_e)
+
+
+def test_split_nonfinite_raises():
+    oz = _pkg()
+    with pytest.raises(oz.NonFiniteEntryError):
+        oz.split_matrix(np.array([[np.nan, 1.0]]), 2)
+    with pytest.raises(oz.NonFiniteEntryError):
+        oz.split_matrix(np.array([[np.inf], [1.0]]), 2, orientation=oz.Orientation.COL_SCALED)
+
+
+@pytest.mark.parametrize("m,n,kk", [(1, 1, 1), (128, 128, 128), (129, 257, 300), (300, 100, 1000),
+                                    (64, 512, 4096), (1000, 700, 33)])
+def test_pair_product_int32_exact(m, n, kk):
+    """Per-slice-pair INT32 products are exact (test_gemm.py:218-240 pattern)."""
+    import torch
+    from paper_2509_23565_b200 import _lib
+    rng = np.random.default_rng(m * 7 + n * 13 + kk)
+    a = rng.integers(-127, 128, size=(m, kk), dtype=np.int8)
+    b = rng.integers(-127, 128, size=(n, kk), dtype=np.int8)
+    ld = -(-kk // 16) * 16
+    da = torch.zeros((m, ld), dtype=torch.int8, device="cuda")
+    db = torch.zeros((n, ld), dtype=torch.int8, device="cuda")
+    da[:, :kk] = torch.from_numpy(a).cuda()
+    db[:, :kk] = torch.from_numpy(b).cuda()
+    out = torch.zeros((n, m), dtype=torch.int32, device="cuda")  # column-major m x n
+    _lib.call("oz_gemm_pair_i32", m, n, kk, da.data_ptr(), ld, db.data_ptr(), ld,
+              out.data_ptr(), m, torch.cuda.current_stream().cuda_stream)
+    got = out.cpu().numpy().T
+    want = a.astype(np.int64) @ b.astype(np.int64).T
+    assert np.array_equal(got.astype(np.int64), want)
+
+
+def test_gemm_matches_reference_golden():
+    oz = _pkg()
+    g = load_golden("gemm")
+    for i in range(int(g["count"][0])):
+        k, limit, mode = (int(v) for v in g[f"g{i}_meta"])
+        alpha, beta = (float(v) for v in g[f"g{i}_ab"])
+        trunc = oz.FULL if limit == 2 * k else oz.Band(limit)
+        bk = oz.GemmBackend.int8(k, 7, truncation=trunc,
+                                 scaling=oz.ScalingMode.GLOBAL if mode else
+                                 oz.ScalingMode.PER_VECTOR)
+        c = g[f"g{i}_c"]
+        out = oz.gemm(bk, alpha, g[f"g{i}_a"], g[f"g{i}_b"], beta, c if c.size else None)
+        assert np.array_equal(out, g[f"g{i}_out"]), (i, k, limit)
+
+
+def test_schur_calls_match_reference_golden():
+    """The 9 Schur updates of the reference LU on ParaWilk_256 (k=3,7,9), bit-exact."""
+    oz = _pkg()
+    g = load_golden("schur")
+    for i in range(int(g["count"][0])):
+        k = int(g[f"c{i}_k"][0])
+        out = oz.gemm(oz.GemmBackend.int8(k), -1.0, g[f"c{i}_a"], g[f"c{i}_b"], 1.0,
+                      g[f"c{i}_c"])
+        assert np.array_equal(out, g[f"c{i}_out"]), (i, k)
+
+
+@pytest.mark.parametrize("k", [3, 6, 7, 9])
+def test_gemm_matches_oracle_larger(k):
+    oz = _pkg()
+    rng = np.random.default_rng(k)
+    a = rng.random((700, 1200)) - 0.5
+    b = rng.random((1200, 530)) - 0.5
+    out = oz.gemm(oz.GemmBackend.int8(k), 1.0, a, b, 0.0)
+    assert np.array_equal(out, orc.gemm(1.0, a, b, 0.0, k=k))
+
+
+def test_gemm_device_tensors_and_layouts():
+    import torch
+    oz = _pkg()
+    rng = np.random.default_rng(3)
+    a = rng.random((300, 257)) - 0.5
+    b = rng.random((257, 190)) - 0.5
+    c = rng.random((300, 190)) - 0.5
+    want = orc.gemm(-1.0, a, b, 1.0, c, k=7)
+    da = torch.from_numpy(a).cuda()
+    db = torch.from_numpy(b).cuda().t().contiguous().t()   # column-major view
+    dc = torch.from_numpy(c).cuda()
+    out = oz.gemm(oz.GemmBackend.int8(7), -1.0, da, db, 1.0, dc)
+    assert out.is_cuda
+    assert np.array_equal(out.cpu().numpy(), want)
+    assert np.array_equal(dc.cpu().numpy(), c)   # inputs never mutated
+
+
+def test_gemm_native_close():
+    oz = _pkg()
+    rng = np.random.default_rng(4)
+    a, b, c = rng.random((64, 80)) - 0.5, rng.random((80, 50)) - 0.5, rng.random((64, 50)) - 0.5
+    out = oz.gemm(oz.GemmBackend.native(), -1.0, a, b, 1.0, c)
+    scale = np.abs(a) @ np.abs(b) + np.abs(c)
+    assert (np.abs(out - (c - a @ b)) <= 4 * 2.0**-52 * scale).all()
