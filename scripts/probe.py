@@ -1,0 +1,61 @@
+"""Developer probe: time the emulated GEMM / LU on device-resident inputs."""
+import sys, time, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_2509_23565_b200 as oz
+from paper_2509_23565_b200 import _lib, _dev
+from paper_2509_23565_b200.gemm import emulated_into
+from paper_2509_23565_b200.matgen import generate_device
+from paper_2509_23565_b200.solve import factor_device, _col_major_copy
+
+
+def timeit(fn, reps=3):
+    fn(); torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 1e9
+    for _ in range(reps):
+        s.record(); fn(); e.record(); torch.cuda.synchronize()
+        best = min(best, s.elapsed_time(e) / 1e3)
+    return best
+
+
+def gemm_probe(n, ks):
+    a = generate_device(0, n, seed=2)
+    b = generate_device(0, n, seed=3)
+    out = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    fl = 2.0 * n**3
+    t = timeit(lambda: _lib.call("oz_dgemm", 0, 0, n, n, n, 1.0, b.data_ptr(), n, a.data_ptr(), n,
+                                 0.0, out.data_ptr(), n, _dev.stream()))
+    print(f"gemm n={n} native cuBLAS DGEMM: {t*1e3:.2f} ms  {fl/t/1e12:.2f} TFLOP/s", flush=True)
+    for k in ks:
+        bk = oz.GemmBackend.int8(k)
+        np_ = k * (k + 1) // 2
+        t = timeit(lambda: emulated_into(bk, a, b, 1.0, 0.0, out, False))
+        print(f"gemm n={n} k={k} pairs={np_}: {t*1e3:.2f} ms  {fl/t/1e12:.2f} TFLOP/s-eq  "
+              f"int8 {np_*fl/t/1e15:.3f} POPS", flush=True)
+
+
+def lu_probe(n, nb, backends):
+    for name, bk in backends:
+        a = generate_device(0, n, seed=99, layout="F")
+        work = a.clone()
+        def run():
+            work.copy_(a)
+            return factor_device(work, nb, bk)
+        run(); torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(); r = run(); e.record(); torch.cuda.synchronize()
+        t = s.elapsed_time(e) / 1e3
+        print(f"lu n={n} nb={nb} {name}: {t*1e3:.1f} ms  {2*n**3/3/t/1e12:.2f} TFLOP/s-eq "
+              f"info={int(r[2].item())}", flush=True)
+
+
+if __name__ == "__main__":
+    what = sys.argv[1]
+    if what == "gemm":
+        gemm_probe(int(sys.argv[2]), [int(k) for k in sys.argv[3].split(",")])
+    else:
+        n, nb = int(sys.argv[2]), int(sys.argv[3])
+        lu_probe(n, nb, [("fp64", oz.GemmBackend.native()), ("k7", oz.GemmBackend.int8(7)),
+                         ("k6", oz.GemmBackend.int8(6))])

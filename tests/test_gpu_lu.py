@@ -1,0 +1,171 @@
+"""GPU parity: generators, LU factor/solve and the HPL scaled residual.
+
+Bars:
+  * generators: bit-exact with numpy's PCG64 stream (golden fixtures);
+  * unblocked LU (lu_block = n <= 64): bit-exact factors, pivots and growth;
+  * blocked LU: identical pivots, factors within 2^-40 (test_solve.py:61-66);
+  * residual table on ParaWilk_256(4,15,1/2): identical verdicts, each entry
+    within 2x of the reference oracle on the same matrix.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _oz():
+    import paper_2509_23565_b200 as oz
+    return oz
+
+
+def test_generators_bit_exact():
+    oz = _oz()
+    g = load_golden("matgen")
+    assert np.array_equal(
+        oz.parawilk_randomized(oz.ParaWilkParams(40, 3, 7, 0.5, randomize=True, seed=9)), g["pw40"])
+    assert np.array_equal(oz.parawilk(oz.ParaWilkParams(5, 4, 2, 1.0)), g["pw5_det"])
+    assert np.array_equal(oz.hpl_uniform(64, 99), g["uni64"])
+    big = oz.hpl_uniform(2048, 7)
+    assert np.array_equal(big.ravel()[g["uni2048_seed7_pos"]], g["uni2048_seed7_val"])
+    assert np.array_equal(
+        oz.parawilk_randomized(oz.ParaWilkParams(256, 4, 15, 0.5, randomize=True, seed=42)),
+        g["pw256_seed42"])
+
+
+def test_generator_layouts_agree():
+    import torch
+    from paper_2509_23565_b200.matgen import generate_device
+    for kind in (0, 2):
+        c = generate_device(kind, 333, seed=5, depth=3, block=7, alpha=0.25, layout="C")
+        f = generate_device(kind, 333, seed=5, depth=3, block=7, alpha=0.25, layout="F")
+        assert f.stride() == (1, 333)
+        assert torch.equal(c, f)
+
+
+def test_generator_sampled_at_scale():
+    """Sampled stream positions of a large U(-1/2,1/2) draw match the PCG64 restatement."""
+    from oracle import ozaki_oracle as orc
+    from paper_2509_23565_b200.matgen import generate_device
+    n = 20000
+    a = generate_device(0, n, seed=99)
+    rng = np.random.default_rng(1)
+    for idx in list(rng.integers(0, n * n, size=20)) + [0, n * n - 1]:
+        i, j = divmod(int(idx), n)
+        assert float(a[i, j]) == orc.pcg64_uniform_at(99, int(idx)) - 0.5
+
+
+def test_unblocked_lu_bit_exact():
+    oz = _oz()
+    g = load_golden("lu")
+    f = oz.lu_factor(g["unblocked_a"], 24)
+    assert np.array_equal(f.pivots, g["unblocked_perm"])
+    assert np.array_equal(f.lu, g["unblocked_lu"])
+    assert f.growth == float(g["unblocked_growth"][0])
+
+
+def test_blocked_lu_close():
+    oz = _oz()
+    g = load_golden("lu")
+    f = oz.lu_factor(g["blocked_a"], 16)
+    assert np.array_equal(f.pivots, g["blocked_perm"])
+    assert np.abs(f.lu - g["blocked_lu"]).max() <= 2.0**-40
+
+
+def test_wilkinson_growth():
+    oz = _oz()
+    g = load_golden("lu")
+    for n in range(5, 21):
+        f = oz.lu_factor(oz.wilkinson(n), min(4, n))
+        assert f.growth == 2.0 ** (n - 1) == float(g[f"wilkinson_{n}_growth"][0])
+
+
+@pytest.mark.parametrize("n,nb", [(40, 8), (100, 7), (257, 64), (700, 128), (1500, 300)])
+def test_factorization_reconstructs(n, nb):
+    oz = _oz()
+    a = np.random.default_rng(n).random((n, n)) - 0.5
+    f = oz.lu_factor(a, nb)
+    l = np.tril(f.lu, -1) + np.eye(n)
+    u = np.triu(f.lu)
+    assert np.allclose(l @ u, a[f.pivots], atol=1e-12 * n)
+    assert np.abs(np.tril(f.lu, -1)).max() <= 1.0
+    # same pivots as the unblocked CPU oracle on a generic matrix
+    from oracle import ozaki_oracle as orc
+    _, perm, _ = orc.lu_factor(a, nb)
+    assert np.array_equal(f.pivots, perm)
+
+
+def test_singular_and_validation():
+    oz = _oz()
+    a = np.ones((3, 3))
+    a[:, 0] = 0.0
+    with pytest.raises(oz.SingularPivotError):
+        oz.lu_factor(a, 1)
+    with pytest.raises(oz.NonSquareError):
+        oz.lu_factor(np.ones((2, 3)), 1)
+    for nb in (0, -1, 5):
+        with pytest.raises(oz.InvalidParamsError):
+            oz.lu_factor(np.eye(4), nb)
+    f = oz.lu_factor(np.random.default_rng(0).random((4, 4)), 2)
+    with pytest.raises(ValueError):
+        f.lu[0, 0] = 0.0
+
+
+def test_solve_small_and_norms():
+    oz = _oz()
+    b = np.random.default_rng(1).random(5)
+    f = oz.lu_factor(np.eye(5), 2)
+    assert np.array_equal(oz.lu_solve(f, b), b)
+    f = oz.lu_factor(np.array([[2.0, 0.0], [0.0, 4.0]]), 1)
+    assert np.array_equal(oz.lu_solve(f, np.array([2.0, 8.0])), np.array([1.0, 2.0]))
+    rep = oz.scaled_residual(np.array([[1.0, -2.0], [3.0, 4.0]]), np.array([1.0, -5.0]),
+                             np.array([0.5, 2.0]))
+    assert (rep.norm_a_inf, rep.norm_x_inf, rep.norm_b_inf) == (7.0, 5.0, 2.0)
+    for backend in (oz.GemmBackend.native(), oz.GemmBackend.int8(3)):
+        x, rep = oz.solve_system(np.eye(8), np.ones(8), 2, backend)
+        assert rep.scaled_residual == 0.0 and rep.passed
+        assert np.array_equal(x, np.ones(8))
+
+
+def test_parawilk256_residual_table():
+    """Paper table: fail k<=6, pass k>=7, each within 2x of the oracle."""
+    oz = _oz()
+    g = load_golden("residual")
+    ks = list(g["parawilk256_splits"])
+    ref = list(g["parawilk256_resid"])
+    a = oz.parawilk_randomized(oz.ParaWilkParams(256, 4, 15, 0.5, randomize=True, seed=42))
+    b = a @ np.ones(256)
+    for k, r in zip(ks, ref):
+        bk = oz.GemmBackend.native() if k == 0 else oz.GemmBackend.int8(int(k))
+        _, rep = oz.solve_system(a, b, 64, bk)
+        assert rep.passed == (r < 16.0), (k, rep.scaled_residual, r)
+        assert 0.5 <= rep.scaled_residual / r <= 2.0, (k, rep.scaled_residual, r)
+
+
+@pytest.mark.parametrize("n", [256, 512, 1024])
+def test_uniform_residuals_vs_oracle(n):
+    oz = _oz()
+    g = load_golden("residual")
+    ref = g[f"uniform{n}_resid"]
+    a = oz.hpl_uniform(n, 99)
+    b = a @ np.ones(n)
+    for bk, r in zip((oz.GemmBackend.native(), oz.GemmBackend.int8(6), oz.GemmBackend.int8(7)),
+                     ref):
+        _, rep = oz.solve_system(a, b, 64, bk)
+        assert rep.passed == (r < 16.0), (bk.describe(), rep.scaled_residual, r)
+        assert 0.5 <= rep.scaled_residual / r <= 2.0, (bk.describe(), rep.scaled_residual, r)
+
+
+def test_uniform_2048_nb256_verdicts():
+    """n=2048, nb=256 -> fp64 0.0101, k=6 65.1 (fail), k=7 0.597."""
+    oz = _oz()
+    a = oz.hpl_uniform(2048, 99)
+    b = a @ np.ones(2048)
+    res = {}
+    for name, bk in (("fp64", oz.GemmBackend.native()), ("k6", oz.GemmBackend.int8(6)),
+                     ("k7", oz.GemmBackend.int8(7))):
+        res[name] = oz.solve_system(a, b, 256, bk)[1].scaled_residual
+    assert res["fp64"] < 1.0 and res["k7"] < 16.0 and res["k6"] >= 16.0, res
+    assert 0.5 <= res["k6"] / 65.12 <= 2.0 and 0.5 <= res["k7"] / 0.5967 <= 2.0, res
