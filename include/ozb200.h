@@ -56,6 +56,14 @@ enum oz_gen_kind {
 
 const char* oz_last_error(void);
 int oz_version(void);
+/* Number of kernels this library has launched (process-wide, monotone). */
+long long oz_launch_count(void);
+/* Per-phase CUDA-event timing: enable (and clear) / read.  summary writes
+ * 8 kinds x {total ms, launches, algorithmic work}; kinds: 0 emulated GEMM
+ * (work = INT8 ops), 1 panel, 2 cuBLAS DGEMM (flops), 3 split (bytes),
+ * 4 laswp, 5 trsm, 6 solve, 7 other. */
+int oz_prof_enable(int on);
+int oz_prof_summary(double* out);
 /* Number of SMs of the current device (used by host-side schedulers). */
 int oz_sm_count(int* out);
 

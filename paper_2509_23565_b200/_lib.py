@@ -26,6 +26,9 @@ _u64 = C.c_uint64
 # name -> argtypes (restype is always int status unless listed in _RESTYPES)
 _SIGNATURES = {
     "oz_version": [],
+    "oz_launch_count": [],
+    "oz_prof_enable": [_int],
+    "oz_prof_summary": [_vp],
     "oz_sm_count": [_vp],
     "oz_split_aux_bytes": [],
     "oz_split": [_vp, _i64, _i64, _i64, _i64, _int, _int, _int, _int, _vp, _i64, _i64, _vp, _vp,
@@ -47,6 +50,7 @@ _SIGNATURES = {
     "oz_copy2d": [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _vp],
 }
 _RESTYPES = {
+    "oz_launch_count": C.c_longlong,
     "oz_split_aux_bytes": C.c_size_t,
     "oz_lu_workspace_bytes": C.c_size_t,
     "oz_lu_solve_workspace_bytes": C.c_size_t,

@@ -4,8 +4,10 @@
 #include <cublas_v2.h>
 #include <stdarg.h>
 
+#include <atomic>
 #include <mutex>
 #include <unordered_map>
+#include <vector>
 
 #include "common.cuh"
 
@@ -21,6 +23,44 @@ void set_error(const char* fmt, ...) {
 }
 
 const char* last_error() { return g_err; }
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+struct ProfEntry {
+  cudaEvent_t a = nullptr, b = nullptr;
+  int kind = 0;
+  double work = 0.0;
+  bool done = false;
+};
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<ProfEntry> g_prof;
+static size_t g_prof_used = 0;
+
+int prof_start(cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (!g_prof_on) return -1;
+  if (g_prof_used == g_prof.size()) {
+    ProfEntry e;
+    if (cudaEventCreate(&e.a) != cudaSuccess || cudaEventCreate(&e.b) != cudaSuccess) return -1;
+    g_prof.push_back(e);
+  }
+  const int tag = (int)g_prof_used++;
+  g_prof[tag].done = false;
+  cudaEventRecord(g_prof[tag].a, st);
+  return tag;
+}
+
+void prof_stop(int tag, cudaStream_t st, int kind, double work) {
+  if (tag < 0) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  ProfEntry& e = g_prof[tag];
+  cudaEventRecord(e.b, st);
+  e.kind = kind;
+  e.work = work;
+  e.done = true;
+}
 
 int sm_count() {
   static std::mutex mu;
@@ -72,6 +112,35 @@ int dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha,
 extern "C" const char* oz_last_error(void) { return oz::last_error(); }
 
 extern "C" int oz_version(void) { return 100; }
+
+extern "C" long long oz_launch_count(void) { return oz::g_launches.load(); }
+
+extern "C" int oz_prof_enable(int on) {
+  std::lock_guard<std::mutex> lk(oz::g_prof_mu);
+  oz::g_prof_on = on != 0;
+  oz::g_prof_used = 0;
+  return OZ_OK;
+}
+
+// Per kind: out[3*kind + {0,1,2}] = {total ms, launches, total work}; syncs events.
+extern "C" int oz_prof_summary(double* out) {
+  std::lock_guard<std::mutex> lk(oz::g_prof_mu);
+  for (int i = 0; i < 3 * oz::PROF_KINDS; ++i) out[i] = 0.0;
+  for (size_t i = 0; i < oz::g_prof_used; ++i) {
+    oz::ProfEntry& e = oz::g_prof[i];
+    if (!e.done) continue;
+    if (cudaEventSynchronize(e.b) != cudaSuccess) {
+      oz::set_error("cudaEventSynchronize failed");
+      return OZ_CUDA_ERROR;
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    out[3 * e.kind] += ms;
+    out[3 * e.kind + 1] += 1.0;
+    out[3 * e.kind + 2] += e.work;
+  }
+  return OZ_OK;
+}
 
 extern "C" int oz_sm_count(int* out) {
   *out = oz::sm_count();

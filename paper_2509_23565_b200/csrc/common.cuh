@@ -26,7 +26,21 @@ const char* last_error();
     }                                                                             \
   } while (0)
 
-#define OZ_CHECK_LAUNCH() OZ_CHECK_CUDA(cudaGetLastError())
+// Every kernel launched by this library is counted (bench.py reports it as
+// gpu_launches); cuBLAS launches are not ours and are not counted.
+void count_launch();
+#define OZ_CHECK_LAUNCH()                                                         \
+  do {                                                                            \
+    ::oz::count_launch();                                                         \
+    OZ_CHECK_CUDA(cudaGetLastError());                                            \
+  } while (0)
+
+// Optional per-phase timing (CUDA events on the launching stream), enabled by
+// oz_prof_enable(); used by bench.py for the roofline of the dominant kernel.
+enum ProfKind { PROF_EMU_GEMM = 0, PROF_PANEL = 1, PROF_DGEMM = 2, PROF_SPLIT = 3,
+                PROF_LASWP = 4, PROF_TRSM = 5, PROF_SOLVE = 6, PROF_OTHER = 7, PROF_KINDS = 8 };
+int prof_start(cudaStream_t st);
+void prof_stop(int tag, cudaStream_t st, int kind, double work);
 
 #define OZ_REQUIRE(cond, code, ...)                                               \
   do {                                                                            \

@@ -443,10 +443,14 @@ extern "C" int oz_gemm_emu(int64_t m, int64_t n, int64_t inner, const int8_t* a_
                            const int32_t* pair_b, const int32_t* pair_shift, double alpha,
                            double beta, double* c, int64_t ldc, int c_is_input,
                            unsigned long long* growth_max, void* stream) {
-  return oz::gemm_emu_launch(m, n, inner, a_slices, a_ld, a_sstride, a_nslices, a_exps, b_slices,
-                             b_ld, b_sstride, b_nslices, b_exps, npairs, pair_a, pair_b,
-                             pair_shift, alpha, beta, c, ldc, c_is_input, growth_max,
-                             oz::as_stream(stream));
+  cudaStream_t st = oz::as_stream(stream);
+  const int tag = oz::prof_start(st);
+  const int s = oz::gemm_emu_launch(m, n, inner, a_slices, a_ld, a_sstride, a_nslices, a_exps,
+                                    b_slices, b_ld, b_sstride, b_nslices, b_exps, npairs, pair_a,
+                                    pair_b, pair_shift, alpha, beta, c, ldc, c_is_input,
+                                    growth_max, st);
+  oz::prof_stop(tag, st, oz::PROF_EMU_GEMM, 2.0 * npairs * (double)m * n * inner);
+  return s;
 }
 
 extern "C" int oz_gemm_pair_i32(int64_t m, int64_t n, int64_t inner, const int8_t* a_slice,

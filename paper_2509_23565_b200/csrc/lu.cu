@@ -570,6 +570,11 @@ int max_abs(const double* a, int64_t m, int64_t n, int64_t rs, int64_t cs, int u
 int apply_swaps(double* a, int64_t lda, const int32_t* ipiv, int64_t t0, int S, const LuWs& ws,
                 int64_t c0a, int64_t c1a, int64_t c0b, int64_t c1b, cudaStream_t st) {
   if (S <= 0) return OZ_OK;
+  struct Stop {
+    int tag;
+    cudaStream_t st;
+    ~Stop() { prof_stop(tag, st, PROF_LASWP, 0.0); }
+  } stop{prof_start(st), st};
   compose_swaps_kernel<<<1, 256, 0, st>>>(ipiv, t0, S, ws.swap_dst, ws.swap_src, ws.swap_cnt);
   OZ_CHECK_LAUNCH();
   const int64_t ncols = (c1a - c0a) + (c1b - c0b);
@@ -585,6 +590,12 @@ int apply_swaps(double* a, int64_t lda, const int32_t* ipiv, int64_t t0, int S, 
 int trsm_blocked(double* a, int64_t lda, int64_t j, int64_t jb, double* b, int64_t ldb,
                  int64_t ncols, cudaStream_t st) {
   if (ncols <= 0) return OZ_OK;
+  struct Stop {
+    int tag;
+    cudaStream_t st;
+    double work;
+    ~Stop() { prof_stop(tag, st, PROF_TRSM, work); }
+  } stop{prof_start(st), st, (double)jb * jb * ncols};
   for (int64_t i = 0; i < jb; i += TRSM_W) {
     const int w = (int)(jb - i < TRSM_W ? jb - i : TRSM_W);
     const double* L = a + (j + i) * lda + (j + i);
@@ -636,9 +647,12 @@ int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int32_t* 
   pa.bar = ws.bar;
   pa.cand = ws.cand;
   void* args[] = {&pa};
+  const int tag = prof_start(st);
+  count_launch();
   OZ_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)panel_window_kernel, dim3(G),
                                             dim3(PANEL_THREADS), args, panel_smem_bytes(w, R),
                                             st));
+  prof_stop(tag, st, PROF_PANEL, (double)m * w);
   return OZ_OK;
 }
 
@@ -676,9 +690,12 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
       if (rest > 0) {
         OZ_TRY(trsm_blocked(a, lda, jj, w, a + (jj + w) * lda + jj, lda, rest, st));
         const int64_t below = n - jj - w;
-        if (below > 0)
+        if (below > 0) {
+          const int tag = prof_start(st);
           OZ_TRY(dgemm(0, 0, below, rest, w, -1.0, a + jj * lda + jj + w, lda,
                        a + (jj + w) * lda + jj, lda, 1.0, a + (jj + w) * lda + jj + w, lda, st));
+          prof_stop(tag, st, PROF_DGEMM, 2.0 * below * rest * w);
+        }
       }
     }
     // ---- panel interchanges on the columns outside the panel (whole-row swaps, :80-82)
@@ -690,17 +707,23 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
       double* a22 = a + (j + jb) * lda + (j + jb);
       OZ_TRY(trsm_blocked(a, lda, j, jb, a12, lda, rest, st));  // solve.py:123-127
       if (backend == 0) {                                         // solve.py:130-134 native
+        const int tag = prof_start(st);
         OZ_TRY(dgemm(0, 0, rest, rest, jb, -1.0, a21, lda, a12, lda, 1.0, a22, lda, st));
+        prof_stop(tag, st, PROF_DGEMM, 2.0 * rest * rest * jb);
         OZ_TRY(max_abs(a22, rest, rest, 1, lda, 0, 0, ws.bits, st));
       } else {                                                    // emulated Schur update
         const int64_t sst = rest * ws.ldK;
+        int tag = prof_start(st);
         OZ_TRY(split_launch(a21, rest, jb, 1, lda, OZ_ROW_SCALED, OZ_PER_VECTOR, k, q, ws.slA,
                             ws.ldK, sst, ws.expA, ws.split_aux, st));
         OZ_TRY(split_launch(a12, jb, rest, 1, lda, OZ_COL_SCALED, OZ_PER_VECTOR, k, q, ws.slB,
                             ws.ldK, sst, ws.expB, ws.split_aux, st));
+        prof_stop(tag, st, PROF_SPLIT, 2.0 * rest * jb * (8.0 + k));
+        tag = prof_start(st);
         OZ_TRY(gemm_emu_launch(rest, rest, jb, ws.slA, ws.ldK, sst, k, ws.expA, ws.slB, ws.ldK,
                                sst, k, ws.expB, npairs, pa, pb, ps, -1.0, 1.0, a22, lda, 1,
                                ws.bits, st));
+        prof_stop(tag, st, PROF_EMU_GEMM, 2.0 * npairs * rest * rest * jb);
       }
     }
     // finalized U rows of this panel: triu(lu[j:j+jb, j:]) (solve.py:135-137)
@@ -713,6 +736,12 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
 
 int lu_solve(const double* lu, int64_t n, int64_t lda, const int64_t* perm, const double* b,
              double* x, int32_t* flag, cudaStream_t st) {
+  struct Stop {
+    int tag;
+    cudaStream_t st;
+    double work;
+    ~Stop() { prof_stop(tag, st, PROF_SOLVE, work); }
+  } stop{prof_start(st), st, 2.0 * n * n};
   gather_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(b, perm, n, x);
   OZ_CHECK_LAUNCH();
   // forward: unit lower
