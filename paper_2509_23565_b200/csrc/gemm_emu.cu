@@ -34,8 +34,8 @@ constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int BK = 128;  // bytes of K per stage (one 128B swizzle atom)
 constexpr int STAGES = 6;
-constexpr int NUM_ACC = 2;
-constexpr int TMEM_COLS = 256;
+constexpr int NUM_ACC = 4;
+constexpr int TMEM_COLS = 512;
 constexpr int NUM_THREADS = 384;
 constexpr int EPI_WARP0 = 4;
 constexpr int MAX_PAIRS = 256;
@@ -62,9 +62,11 @@ struct Params {
   unsigned long long* growth;
   int32_t* debug_out;  // pair-debug mode: raw INT32 product
   int64_t ldo;
+  int ngroups;
   uint8_t pa[MAX_PAIRS];
   uint8_t pb[MAX_PAIRS];
-  uint16_t shift[MAX_PAIRS];
+  uint16_t gshift[MAX_PAIRS];      // (i+j)*q of the group's pairs
+  uint16_t gstart[MAX_PAIRS + 1];  // group g = pairs [gstart[g], gstart[g+1])
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -235,25 +237,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       uint32_t it = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        for (int q = 0; q < p.npairs; ++q, ++it) {
-          const uint32_t buf = it & 1, aph = (it >> 1) & 1;
+        for (int g = 0; g < p.ngroups; ++g, ++it) {
+          const uint32_t buf = it % NUM_ACC, aph = (it / NUM_ACC) & 1;
           mbar_wait(smem_u32(&tempty[buf]), aph ^ 1);
           tc_fence_after();
           const uint32_t dtmem = tmem_base + buf * BN;
-          for (int kb = 0; kb < p.nkb; ++kb) {
-            mbar_wait(smem_u32(&full[stage]), phase);
-            tc_fence_after();
-            const uint32_t a0 = smem_u32(smA + stage * TILE_BYTES);
-            const uint32_t b0 = smem_u32(smB + stage * TILE_BYTES);
+          // every pair of an exact group accumulates into the same INT32 tile
+          for (int q = p.gstart[g]; q < p.gstart[g + 1]; ++q) {
+            const bool first_pair = q == p.gstart[g];
+            for (int kb = 0; kb < p.nkb; ++kb) {
+              mbar_wait(smem_u32(&full[stage]), phase);
+              tc_fence_after();
+              const uint32_t a0 = smem_u32(smA + stage * TILE_BYTES);
+              const uint32_t b0 = smem_u32(smB + stage * TILE_BYTES);
 #pragma unroll
-            for (int kk = 0; kk < BK / 32; ++kk) {
-              tc_mma_i8(dtmem, sdesc(a0 + kk * 32), sdesc(b0 + kk * 32), IDESC,
-                        (kb | kk) != 0 ? 1u : 0u);
-            }
-            tc_commit(smem_u32(&empty[stage]));
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
+              for (int kk = 0; kk < BK / 32; ++kk) {
+                tc_mma_i8(dtmem, sdesc(a0 + kk * 32), sdesc(b0 + kk * 32), IDESC,
+                          (first_pair && (kb | kk) == 0) ? 0u : 1u);
+              }
+              tc_commit(smem_u32(&empty[stage]));
+              if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
+              }
             }
           }
           tc_commit(smem_u32(&tfull[buf]));
@@ -278,11 +284,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int i = 0; i < 64; ++i) acc[i] = 0.0;
       const int row = mt * BM + quad * 32 + lane;
       const int col0 = nt * BN + half * 64;
-      for (int q = 0; q < p.npairs; ++q, ++it) {
-        const uint32_t buf = it & 1, aph = (it >> 1) & 1;
+      for (int q = 0; q < p.ngroups; ++q, ++it) {
+        const uint32_t buf = it % NUM_ACC, aph = (it / NUM_ACC) & 1;
         mbar_wait(smem_u32(&tfull[buf]), aph);
         tc_fence_after();
-        const double s = pow2(-(int)p.shift[q]);
+        const double s = pow2(-(int)p.gshift[q]);
         const uint32_t taddr = tmem_base + lane_base + buf * BN + half * 64;
 #pragma unroll
         for (int c = 0; c < 64; c += 16) {
@@ -309,16 +315,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (row < p.m) {
         const int er = p.expA[row];
         const bool use_c = p.c_is_input && p.beta != 0.0;
+        // chunks of 16 columns: issue all loads of a chunk before any store
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          const int col = col0 + i;
-          if (col < p.n) {
-            const double ab = ldexp_exact(acc[i], er + p.expB[col]);
-            double out = __dmul_rn(p.alpha, ab);
-            double* dst = p.c + (int64_t)col * p.ldc + row;
-            if (use_c) out = __dadd_rn(out, __dmul_rn(p.beta, *dst));
-            *dst = out;
-            gmax = fmax(gmax, fabs(out));
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+          int eb[16];
+          double cv[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int col = col0 + c0 + i;
+            const bool ok = col < p.n;
+            eb[i] = ok ? __ldg(p.expB + col) : 0;
+            cv[i] = (ok && use_c) ? p.c[(int64_t)col * p.ldc + row] : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int col = col0 + c0 + i;
+            if (col < p.n) {
+              const double ab = ldexp_exact(acc[c0 + i], er + eb[i]);
+              double out = __dmul_rn(p.alpha, ab);
+              if (use_c) out = __dadd_rn(out, __dmul_rn(p.beta, cv[i]));
+              p.c[(int64_t)col * p.ldc + row] = out;
+              gmax = fmax(gmax, fabs(out));
+            }
           }
         }
       }
@@ -372,6 +390,50 @@ int make_slice_map(CUtensorMap* map, const int8_t* base, int64_t inner, int64_t 
   return OZ_OK;
 }
 
+// Exact-level grouping.  The reference adds the scaled pair products one by one
+// into an FP64 accumulator (gemm.py:218-222).  While every partial sum is
+// exactly representable no rounding happens, so the pairs of such a level can
+// be summed first (exactly, in INT32 on the tensor core) without changing a
+// single bit.  A level qualifies when (a) its INT32 sum cannot overflow and
+// (b) the running magnitude bound, in units of the level's LSB 2^-shift, stays
+// below 2^53.  From the first level that fails, every pair is its own group
+// and is accumulated in the reference order with one rounding per pair.
+void build_groups(Params& p, const int32_t* shift, int npairs, int64_t inner) {
+  const double term = (double)inner * 127.0 * 127.0;  // max |P| of one pair
+  double bound = 0.0;                                  // sum of max |P_p| * 2^-shift_p
+  bool exact = true;
+  int g = 0, i = 0;
+  while (i < npairs) {
+    int j = i;
+    while (j < npairs && shift[j] == shift[i]) ++j;
+    bool grouped = false;
+    if (exact) {
+      const double lvl = term * (j - i);
+      const double nb = bound + ldexp(lvl, -shift[i]);
+      if (lvl < 2147483648.0 && ldexp(nb, shift[i]) < 9007199254740992.0) {
+        bound = nb;
+        grouped = true;
+      } else {
+        exact = false;
+      }
+    }
+    if (grouped) {
+      p.gstart[g] = (uint16_t)i;
+      p.gshift[g] = (uint16_t)shift[i];
+      ++g;
+    } else {
+      for (int q = i; q < j; ++q) {
+        p.gstart[g] = (uint16_t)q;
+        p.gshift[g] = (uint16_t)shift[q];
+        ++g;
+      }
+    }
+    i = j;
+  }
+  p.gstart[g] = (uint16_t)npairs;
+  p.ngroups = g;
+}
+
 int launch(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
@@ -416,10 +478,12 @@ int gemm_emu_launch(int64_t m, int64_t n, int64_t inner, const int8_t* a_slices,
     OZ_REQUIRE(pair_a[i] >= 0 && pair_a[i] < a_nslices && pair_b[i] >= 0 &&
                    pair_b[i] < b_nslices && pair_shift[i] >= 0 && pair_shift[i] < 1000,
                OZ_INVALID_PARAMS, "bad pair table entry %d", i);
+    OZ_REQUIRE(i == 0 || pair_shift[i] >= pair_shift[i - 1], OZ_INVALID_PARAMS,
+               "pair table must be ordered by level");
     p.pa[i] = (uint8_t)pair_a[i];
     p.pb[i] = (uint8_t)pair_b[i];
-    p.shift[i] = (uint16_t)pair_shift[i];
   }
+  build_groups(p, pair_shift, npairs, inner);
   p.expA = a_exps;
   p.expB = b_exps;
   p.c = c;
@@ -466,6 +530,10 @@ extern "C" int oz_gemm_pair_i32(int64_t m, int64_t n, int64_t inner, const int8_
   p.n = (int)n;
   p.inner = (int)inner;
   p.npairs = 1;
+  p.ngroups = 1;
+  p.gstart[0] = 0;
+  p.gstart[1] = 1;
+  p.gshift[0] = 0;
   p.debug_out = out;
   p.ldo = ldo;
   p.alpha = 1.0;

@@ -50,7 +50,6 @@ constexpr int PANEL_THREADS = 256;
 constexpr int PANEL_WARPS = PANEL_THREADS / 32;
 constexpr int CAND_STRIDE = 4 + PANEL_W;  // doubles per candidate record
 constexpr int TRSM_W = 64;                // diagonal block of the blocked trsm
-constexpr int TRSM_C = 16;                // right-hand-side columns per CTA
 constexpr int SWAP_MAX = 2048;            // max entries of a composed swap list (2*nb)
 
 // ------------------------------------------------------------------ grid barrier
@@ -342,34 +341,47 @@ __global__ void laswp_gather_kernel(double* __restrict__ a, int64_t lda, const i
 }
 
 // ---------------------------------------------------------------- small trsm
-// B[0:w, c] <- L^{-1} B[0:w, c] with L the unit-lower w x w block (w <= 64).
-__global__ void trsm_unit_lower_kernel(const double* __restrict__ L, int64_t ldl, int w,
-                                       double* __restrict__ B, int64_t ldb, int64_t ncols) {
-  __shared__ double sL[TRSM_W][TRSM_W + 1];
-  __shared__ double sX[TRSM_W][TRSM_C + 1];
+// B[0:w, c] <- L^{-1} B[0:w, c], L the unit-lower w x w block (w <= TRSM_W).
+// One thread per right-hand-side column, the column held in registers, L in
+// shared memory (broadcast reads); the 64 x TRSM_COLS tile is staged through
+// shared memory so global loads/stores are coalesced along the columns.
+constexpr int TRSM_COLS = 128;
+__global__ void __launch_bounds__(TRSM_COLS) trsm_unit_lower_kernel(
+    const double* __restrict__ L, int64_t ldl, int w, double* __restrict__ B, int64_t ldb,
+    int64_t ncols) {
+  extern __shared__ double dsm[];
+  double* sL = dsm;                         // [TRSM_W][TRSM_W], row-major sL[r*W+c]
+  double* sX = dsm + TRSM_W * TRSM_W;       // [TRSM_W][TRSM_COLS]
   const int tid = threadIdx.x;
-  const int64_t c0 = (int64_t)blockIdx.x * TRSM_C;
-  for (int i = tid; i < w * w; i += blockDim.x) {
-    const int r = i % w, c = i / w;
-    sL[r][c] = L[c * ldl + r];
+  const int64_t c0 = (int64_t)blockIdx.x * TRSM_COLS;
+  for (int i = tid; i < TRSM_W * TRSM_W; i += TRSM_COLS) {
+    const int r = i % TRSM_W, c = i / TRSM_W;
+    sL[r * TRSM_W + c] = (r < w && c < w && r > c) ? L[c * ldl + r] : 0.0;
   }
-  for (int i = tid; i < w * TRSM_C; i += blockDim.x) {
-    const int r = i % w, c = i / w;
-    sX[r][c] = (c0 + c < ncols) ? B[(c0 + c) * ldb + r] : 0.0;
+  const int lane = tid & 31, wid = tid >> 5;
+  for (int c = wid; c < TRSM_COLS; c += TRSM_COLS / 32) {
+    const bool okc = c0 + c < ncols;
+    for (int r = lane; r < TRSM_W; r += 32)
+      sX[r * TRSM_COLS + c] = (okc && r < w) ? B[(c0 + c) * ldb + r] : 0.0;
   }
   __syncthreads();
-  for (int i = 0; i < w - 1; ++i) {
-    for (int e = tid; e < (w - 1 - i) * TRSM_C; e += blockDim.x) {
-      const int r = i + 1 + e % (w - 1 - i), c = e / (w - 1 - i);
-      sX[r][c] = fma(-sL[r][i], sX[i][c], sX[r][c]);
-    }
-    __syncthreads();
+  double x[TRSM_W];
+#pragma unroll
+  for (int i = 0; i < TRSM_W; ++i) x[i] = sX[i * TRSM_COLS + tid];
+#pragma unroll
+  for (int i = 0; i < TRSM_W - 1; ++i) {
+#pragma unroll
+    for (int r = i + 1; r < TRSM_W; ++r) x[r] = fma(-sL[r * TRSM_W + i], x[i], x[r]);
   }
-  for (int i = tid; i < w * TRSM_C; i += blockDim.x) {
-    const int r = i % w, c = i / w;
-    if (c0 + c < ncols) B[(c0 + c) * ldb + r] = sX[r][c];
+#pragma unroll
+  for (int i = 0; i < TRSM_W; ++i) sX[i * TRSM_COLS + tid] = x[i];
+  __syncthreads();
+  for (int c = wid; c < TRSM_COLS; c += TRSM_COLS / 32) {
+    if (c0 + c >= ncols) continue;
+    for (int r = lane; r < w; r += 32) B[(c0 + c) * ldb + r] = sX[r * TRSM_COLS + c];
   }
 }
+constexpr size_t TRSM_SMEM = sizeof(double) * (TRSM_W * TRSM_W + TRSM_W * TRSM_COLS);
 
 // --------------------------------------------------------------- reductions
 __global__ void max_abs_kernel(const double* __restrict__ a, int64_t m, int64_t n, int64_t rs,
@@ -434,45 +446,78 @@ __global__ void gemv_finish_kernel(const double* __restrict__ part,
 }
 
 // ------------------------------------------------------------------ triangular solves
-constexpr int TRSV_B = 128;
-// x[blk] <- L_bb^{-1} x[blk] (unit lower) or U_bb^{-1} x[blk] (upper)
-__global__ void trsv_diag_kernel(const double* __restrict__ a, int64_t lda, int64_t r0, int bs,
-                                 int upper, double* __restrict__ x, int32_t* zero_diag) {
-  __shared__ double sx[TRSV_B];
-  const int r = threadIdx.x;
-  if (r < bs) sx[r] = x[r0 + r];
+// Sync-free blocked triangular solve, one launch per triangle.  Row block i
+// (TRSV_B rows) is owned by the CTA that draws ticket i (tickets follow the
+// dependency order, so the scheme cannot deadlock).  The CTA folds in the
+// contribution of every finished block j (spinning on its ready flag), then
+// solves its diagonal block and publishes x_i.  Reads of A are coalesced
+// (consecutive threads = consecutive rows of a column-major block).
+constexpr int TRSV_B = 64;
+constexpr int TRSV_G = 4;  // thread groups of TRSV_B threads splitting the j loop
+__global__ void __launch_bounds__(TRSV_B * TRSV_G) trsv_syncfree_kernel(
+    const double* __restrict__ a, int64_t lda, int64_t n, int upper, double* x, int* flags,
+    int* ticket, int32_t* zero_diag) {
+  __shared__ int s_blk;
+  __shared__ double s_acc[TRSV_G][TRSV_B];
+  __shared__ double s_x[TRSV_B];
+  __shared__ double s_diag[TRSV_B][TRSV_B + 1];
+  const int tid = threadIdx.x, r = tid % TRSV_B, grp = tid / TRSV_B;
+  const int nblk = (int)((n + TRSV_B - 1) / TRSV_B);
+  if (tid == 0) s_blk = atomicAdd(ticket, 1);
   __syncthreads();
-  if (!upper) {
-    for (int i = 0; i < bs - 1; ++i) {
-      if (r > i && r < bs) sx[r] = fma(-a[(r0 + i) * lda + r0 + r], sx[i], sx[r]);
-      __syncthreads();
+  const int order = s_blk;
+  const int blk = upper ? nblk - 1 - order : order;
+  const int64_t r0 = (int64_t)blk * TRSV_B;
+  const int bs = (int)min((int64_t)TRSV_B, n - r0);
+  // diagonal block into shared memory (independent of the other blocks)
+  for (int c = grp; c < bs; c += TRSV_G)
+    if (r < bs) s_diag[r][c] = a[(r0 + c) * lda + r0 + r];
+  double acc = 0.0;
+  for (int t = grp; t < order; t += TRSV_G) {
+    const int j = upper ? nblk - 1 - t : t;
+    const int64_t c0 = (int64_t)j * TRSV_B;
+    const int cs = (int)min((int64_t)TRSV_B, n - c0);
+    volatile int* f = flags + j;
+    while (*f == 0) {
     }
-  } else {
-    for (int i = bs - 1; i >= 0; --i) {
-      if (r == i) {
-        const double d = a[(r0 + i) * lda + r0 + i];
-        if (d == 0.0 && zero_diag) *zero_diag = 1;
-        sx[i] = sx[i] / d;
-      }
-      __syncthreads();
-      if (r < i) sx[r] = fma(-a[(r0 + i) * lda + r0 + r], sx[i], sx[r]);
-      __syncthreads();
+    __threadfence();
+    if (r < bs) {
+      const double* col = a + c0 * lda + r0 + r;
+      for (int c = 0; c < cs; ++c) acc = fma(col[c * lda], __ldcg(x + c0 + c), acc);
     }
   }
-  if (r < bs) x[r0 + r] = sx[r];
-}
-
-// x[rows] -= A[rows, r0:r0+bs] x[r0:r0+bs]
-__global__ void trsv_update_kernel(const double* __restrict__ a, int64_t lda, int64_t row_lo,
-                                   int64_t row_hi, int64_t r0, int bs, double* __restrict__ x) {
-  __shared__ double sx[TRSV_B];
-  if (threadIdx.x < bs) sx[threadIdx.x] = x[r0 + threadIdx.x];
+  s_acc[grp][r] = acc;
   __syncthreads();
-  const int64_t i = row_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= row_hi) return;
-  double s = 0.0;
-  for (int j = 0; j < bs; ++j) s = fma(a[(r0 + j) * lda + i], sx[j], s);
-  x[i] -= s;
+  if (tid < 32) {
+    // lane l owns rows l and l+32 of the block
+    double y0 = 0.0, y1 = 0.0;
+    const int ra = tid, rb = tid + 32;
+    if (ra < bs) y0 = x[r0 + ra] - (s_acc[0][ra] + s_acc[1][ra] + s_acc[2][ra] + s_acc[3][ra]);
+    if (rb < bs) y1 = x[r0 + rb] - (s_acc[0][rb] + s_acc[1][rb] + s_acc[2][rb] + s_acc[3][rb]);
+    if (!upper) {
+      for (int c = 0; c < bs; ++c) {
+        const double xc = __shfl_sync(0xffffffffu, c < 32 ? y0 : y1, c & 31);
+        if (ra > c && ra < bs) y0 = fma(-s_diag[ra][c], xc, y0);
+        if (rb > c && rb < bs) y1 = fma(-s_diag[rb][c], xc, y1);
+      }
+    } else {
+      for (int c = bs - 1; c >= 0; --c) {
+        const double d = s_diag[c][c];
+        if (d == 0.0 && tid == 0) *zero_diag = 1;
+        double v = __shfl_sync(0xffffffffu, c < 32 ? y0 : y1, c & 31);
+        v = v / d;
+        if (c < 32 && ra == c) y0 = v;
+        if (c >= 32 && rb == c) y1 = v;
+        if (ra < c) y0 = fma(-s_diag[ra][c], v, y0);
+        if (rb < c) y1 = fma(-s_diag[rb][c], v, y1);
+      }
+    }
+    if (ra < bs) x[r0 + ra] = y0;
+    if (rb < bs) x[r0 + rb] = y1;
+    __threadfence();
+    __syncwarp();
+    if (tid == 0) atomicExch(flags + blk, 1);
+  }
 }
 
 __global__ void gather_kernel(const double* __restrict__ b, const int64_t* __restrict__ perm,
@@ -590,6 +635,13 @@ int apply_swaps(double* a, int64_t lda, const int32_t* ipiv, int64_t t0, int S, 
 int trsm_blocked(double* a, int64_t lda, int64_t j, int64_t jb, double* b, int64_t ldb,
                  int64_t ncols, cudaStream_t st) {
   if (ncols <= 0) return OZ_OK;
+  static bool attr = false;
+  if (!attr) {
+    OZ_CHECK_CUDA(cudaFuncSetAttribute(trsm_unit_lower_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)TRSM_SMEM));
+    attr = true;
+  }
   struct Stop {
     int tag;
     cudaStream_t st;
@@ -599,8 +651,8 @@ int trsm_blocked(double* a, int64_t lda, int64_t j, int64_t jb, double* b, int64
   for (int64_t i = 0; i < jb; i += TRSM_W) {
     const int w = (int)(jb - i < TRSM_W ? jb - i : TRSM_W);
     const double* L = a + (j + i) * lda + (j + i);
-    trsm_unit_lower_kernel<<<(unsigned)ceil_div(ncols, TRSM_C), 256, 0, st>>>(L, lda, w, b + i, ldb,
-                                                                          ncols);
+    trsm_unit_lower_kernel<<<(unsigned)ceil_div(ncols, TRSM_COLS), TRSM_COLS, TRSM_SMEM, st>>>(
+        L, lda, w, b + i, ldb, ncols);
     OZ_CHECK_LAUNCH();
     const int64_t below = jb - i - w;
     if (below > 0)
@@ -735,7 +787,7 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
 }
 
 int lu_solve(const double* lu, int64_t n, int64_t lda, const int64_t* perm, const double* b,
-             double* x, int32_t* flag, cudaStream_t st) {
+             double* x, int32_t* flag, int* sync, cudaStream_t st) {
   struct Stop {
     int tag;
     cudaStream_t st;
@@ -744,29 +796,12 @@ int lu_solve(const double* lu, int64_t n, int64_t lda, const int64_t* perm, cons
   } stop{prof_start(st), st, 2.0 * n * n};
   gather_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(b, perm, n, x);
   OZ_CHECK_LAUNCH();
-  // forward: unit lower
-  for (int64_t r0 = 0; r0 < n; r0 += TRSV_B) {
-    const int bs = (int)(n - r0 < TRSV_B ? n - r0 : TRSV_B);
-    trsv_diag_kernel<<<1, TRSV_B, 0, st>>>(lu, lda, r0, bs, 0, x, flag);
+  const int nblk = (int)ceil_div(n, TRSV_B);
+  for (int upper = 0; upper < 2; ++upper) {
+    OZ_CHECK_CUDA(cudaMemsetAsync(sync, 0, sizeof(int) * (nblk + 1), st));
+    trsv_syncfree_kernel<<<nblk, TRSV_B * TRSV_G, 0, st>>>(lu, lda, n, upper, x, sync + 1, sync,
+                                                           flag);
     OZ_CHECK_LAUNCH();
-    const int64_t lo = r0 + bs;
-    if (lo < n) {
-      trsv_update_kernel<<<(unsigned)ceil_div(n - lo, 256), 256, 0, st>>>(lu, lda, lo, n, r0, bs,
-                                                                           x);
-      OZ_CHECK_LAUNCH();
-    }
-  }
-  // backward: upper
-  const int64_t nblk = ceil_div(n, TRSV_B);
-  for (int64_t bi = nblk - 1; bi >= 0; --bi) {
-    const int64_t r0 = bi * TRSV_B;
-    const int bs = (int)(n - r0 < TRSV_B ? n - r0 : TRSV_B);
-    trsv_diag_kernel<<<1, TRSV_B, 0, st>>>(lu, lda, r0, bs, 1, x, flag);
-    OZ_CHECK_LAUNCH();
-    if (r0 > 0) {
-      trsv_update_kernel<<<(unsigned)ceil_div(r0, 256), 256, 0, st>>>(lu, lda, 0, r0, r0, bs, x);
-      OZ_CHECK_LAUNCH();
-    }
   }
   return OZ_OK;
 }
@@ -801,14 +836,18 @@ extern "C" int oz_lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int b
                        pair_shift, ipiv, stats, info, workspace, ws_bytes, oz::as_stream(stream));
 }
 
-extern "C" size_t oz_lu_solve_workspace_bytes(int64_t n) { return 256; }
+extern "C" size_t oz_lu_solve_workspace_bytes(int64_t n) {
+  return sizeof(int) * (2 + oz::ceil_div(n, 64) + 16);
+}
 
 extern "C" int oz_lu_solve(const double* lu, int64_t n, int64_t lda, const int64_t* perm,
                            const double* b, double* x, void* workspace, size_t ws_bytes,
                            void* stream) {
-  OZ_REQUIRE(ws_bytes >= 4, OZ_INVALID_PARAMS, "workspace too small");
+  OZ_REQUIRE(ws_bytes >= oz_lu_solve_workspace_bytes(n), OZ_INVALID_PARAMS,
+             "workspace too small");
   OZ_CHECK_CUDA(cudaMemsetAsync(workspace, 0, 4, oz::as_stream(stream)));
-  return oz::lu_solve(lu, n, lda, perm, b, x, reinterpret_cast<int32_t*>(workspace),
+  int32_t* flag = reinterpret_cast<int32_t*>(workspace);
+  return oz::lu_solve(lu, n, lda, perm, b, x, flag, reinterpret_cast<int*>(flag + 4),
                       oz::as_stream(stream));
 }
 

@@ -238,9 +238,10 @@ def _solve_device(lu_cm, dperm, b_dev):
     t = _dev.torch()
     n = int(lu_cm.shape[0])
     x = t.empty((n,), dtype=t.float64, device="cuda")
-    ws = t.zeros((64,), dtype=t.int32, device="cuda")
+    nbytes = int(_lib.query("oz_lu_solve_workspace_bytes", n))
+    ws = t.zeros((nbytes // 4 + 1,), dtype=t.int32, device="cuda")
     _lib.call("oz_lu_solve", lu_cm.data_ptr(), n, int(lu_cm.stride(1)), dperm.data_ptr(),
-              b_dev.data_ptr(), x.data_ptr(), ws.data_ptr(), 256, _dev.stream())
+              b_dev.data_ptr(), x.data_ptr(), ws.data_ptr(), nbytes, _dev.stream())
     return x, ws
 
 

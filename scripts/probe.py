@@ -53,9 +53,26 @@ def lu_probe(n, nb, backends):
 
 if __name__ == "__main__":
     what = sys.argv[1]
-    if what == "gemm":
+    if what == "gemm1":
+        pass
+    elif what == "gemm":
         gemm_probe(int(sys.argv[2]), [int(k) for k in sys.argv[3].split(",")])
     else:
         n, nb = int(sys.argv[2]), int(sys.argv[3])
         lu_probe(n, nb, [("fp64", oz.GemmBackend.native()), ("k7", oz.GemmBackend.int8(7)),
                          ("k6", oz.GemmBackend.int8(6))])
+
+
+def gemm_once(m, n, K, k, reps=2):
+    """One emulated GEMM call (column-major C) for ncu capture."""
+    a = torch.rand((m, K), dtype=torch.float64, device="cuda") - 0.5
+    b = torch.rand((K, n), dtype=torch.float64, device="cuda") - 0.5
+    out = torch.empty((n, m), dtype=torch.float64, device="cuda").t()
+    bk = oz.GemmBackend.int8(k)
+    for _ in range(reps):
+        emulated_into(bk, a, b, -1.0, 1.0, out, True)
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__" and sys.argv[1] == "gemm1":
+    gemm_once(*[int(v) for v in sys.argv[2:6]])
