@@ -77,8 +77,11 @@ __device__ __forceinline__ void grid_sync(GridBar* bar, unsigned nblocks) {
   __syncthreads();
 }
 
-// np.argmax(|col|) order: larger magnitude wins, ties -> smaller logical position
+// np.argmax(|col|) order: larger magnitude wins, ties -> smaller logical position;
+// NaN counts as the maximum (numpy returns the first NaN).
 __device__ __forceinline__ bool better(double a1, int p1, double a2, int p2) {
+  const bool n1 = isnan(a1), n2 = isnan(a2);
+  if (n1 || n2) return n1 && (!n2 || p1 < p2);
   return a1 > a2 || (a1 == a2 && p1 < p2);
 }
 
