@@ -227,7 +227,7 @@ def run_ours(args, rank, world):
         torch.cuda.synchronize()
         barrier()
     launches = _lib.load().oz_launch_count() - launches0
-    prof = np.zeros(24)
+    prof = np.zeros(36)
     _lib.call("oz_prof_summary", prof.ctypes.data)
     _lib.call("oz_prof_enable", 0)
     ms = ev0.elapsed_time(ev1) / args.steps
@@ -289,10 +289,11 @@ def run_ours(args, rank, world):
     if rank != 0:
         return
     peaks, peak_kind = load_peaks()
-    kinds = ["emu_gemm", "panel", "dgemm", "split", "laswp", "trsm", "solve", "other"]
+    kinds = ["emu_gemm", "panel", "schur_dgemm", "split", "laswp", "trsm", "solve", "other",
+             "swap_compose", "panel_dgemm", "trsm_dgemm", "-"]
     breakdown = {kinds[i]: {"ms_per_step": prof[3 * i] / args.steps,
                             "launches_per_step": prof[3 * i + 1] / args.steps}
-                 for i in range(8) if prof[3 * i + 1] > 0}
+                 for i in range(12) if prof[3 * i + 1] > 0}
     gemm_ms, gemm_launch, gemm_ops = prof[0], prof[1], prof[2]
     achieved = gemm_ops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     peak = 2.0 * float(peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"])

@@ -59,9 +59,10 @@ int oz_version(void);
 /* Number of kernels this library has launched (process-wide, monotone). */
 long long oz_launch_count(void);
 /* Per-phase CUDA-event timing: enable (and clear) / read.  summary writes
- * 8 kinds x {total ms, launches, algorithmic work}; kinds: 0 emulated GEMM
- * (work = INT8 ops), 1 panel, 2 cuBLAS DGEMM (flops), 3 split (bytes),
- * 4 laswp, 5 trsm, 6 solve, 7 other. */
+ * 12 kinds x {total ms, launches, algorithmic work}; kinds: 0 emulated GEMM
+ * (work = INT8 ops), 1 panel, 2 Schur cuBLAS DGEMM (flops), 3 split (bytes),
+ * 4 laswp gather, 5 trsm kernel, 6 solve, 7 other, 8 swap composition,
+ * 9 in-panel DGEMM, 10 trsm DGEMM. */
 int oz_prof_enable(int on);
 int oz_prof_summary(double* out);
 /* Number of SMs of the current device (used by host-side schedulers). */

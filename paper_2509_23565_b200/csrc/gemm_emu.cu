@@ -25,6 +25,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace oz {
@@ -446,6 +448,7 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStream_t
   p.num_tiles = p.num_m_tiles * p.num_n_tiles;
   p.nkb = (int)ceil_div(p.inner, BK);
   int grid = sm_count();
+  if (const char* g = getenv("OZ_GEMM_GRID")) grid = atoi(g) > 0 ? atoi(g) : grid;  // tuning knob
   if (grid > p.num_tiles) grid = p.num_tiles;
   emu_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ta, tb, p);
   OZ_CHECK_LAUNCH();

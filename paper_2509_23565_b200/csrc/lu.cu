@@ -97,13 +97,29 @@ struct PanelArgs {
   int32_t* info;
   GridBar* bar;
   double* cand;  // [2][gridDim][CAND_STRIDE]
+  unsigned epoch;  // unique per window launch: candidate tags are epoch*64 + step + 1
+  int32_t* list_dst;  // gather list of this window's interchanges (rows outside
+  int32_t* list_src;  // the window columns): new_row[dst] = old_row[src]
+  int32_t* list_cnt;
 };
+
+__device__ __forceinline__ long long ld_relaxed(const long long* p) {
+  long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(long long* p, long long v) {
+  asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// candidate record: [0] |v| (double), [1] pos (low 32) | tag (high 32), [2] physical
+// row, [4..4+w) row values.  Data first, tag last (release store).
 
 struct PanelShared {
   double red_a[PANEL_WARPS];
   int red_p[PANEL_WARPS];
   int red_r[PANEL_WARPS];
   int occ[PANEL_W];
+  int prow[PANEL_W];
   double urow[PANEL_W];
   int best;
 };
@@ -184,37 +200,56 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
       const int br_ = sh.best;
       double* rec = p.cand + ((size_t)buf * gridDim.x + blockIdx.x) * CAND_STRIDE;
       long long* irec = reinterpret_cast<long long*>(rec);
-      if (br_ < 0) {
-        if (tid == 0) {
+      if (tid == 0) {
+        if (br_ < 0) {
           rec[0] = -1.0;
           irec[1] = 0x7fffffff;
           irec[2] = -1;
-        }
-      } else {
-        if (tid == 0) {
+        } else {
           rec[0] = fabs(sm[t * R + br_]);
           irec[1] = pos[br_];
           irec[2] = row_lo + br_;
+          for (int c = t; c < w; ++c) rec[4 + c] = sm[c * R + br_];
         }
-        for (int c = t + tid; c < w; c += PANEL_THREADS) rec[4 + c] = sm[c * R + br_];
+        // arrival: data, fence, then one atomic on a counter that only grows
+        __threadfence();
+        atomicAdd(&p.bar->count, 1u);
       }
     }
     if (t == w) break;
 
-    // ---- one grid barrier per column, then every CTA reduces all candidates
+    // ---- wait until all CTAs published column t (counter reaches G*(t+1)), then
+    //      every CTA reduces all candidate records identically
     const int buf = t & 1;
-    grid_sync(p.bar, gridDim.x);
+    if (tid == 0) {
+      const unsigned target = gridDim.x * (unsigned)(t + 1);
+      volatile unsigned* ctr = &p.bar->count;
+      while (*ctr < target) {
+      }
+      __threadfence();
+    }
+    __syncthreads();
     if (wid == 0) {
-      double ba = -1.0;
-      int bp = 0x7fffffff, bg = 0;
-      for (int g = lane; g < (int)gridDim.x; g += 32) {
+      constexpr int PER = 5;  // up to 160 CTAs
+      double av[PER];
+      long long pk[PER];
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int g = lane + 32 * i;
         const double* rec = p.cand + ((size_t)buf * gridDim.x + g) * CAND_STRIDE;
-        const double av = __ldcg(rec);
-        const int pv = (int)__ldcg(reinterpret_cast<const long long*>(rec) + 1);
-        if (better(av, pv, ba, bp)) {
-          ba = av;
-          bp = pv;
-          bg = g;
+        av[i] = g < (int)gridDim.x ? __ldcg(rec) : -2.0;
+        pk[i] = g < (int)gridDim.x ? __ldcg(reinterpret_cast<const long long*>(rec) + 1)
+                                   : 0x7fffffffll;
+      }
+      double ba = -2.0;
+      int bp = 0x7fffffff, bg = 0;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        if (lane + 32 * i >= (int)gridDim.x) continue;
+        if (better(av[i], (int)pk[i], ba, bp)) {
+          ba = av[i];
+          bp = (int)pk[i];
+          bg = lane + 32 * i;
         }
       }
 #pragma unroll
@@ -245,7 +280,8 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
       }
       // interchange bookkeeping (solve.py:80-82): pivot row is final; the row
       // at position t takes the pivot's old position
-      if (prow >= row_lo && prow < row_lo + nloc) pos[prow - row_lo] = -1;
+      if (prow >= row_lo && prow < row_lo + nloc) pos[prow - row_lo] = -(t + 1);
+      if (blockIdx.x == 0) sh.prow[t] = (int)prow;
       if (rt != prow) {
         if (rt >= row_lo && rt < row_lo + nloc) pos[rt - row_lo] = ppos;
         if (ppos < PANEL_W) sh.occ[ppos] = rt;
@@ -266,8 +302,21 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
     }
     __syncthreads();
   }
-  for (int c = 0; c < w; ++c)
-    for (int r = tid; r < nloc; r += PANEL_THREADS) abase[c * p.lda + r] = sm[c * R + r];
+  // rows go straight to their final positions (pivot row of step t -> t,
+  // displaced row -> its logical position); every moved row is listed so the
+  // same interchanges can be applied to the other columns by a gather.
+  double* wbase = p.a + p.r0 * p.lda + p.r0;
+  for (int r = tid; r < nloc; r += PANEL_THREADS) {
+    const int ps = pos[r];
+    const int fin = ps < 0 ? -ps - 1 : ps;
+    const int phys = (int)(row_lo + r);
+    for (int c = 0; c < w; ++c) wbase[c * p.lda + fin] = sm[c * R + r];
+    if (fin != phys) {
+      const int slot = atomicAdd(p.list_cnt, 1);
+      p.list_dst[slot] = (int32_t)(p.r0 + fin);
+      p.list_src[slot] = (int32_t)(p.r0 + phys);
+    }
+  }
   if (p.growth) {
     gmax = warp_max(gmax);
     if (lane == 0 && gmax > 0.0) atomic_max_abs(p.growth, gmax);
@@ -357,13 +406,16 @@ __global__ void __launch_bounds__(TRSM_COLS) trsm_unit_lower_kernel(
   double* sX = dsm + TRSM_W * TRSM_W;       // [TRSM_W][TRSM_COLS]
   const int tid = threadIdx.x;
   const int64_t c0 = (int64_t)blockIdx.x * TRSM_COLS;
+#pragma unroll 8
   for (int i = tid; i < TRSM_W * TRSM_W; i += TRSM_COLS) {
     const int r = i % TRSM_W, c = i / TRSM_W;
-    sL[r * TRSM_W + c] = (r < w && c < w && r > c) ? L[c * ldl + r] : 0.0;
+    sL[r * TRSM_W + c] = (r < w && c < w && r > c) ? __ldg(L + c * ldl + r) : 0.0;
   }
   const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll 8
   for (int c = wid; c < TRSM_COLS; c += TRSM_COLS / 32) {
     const bool okc = c0 + c < ncols;
+#pragma unroll
     for (int r = lane; r < TRSM_W; r += 32)
       sX[r * TRSM_COLS + c] = (okc && r < w) ? B[(c0 + c) * ldb + r] : 0.0;
   }
@@ -480,14 +532,18 @@ __global__ void __launch_bounds__(TRSV_B * TRSV_G) trsv_syncfree_kernel(
     const int j = upper ? nblk - 1 - t : t;
     const int64_t c0 = (int64_t)j * TRSV_B;
     const int cs = (int)min((int64_t)TRSV_B, n - c0);
+    // the block of A does not depend on the solution: load it before waiting
+    double av[TRSV_B];
+    const double* col = a + c0 * lda + r0 + r;
+#pragma unroll
+    for (int c = 0; c < TRSV_B; ++c) av[c] = (c < cs && r < bs) ? col[c * lda] : 0.0;
     volatile int* f = flags + j;
     while (*f == 0) {
     }
     __threadfence();
-    if (r < bs) {
-      const double* col = a + c0 * lda + r0 + r;
-      for (int c = 0; c < cs; ++c) acc = fma(col[c * lda], __ldcg(x + c0 + c), acc);
-    }
+    const double* xj = x + c0;
+#pragma unroll
+    for (int c = 0; c < TRSV_B; ++c) acc = fma(av[c], c < cs ? __ldcg(xj + c) : 0.0, acc);
   }
   s_acc[grp][r] = acc;
   __syncthreads();
@@ -615,18 +671,15 @@ int max_abs(const double* a, int64_t m, int64_t n, int64_t rs, int64_t cs, int u
   return OZ_OK;
 }
 
-int apply_swaps(double* a, int64_t lda, const int32_t* ipiv, int64_t t0, int S, const LuWs& ws,
-                int64_t c0a, int64_t c1a, int64_t c0b, int64_t c1b, cudaStream_t st) {
-  if (S <= 0) return OZ_OK;
+int apply_list(double* a, int64_t lda, const LuWs& ws, int64_t c0a, int64_t c1a, int64_t c0b,
+               int64_t c1b, cudaStream_t st) {
+  const int64_t ncols = (c1a - c0a) + (c1b - c0b);
+  if (ncols <= 0) return OZ_OK;
   struct Stop {
     int tag;
     cudaStream_t st;
     ~Stop() { prof_stop(tag, st, PROF_LASWP, 0.0); }
   } stop{prof_start(st), st};
-  compose_swaps_kernel<<<1, 256, 0, st>>>(ipiv, t0, S, ws.swap_dst, ws.swap_src, ws.swap_cnt);
-  OZ_CHECK_LAUNCH();
-  const int64_t ncols = (c1a - c0a) + (c1b - c0b);
-  if (ncols <= 0) return OZ_OK;
   int64_t blocks = ncols < sm_count() * 8 ? ncols : sm_count() * 8;
   laswp_gather_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, lda, ws.swap_dst, ws.swap_src,
                                                         ws.swap_cnt, c0a, c1a, c0b, c1b);
@@ -645,22 +698,21 @@ int trsm_blocked(double* a, int64_t lda, int64_t j, int64_t jb, double* b, int64
                                        (int)TRSM_SMEM));
     attr = true;
   }
-  struct Stop {
-    int tag;
-    cudaStream_t st;
-    double work;
-    ~Stop() { prof_stop(tag, st, PROF_TRSM, work); }
-  } stop{prof_start(st), st, (double)jb * jb * ncols};
   for (int64_t i = 0; i < jb; i += TRSM_W) {
     const int w = (int)(jb - i < TRSM_W ? jb - i : TRSM_W);
     const double* L = a + (j + i) * lda + (j + i);
+    int tag = prof_start(st);
     trsm_unit_lower_kernel<<<(unsigned)ceil_div(ncols, TRSM_COLS), TRSM_COLS, TRSM_SMEM, st>>>(
         L, lda, w, b + i, ldb, ncols);
     OZ_CHECK_LAUNCH();
+    prof_stop(tag, st, PROF_TRSM, (double)w * w * ncols);
     const int64_t below = jb - i - w;
-    if (below > 0)
+    if (below > 0) {
+      tag = prof_start(st);
       OZ_TRY(dgemm(0, 0, below, ncols, w, -1.0, a + (j + i) * lda + (j + i + w), lda, b + i, ldb,
                    1.0, b + i + w, ldb, st));
+      prof_stop(tag, st, PROF_DGEMM_TRSM, 2.0 * below * ncols * w);
+    }
   }
   return OZ_OK;
 }
@@ -701,6 +753,15 @@ int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int32_t* 
   pa.info = info;
   pa.bar = ws.bar;
   pa.cand = ws.cand;
+  static unsigned epoch = 0;
+  epoch = (epoch + 1) & 0x3ffffff;
+  if (epoch == 0) epoch = 1;
+  pa.epoch = epoch;
+  pa.list_dst = ws.swap_dst;
+  pa.list_src = ws.swap_src;
+  pa.list_cnt = ws.swap_cnt;
+  OZ_CHECK_CUDA(cudaMemsetAsync(ws.swap_cnt, 0, sizeof(int32_t), st));
+  OZ_CHECK_CUDA(cudaMemsetAsync(ws.bar, 0, sizeof(GridBar), st));
   void* args[] = {&pa};
   const int tag = prof_start(st);
   count_launch();
@@ -729,6 +790,7 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
   OZ_REQUIRE(ws_bytes >= need, OZ_INVALID_PARAMS, "workspace too small (%zu < %zu)", ws_bytes,
              need);
   OZ_CHECK_CUDA(cudaMemsetAsync(ws.bar, 0, sizeof(GridBar), st));
+  OZ_CHECK_CUDA(cudaMemsetAsync(ws.cand, 0, sizeof(double) * 2 * 1024 * CAND_STRIDE, st));
   OZ_CHECK_CUDA(cudaMemsetAsync(ws.bits, 0, 4 * sizeof(unsigned long long), st));
   OZ_CHECK_CUDA(cudaMemsetAsync(info, 0, sizeof(int32_t), st));
   OZ_TRY(max_abs(a, n, n, 1, lda, 0, 0, ws.bits + 1, st));
@@ -739,8 +801,9 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
     for (int64_t jj = j; jj < j + jb; jj += PANEL_W) {
       const int w = (int)((j + jb - jj) < PANEL_W ? (j + jb - jj) : PANEL_W);
       OZ_TRY(panel_window(a, lda, jj, n - jj, w, ipiv, info, ws, st));
-      // interchanges of this window on all panel columns (the window's own included)
-      OZ_TRY(apply_swaps(a, lda, ipiv, jj, w, ws, j, j + jb, 0, 0, st));
+      // the window's interchanges on every other column: whole-row swaps
+      // (solve.py:80-82); the window kernel already placed its own columns
+      OZ_TRY(apply_list(a, lda, ws, 0, jj, jj + w, n, st));
       const int64_t rest = j + jb - (jj + w);
       if (rest > 0) {
         OZ_TRY(trsm_blocked(a, lda, jj, w, a + (jj + w) * lda + jj, lda, rest, st));
@@ -749,12 +812,10 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
           const int tag = prof_start(st);
           OZ_TRY(dgemm(0, 0, below, rest, w, -1.0, a + jj * lda + jj + w, lda,
                        a + (jj + w) * lda + jj, lda, 1.0, a + (jj + w) * lda + jj + w, lda, st));
-          prof_stop(tag, st, PROF_DGEMM, 2.0 * below * rest * w);
+          prof_stop(tag, st, PROF_DGEMM_PANEL, 2.0 * below * rest * w);
         }
       }
     }
-    // ---- panel interchanges on the columns outside the panel (whole-row swaps, :80-82)
-    OZ_TRY(apply_swaps(a, lda, ipiv, j, (int)jb, ws, 0, j, j + jb, n, st));
     const int64_t rest = n - j - jb;
     if (rest > 0) {
       double* a12 = a + (j + jb) * lda + j;
