@@ -22,6 +22,7 @@
 // interchanges into one read-all/write-all pass per column.  The rest of the
 // panel is updated with trsm + cuBLAS DGEMM; the Schur update is cuBLAS DGEMM
 // (native comparator) or the Ozaki-INT8 tcgen05 GEMM (gemm_emu.cu).
+#include <stdlib.h>
 #include <vector>
 
 #include "common.cuh"
@@ -101,6 +102,7 @@ struct PanelArgs {
   int32_t* list_dst;  // gather list of this window's interchanges (rows outside
   int32_t* list_src;  // the window columns): new_row[dst] = old_row[src]
   int32_t* list_cnt;
+  unsigned long long* dbg;  // optional per-phase cycle counters (OZ_PANEL_TIMING)
 };
 
 __device__ __forceinline__ long long ld_relaxed(const long long* p) {
@@ -123,6 +125,16 @@ struct PanelShared {
   double urow[PANEL_W];
   int best;
 };
+
+unsigned long long* panel_dbg() {
+  static unsigned long long* dbg = nullptr;
+  static const bool on = getenv("OZ_PANEL_TIMING") != nullptr;
+  if (on && !dbg) {
+    cudaMalloc(&dbg, 8 * sizeof(unsigned long long));
+    cudaMemset(dbg, 0, 8 * sizeof(unsigned long long));
+  }
+  return on ? dbg : nullptr;
+}
 
 size_t panel_smem_bytes(int w, int R) {
   return (size_t)w * R * sizeof(double) + (size_t)R * sizeof(int);
@@ -152,24 +164,45 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
     gmax = fmax(gmax, fabs(sm[c * R + r]));
   }
 
-  for (int t = 0; t <= w; ++t) {
-    // ---- publish this CTA's pivot candidate for column t (values after step t-1)
-    if (t < w) {
-      const int buf = t & 1;
-      double ba = -1.0;
-      int bp = 0x7fffffff, br = -1;
-      for (int r = tid; r < nloc; r += PANEL_THREADS) {
-        const int pr = pos[r];
-        if (pr < 0) continue;
-        const double v = fabs(sm[t * R + r]);
-        if (better(v, pr, ba, bp)) {
-          ba = v;
-          bp = pr;
-          br = r;
-        }
-      }
+  // thread-local candidate for the current column (values after the last update)
+  double ca = -1.0;
+  int cp = 0x7fffffff, cr = -1;
+  for (int r = tid; r < nloc; r += PANEL_THREADS) {
+    const double v = fabs(sm[r]);
+    if (better(v, pos[r], ca, cp)) {
+      ca = v;
+      cp = pos[r];
+      cr = r;
+    }
+  }
+
+  long long _tp = clock64();
+  for (int t = 0; t < w; ++t) {
+    const int buf = t & 1;
+    // ---- block argmax of the thread candidates (np.argmax order)
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
+    for (int o = 16; o > 0; o >>= 1) {
+      const double oa = __shfl_xor_sync(0xffffffffu, ca, o);
+      const int op = __shfl_xor_sync(0xffffffffu, cp, o);
+      const int orr = __shfl_xor_sync(0xffffffffu, cr, o);
+      if (better(oa, op, ca, cp)) {
+        ca = oa;
+        cp = op;
+        cr = orr;
+      }
+    }
+    if (lane == 0) {
+      sh.red_a[wid] = ca;
+      sh.red_p[wid] = cp;
+      sh.red_r[wid] = cr;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      double ba = lane < PANEL_WARPS ? sh.red_a[lane] : -2.0;
+      int bp = lane < PANEL_WARPS ? sh.red_p[lane] : 0x7fffffff;
+      int br = lane < PANEL_WARPS ? sh.red_r[lane] : -1;
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
         const double oa = __shfl_xor_sync(0xffffffffu, ba, o);
         const int op = __shfl_xor_sync(0xffffffffu, bp, o);
         const int orr = __shfl_xor_sync(0xffffffffu, br, o);
@@ -179,70 +212,45 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
           br = orr;
         }
       }
-      if (lane == 0) {
-        sh.red_a[wid] = ba;
-        sh.red_p[wid] = bp;
-        sh.red_r[wid] = br;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        double fa = sh.red_a[0];
-        int fp = sh.red_p[0], fr = sh.red_r[0];
-        for (int i = 1; i < PANEL_WARPS; ++i)
-          if (better(sh.red_a[i], sh.red_p[i], fa, fp)) {
-            fa = sh.red_a[i];
-            fp = sh.red_p[i];
-            fr = sh.red_r[i];
-          }
-        sh.best = fr;
-      }
-      __syncthreads();
-      const int br_ = sh.best;
+      br = __shfl_sync(0xffffffffu, br, 0);
+      // ---- publish the CTA's candidate record, then arrive on the step counter
       double* rec = p.cand + ((size_t)buf * gridDim.x + blockIdx.x) * CAND_STRIDE;
       long long* irec = reinterpret_cast<long long*>(rec);
-      if (tid == 0) {
-        if (br_ < 0) {
-          rec[0] = -1.0;
-          irec[1] = 0x7fffffff;
-          irec[2] = -1;
-        } else {
-          rec[0] = fabs(sm[t * R + br_]);
-          irec[1] = pos[br_];
-          irec[2] = row_lo + br_;
-          for (int c = t; c < w; ++c) rec[4 + c] = sm[c * R + br_];
-        }
-        // arrival: data, fence, then one atomic on a counter that only grows
-        __threadfence();
-        atomicAdd(&p.bar->count, 1u);
-      }
-    }
-    if (t == w) break;
-
-    // ---- wait until all CTAs published column t (counter reaches G*(t+1)), then
-    //      every CTA reduces all candidate records identically
-    const int buf = t & 1;
-    if (tid == 0) {
-      const unsigned target = gridDim.x * (unsigned)(t + 1);
-      volatile unsigned* ctr = &p.bar->count;
-      while (*ctr < target) {
+      if (br >= 0)
+        for (int c = t + lane; c < w; c += 32) rec[4 + c] = sm[c * R + br];
+      if (lane == 0) {
+        rec[0] = br >= 0 ? fabs(sm[t * R + br]) : -1.0;
+        irec[1] = br >= 0 ? pos[br] : 0x7fffffff;
+        irec[2] = br >= 0 ? row_lo + br : -1;
       }
       __threadfence();
-    }
-    __syncthreads();
-    if (wid == 0) {
+      __syncwarp();
+      if (lane == 0) atomicAdd(&p.bar->count, 1u);
+      if (p.dbg && lane == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 0, (unsigned long long)(_n - _tp)); _tp = _n; }
+      // ---- wait for all CTAs (counter reaches G*(t+1)), reduce all records
+      if (lane == 0) {
+        const unsigned target = gridDim.x * (unsigned)(t + 1);
+        volatile unsigned* ctr = &p.bar->count;
+        while (*ctr < target) {
+        }
+      }
+      __syncwarp();
+      __threadfence();
+      if (p.dbg && lane == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 1, (unsigned long long)(_n - _tp)); _tp = _n; }
       constexpr int PER = 5;  // up to 160 CTAs
       double av[PER];
       long long pk[PER];
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
         const int g = lane + 32 * i;
-        const double* rec = p.cand + ((size_t)buf * gridDim.x + g) * CAND_STRIDE;
-        av[i] = g < (int)gridDim.x ? __ldcg(rec) : -2.0;
-        pk[i] = g < (int)gridDim.x ? __ldcg(reinterpret_cast<const long long*>(rec) + 1)
+        const double* cr_ = p.cand + ((size_t)buf * gridDim.x + g) * CAND_STRIDE;
+        av[i] = g < (int)gridDim.x ? __ldcg(cr_) : -2.0;
+        pk[i] = g < (int)gridDim.x ? __ldcg(reinterpret_cast<const long long*>(cr_) + 1)
                                    : 0x7fffffffll;
       }
-      double ba = -2.0;
-      int bp = 0x7fffffff, bg = 0;
+      ba = -2.0;
+      bp = 0x7fffffff;
+      int bg = 0;
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
         if (lane + 32 * i >= (int)gridDim.x) continue;
@@ -263,45 +271,65 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
           bg = og;
         }
       }
-      if (lane == 0) sh.best = bg;
+      if (p.dbg && lane == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 2, (unsigned long long)(_n - _tp)); _tp = _n; }
+      // ---- winner's row (the new U row) and interchange bookkeeping
+      const double* win = p.cand + ((size_t)buf * gridDim.x + bg) * CAND_STRIDE;
+      for (int c = t + lane; c < w; c += 32) sh.urow[c] = __ldcg(win + 4 + c);
+      if (lane == 0) {
+        const int ppos = (int)__ldcg(reinterpret_cast<const long long*>(win) + 1);
+        const int64_t prow = __ldcg(reinterpret_cast<const long long*>(win) + 2);
+        const int rt = sh.occ[t];  // relative physical row currently at position t
+        const double piv = __ldcg(win + 4 + t);
+        if (blockIdx.x == 0) {
+          p.ipiv[p.r0 + t] = (int32_t)(p.r0 + ppos);
+          if (piv == 0.0) atomicCAS(reinterpret_cast<int*>(p.info), 0, (int)(p.r0 + t + 1));
+          sh.prow[t] = (int)prow;
+        }
+        // solve.py:80-82: the pivot row is final; the row at position t takes
+        // the pivot's old position
+        if (prow >= row_lo && prow < row_lo + nloc) pos[prow - row_lo] = -(t + 1);
+        if (rt != prow) {
+          if (rt >= row_lo && rt < row_lo + nloc) pos[rt - row_lo] = ppos;
+          if (ppos < PANEL_W) sh.occ[ppos] = rt;
+        }
+      }
+      if (p.dbg && lane == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 3, (unsigned long long)(_n - _tp)); _tp = _n; }
     }
     __syncthreads();
-    const double* win = p.cand + ((size_t)buf * gridDim.x + sh.best) * CAND_STRIDE;
-    const int ppos = (int)__ldcg(reinterpret_cast<const long long*>(win) + 1);
-    const int64_t prow = __ldcg(reinterpret_cast<const long long*>(win) + 2);
-    for (int c = t + tid; c < w; c += PANEL_THREADS) sh.urow[c] = __ldcg(win + 4 + c);
-    const int rt = sh.occ[t];  // relative physical row currently at position t
-    __syncthreads();
+    // ---- column scaling by DIVISION (solve.py:84) and rank-1 update (:86) as
+    //      product-then-subtract (np.outer then -=); the next column's
+    //      candidate is tracked on the fly
     const double piv = sh.urow[t];
-    if (tid == 0) {
-      if (blockIdx.x == 0) {
-        p.ipiv[p.r0 + t] = (int32_t)(p.r0 + ppos);
-        if (piv == 0.0) atomicCAS(reinterpret_cast<int*>(p.info), 0, (int)(p.r0 + t + 1));
-      }
-      // interchange bookkeeping (solve.py:80-82): pivot row is final; the row
-      // at position t takes the pivot's old position
-      if (prow >= row_lo && prow < row_lo + nloc) pos[prow - row_lo] = -(t + 1);
-      if (blockIdx.x == 0) sh.prow[t] = (int)prow;
-      if (rt != prow) {
-        if (rt >= row_lo && rt < row_lo + nloc) pos[rt - row_lo] = ppos;
-        if (ppos < PANEL_W) sh.occ[ppos] = rt;
-      }
-    }
-    __syncthreads();
-    // column scaling by DIVISION (solve.py:84) and rank-1 update (:86) as
-    // product-then-subtract, exactly like np.outer followed by -=
+    ca = -1.0;
+    cp = 0x7fffffff;
+    cr = -1;
     for (int r = tid; r < nloc; r += PANEL_THREADS) {
-      if (pos[r] < 0) continue;
+      const int pr = pos[r];
+      if (pr < 0) continue;
       const double l = sm[t * R + r] / piv;
       sm[t * R + r] = l;
-      for (int c = t + 1; c < w; ++c) {
+      int c = t + 1;
+      if (c < w) {
+        const double x = __dsub_rn(sm[c * R + r], __dmul_rn(l, sh.urow[c]));
+        sm[c * R + r] = x;
+        const double ax = fabs(x);
+        gmax = fmax(gmax, ax);
+        if (better(ax, pr, ca, cp)) {
+          ca = ax;
+          cp = pr;
+          cr = r;
+        }
+      }
+#pragma unroll 4
+      for (c = t + 2; c < w; ++c) {
         const double x = __dsub_rn(sm[c * R + r], __dmul_rn(l, sh.urow[c]));
         sm[c * R + r] = x;
         gmax = fmax(gmax, fabs(x));
       }
     }
-    __syncthreads();
+    if (p.dbg && tid == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 5, (unsigned long long)(_n - _tp)); _tp = _n; }
   }
+  __syncthreads();
   // rows go straight to their final positions (pivot row of step t -> t,
   // displaced row -> its logical position); every moved row is listed so the
   // same interchanges can be applied to the other columns by a gather.
@@ -323,72 +351,35 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
   }
 }
 
-// ------------------------------------------------- interchanges -> gather list
-// Simulates LAPACK's sequential interchanges ipiv[t0..t0+S) on row indices and
-// emits (dst, src) pairs: new_row[dst] = old_row[src].  Single thread; the
-// out-of-block positions live in a small open-addressing table.
-__global__ void compose_swaps_kernel(const int32_t* __restrict__ ipiv, int64_t t0, int S,
-                                     int32_t* dst, int32_t* src, int32_t* count) {
-  constexpr int H = 4096;
-  __shared__ int32_t cur[SWAP_MAX / 2];
-  __shared__ int32_t hkey[H];
-  __shared__ int32_t hval[H];
-  for (int i = threadIdx.x; i < H; i += blockDim.x) hkey[i] = -1;
-  for (int i = threadIdx.x; i < S; i += blockDim.x) cur[i] = (int32_t)(t0 + i);
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-  auto slot = [&](int32_t key) {
-    unsigned h = ((unsigned)key * 2654435761u) & (H - 1);
-    while (hkey[h] != -1 && hkey[h] != key) h = (h + 1) & (H - 1);
-    return h;
-  };
-  for (int t = 0; t < S; ++t) {
-    const int32_t pr = ipiv[t0 + t];
-    if (pr == t0 + t) continue;
-    const int32_t a = cur[t];
-    int32_t b;
-    if (pr < t0 + S) {
-      b = cur[pr - t0];
-      cur[pr - t0] = a;
-    } else {
-      const unsigned h = slot(pr);
-      b = (hkey[h] == pr) ? hval[h] : pr;
-      hkey[h] = pr;
-      hval[h] = a;
-    }
-    cur[t] = b;
-  }
-  int n = 0;
-  for (int i = 0; i < S; ++i)
-    if (cur[i] != t0 + i) {
-      dst[n] = (int32_t)(t0 + i);
-      src[n] = cur[i];
-      ++n;
-    }
-  for (int h = 0; h < H; ++h)
-    if (hkey[h] != -1 && hval[h] != hkey[h]) {
-      dst[n] = hkey[h];
-      src[n] = hval[h];
-      ++n;
-    }
-  *count = n;
-}
-
-// Apply a gather list to columns [c0a,c1a) U [c0b,c1b): read all, then write.
+// Apply a gather list (<= 2*PANEL_W entries) to columns [c0a,c1a) U [c0b,c1b):
+// one warp per column, entries staged in registers (read all, then write).
+constexpr int LIST_PER_LANE = (2 * PANEL_W + 31) / 32;
 __global__ void laswp_gather_kernel(double* __restrict__ a, int64_t lda, const int32_t* dst,
                                     const int32_t* src, const int32_t* count, int64_t c0a,
                                     int64_t c1a, int64_t c0b, int64_t c1b) {
-  __shared__ double buf[SWAP_MAX];
   const int cnt = *count;
   if (cnt == 0) return;
+  const int lane = threadIdx.x & 31;
+  int d[LIST_PER_LANE], sidx[LIST_PER_LANE];
+#pragma unroll
+  for (int i = 0; i < LIST_PER_LANE; ++i) {
+    const int e = lane + 32 * i;
+    d[i] = e < cnt ? dst[e] : -1;
+    sidx[i] = e < cnt ? src[e] : 0;
+  }
   const int64_t na = c1a - c0a, nbb = c1b - c0b;
-  for (int64_t ci = blockIdx.x; ci < na + nbb; ci += gridDim.x) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t ci = warp; ci < na + nbb; ci += nwarps) {
     const int64_t col = ci < na ? c0a + ci : c0b + (ci - na);
     double* colp = a + col * lda;
-    for (int e = threadIdx.x; e < cnt; e += blockDim.x) buf[e] = colp[src[e]];
-    __syncthreads();
-    for (int e = threadIdx.x; e < cnt; e += blockDim.x) colp[dst[e]] = buf[e];
-    __syncthreads();
+    double v[LIST_PER_LANE];
+#pragma unroll
+    for (int i = 0; i < LIST_PER_LANE; ++i) v[i] = d[i] >= 0 ? colp[sidx[i]] : 0.0;
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < LIST_PER_LANE; ++i)
+      if (d[i] >= 0) colp[d[i]] = v[i];
   }
 }
 
@@ -680,7 +671,8 @@ int apply_list(double* a, int64_t lda, const LuWs& ws, int64_t c0a, int64_t c1a,
     cudaStream_t st;
     ~Stop() { prof_stop(tag, st, PROF_LASWP, 0.0); }
   } stop{prof_start(st), st};
-  int64_t blocks = ncols < sm_count() * 8 ? ncols : sm_count() * 8;
+  int64_t blocks = ceil_div(ncols, 8);
+  if (blocks > sm_count() * 16) blocks = sm_count() * 16;
   laswp_gather_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, lda, ws.swap_dst, ws.swap_src,
                                                         ws.swap_cnt, c0a, c1a, c0b, c1b);
   OZ_CHECK_LAUNCH();
@@ -760,6 +752,7 @@ int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int32_t* 
   pa.list_dst = ws.swap_dst;
   pa.list_src = ws.swap_src;
   pa.list_cnt = ws.swap_cnt;
+  pa.dbg = panel_dbg();
   OZ_CHECK_CUDA(cudaMemsetAsync(ws.swap_cnt, 0, sizeof(int32_t), st));
   OZ_CHECK_CUDA(cudaMemsetAsync(ws.bar, 0, sizeof(GridBar), st));
   void* args[] = {&pa};
@@ -844,6 +837,15 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
     }
     // finalized U rows of this panel: triu(lu[j:j+jb, j:]) (solve.py:135-137)
     OZ_TRY(max_abs(a + j * lda + j, jb, n - j, 1, lda, 1, 0, ws.bits, st));
+  }
+  if (unsigned long long* dbg = panel_dbg()) {
+    // debug: per-phase cycles of the panel steps, summed over all CTAs
+    cudaStreamSynchronize(st);
+    unsigned long long h[8] = {0};
+    cudaMemcpy(h, dbg, sizeof(h), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "panel phases (Mcycles summed over CTAs): publish %.1f barrier %.1f reduce %.1f urow %.1f book %.1f update %.1f\n",
+            h[0] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6, h[4] / 1e6, h[5] / 1e6);
+    cudaMemset(dbg, 0, sizeof(h));
   }
   finalize_stats_kernel<<<1, 1, 0, st>>>(ws.bits, stats);
   OZ_CHECK_LAUNCH();

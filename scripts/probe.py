@@ -53,7 +53,7 @@ def lu_probe(n, nb, backends):
 
 if __name__ == "__main__":
     what = sys.argv[1]
-    if what == "gemm1":
+    if what in ("gemm1", "lu1"):
         pass
     elif what == "gemm":
         gemm_probe(int(sys.argv[2]), [int(k) for k in sys.argv[3].split(",")])
@@ -76,3 +76,12 @@ def gemm_once(m, n, K, k, reps=2):
 
 if __name__ == "__main__" and sys.argv[1] == "gemm1":
     gemm_once(*[int(v) for v in sys.argv[2:6]])
+
+
+if __name__ == "__main__" and sys.argv[1] == "lu1":
+    n, nb, k = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
+    a = generate_device(0, n, seed=99, layout="F")
+    bk = oz.GemmBackend.int8(k) if k > 0 else oz.GemmBackend.native()
+    r = factor_device(a, nb, bk)
+    torch.cuda.synchronize()
+    print("lu1 done info", int(r[2].item()))
