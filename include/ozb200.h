@@ -105,6 +105,12 @@ int oz_gemm_emu(int64_t m, int64_t n, int64_t inner,
                 double alpha, double beta, double* c, int64_t ldc, int c_is_input,
                 unsigned long long* growth_max, void* stream);
 
+/* Host-only: the exact-level grouping plan oz_gemm_emu uses (see
+ * csrc/gemm_emu.cu build_groups).  Returns the group count; gstart[0..G] are
+ * pair offsets, gshift[0..G) the (i+j)*q of each group. */
+int oz_plan_groups(int npairs, const int32_t* pair_shift, int64_t inner, int32_t* gstart,
+                   int32_t* gshift);
+
 /* One slice-pair product as raw INT32 (debug/parity: test_gemm.py:218-240). */
 int oz_gemm_pair_i32(int64_t m, int64_t n, int64_t inner,
                      const int8_t* a_slice, int64_t a_ld,

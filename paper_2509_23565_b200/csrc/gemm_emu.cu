@@ -545,3 +545,17 @@ extern "C" int oz_gemm_pair_i32(int64_t m, int64_t n, int64_t inner, const int8_
   OZ_TRY(make_slice_map(&tb, b_slice, inner, n, b_ld, round_up(n * b_ld, 16), 1));
   return launch(ta, tb, p, as_stream(stream));
 }
+
+// Host-only: expose the exact-level grouping plan (for tests / introspection).
+// gstart must hold npairs+1 entries; returns the number of groups.
+extern "C" int oz_plan_groups(int npairs, const int32_t* pair_shift, int64_t inner,
+                              int32_t* gstart, int32_t* gshift) {
+  using namespace oz;
+  using namespace oz::emu;
+  OZ_REQUIRE(npairs >= 1 && npairs <= MAX_PAIRS, OZ_INVALID_PARAMS, "npairs out of range");
+  Params p{};
+  build_groups(p, pair_shift, npairs, inner);
+  for (int g = 0; g <= p.ngroups; ++g) gstart[g] = p.gstart[g];
+  for (int g = 0; g < p.ngroups; ++g) gshift[g] = p.gshift[g];
+  return p.ngroups;
+}
