@@ -359,6 +359,284 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+
+// =====================================================================
+// CTA-pair variant (cta_group::2): the pair computes a 256 x 128 tile; each
+// CTA stages its own 128 rows of A and one half (64 rows) of B, the leader
+// issues M=256 MMAs that read both CTAs' shared memory, and each CTA's
+// epilogue owns its 128 x 128 block.  Per SM this ingests 24 KB per 256
+// MMA-cycles instead of 32 KB (the single-CTA kernel is ingress-bound, see
+// profiles/r01_mma_microbench.txt).
+// =====================================================================
+constexpr int P_BM = 256;
+constexpr int P_BN = 128;
+constexpr int P_STAGES = 8;
+constexpr int P_A_BYTES = 128 * BK;
+constexpr int P_B_BYTES = (P_BN / 2) * BK;
+constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
+constexpr size_t P_SMEM_BYTES = 1024 + (size_t)P_STAGES * P_STAGE_BYTES + 256;
+constexpr uint32_t P_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(P_BN >> 3) << 17) |
+                             ((uint32_t)(P_BM >> 4) << 24);
+constexpr int P_EPI_ARRIVALS = 2 * (NUM_THREADS / 32 - EPI_WARP0);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+// TMA into this CTA's shared memory; the transaction bytes land on the
+// leader CTA's barrier (peer bit cleared), as in CUTLASS's 2SM loads.
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map,
+                                                 uint32_t bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void pair_tile_coords(const Params& p, int t, int& mt, int& nt) {
+  tile_coords(p, t, mt, nt);  // same grouped raster, on pair tiles (num_m_tiles in 256 rows)
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    emu_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+                         const __grid_constant__ CUtensorMap tmB, const __grid_constant__ Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + P_STAGES * P_A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + P_STAGES;
+  uint64_t* tfull = bars + 2 * P_STAGES;
+  uint64_t* tempty = bars + 2 * P_STAGES + NUM_ACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * P_STAGES + 2 * NUM_ACC);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P_STAGES; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int b = 0; b < NUM_ACC; ++b) {
+      mbar_init(smem_u32(&tfull[b]), 1);
+      mbar_init(smem_u32(&tempty[b]), P_EPI_ARRIVALS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp < EPI_WARP0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+  }
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < p.num_tiles; t += ncl) {
+        int mt, nt;
+        pair_tile_coords(p, t, mt, nt);
+        const int arow = mt * P_BM + (int)rank * 128;
+        const int brow = nt * P_BN + (int)rank * (P_BN / 2);
+        for (int q = 0; q < p.npairs; ++q) {
+          const int sa = p.pa[q], sb = p.pb[q];
+          for (int kb = 0; kb < p.nkb; ++kb) {
+            mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+            const uint32_t fb = smem_u32(&full[stage]);
+            if (leader) mbar_expect_tx(fb, 2 * P_STAGE_BYTES);
+            const uint32_t fb_leader = mapa_shared(fb, 0);  // both CTAs signal the leader
+            tma_load_3d_pair(smem_u32(smA + stage * P_A_BYTES), &tmA, fb_leader, kb * BK, arow,
+                             sa);
+            tma_load_3d_pair(smem_u32(smB + stage * P_B_BYTES), &tmB, fb_leader, kb * BK, brow,
+                             sb);
+            if (++stage == P_STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (leader CTA only)
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t it = 0;
+      for (int t = cid; t < p.num_tiles; t += ncl) {
+        for (int g = 0; g < p.ngroups; ++g, ++it) {
+          const uint32_t buf = it % NUM_ACC, aph = (it / NUM_ACC) & 1;
+          mbar_wait(smem_u32(&tempty[buf]), aph ^ 1);
+          tc_fence_after();
+          const uint32_t dtmem = tmem_base + buf * P_BN;
+          for (int q = p.gstart[g]; q < p.gstart[g + 1]; ++q) {
+            const bool first_pair = q == p.gstart[g];
+            for (int kb = 0; kb < p.nkb; ++kb) {
+              mbar_wait(smem_u32(&full[stage]), phase);
+              tc_fence_after();
+              const uint32_t a0 = smem_u32(smA + stage * P_A_BYTES);
+              const uint32_t b0 = smem_u32(smB + stage * P_B_BYTES);
+#pragma unroll
+              for (int kk = 0; kk < BK / 32; ++kk) {
+                tc_mma_i8_pair(dtmem, sdesc(a0 + kk * 32), sdesc(b0 + kk * 32), P_IDESC,
+                               (first_pair && (kb | kk) == 0) ? 0u : 1u);
+              }
+              tc_commit_pair(smem_u32(&empty[stage]));
+              if (++stage == P_STAGES) {
+                stage = 0;
+                phase ^= 1;
+              }
+            }
+          }
+          tc_commit_pair(smem_u32(&tfull[buf]));
+        }
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // --------------------------------------------------------------- epilogue
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+    const int ew = warp - EPI_WARP0;
+    const int quad = warp & 3;
+    const int half = ew >> 2;
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    double gmax = 0.0;
+    uint32_t it = 0;
+    for (int t = cid; t < p.num_tiles; t += ncl) {
+      int mt, nt;
+      pair_tile_coords(p, t, mt, nt);
+      double acc[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) acc[i] = 0.0;
+      const int row = mt * P_BM + (int)rank * 128 + quad * 32 + lane;
+      const int col0 = nt * P_BN + half * 64;
+      for (int q = 0; q < p.ngroups; ++q, ++it) {
+        const uint32_t buf = it % NUM_ACC, aph = (it / NUM_ACC) & 1;
+        mbar_wait(smem_u32(&tfull[buf]), aph);
+        tc_fence_after();
+        const double s = pow2(-(int)p.gshift[q]);
+        const uint32_t taddr = tmem_base + lane_base + buf * P_BN + half * 64;
+#pragma unroll
+        for (int c = 0; c < 64; c += 16) {
+          uint32_t v[16];
+          tmem_ld16(taddr + c, v);
+          tmem_wait_ld();
+          if (p.debug_out != nullptr) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int col = col0 + c + i;
+              if (row < p.m && col < p.n) p.debug_out[(int64_t)col * p.ldo + row] = (int32_t)v[i];
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[c + i] = fma(i32_to_f64(v[i]), s, acc[c + i]);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          const uint32_t local = smem_u32(&tempty[buf]);
+          if (leader) mbar_arrive(local);
+          else mbar_arrive_remote(mapa_shared(local, 0));
+        }
+      }
+      if (p.debug_out != nullptr) continue;
+      if (row < p.m) {
+        const int er = p.expA[row];
+        const bool use_c = p.c_is_input && p.beta != 0.0;
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+          int eb[16];
+          double cv[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int col = col0 + c0 + i;
+            const bool ok = col < p.n;
+            eb[i] = ok ? __ldg(p.expB + col) : 0;
+            cv[i] = (ok && use_c) ? p.c[(int64_t)col * p.ldc + row] : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int col = col0 + c0 + i;
+            if (col < p.n) {
+              const double ab = ldexp_exact(acc[c0 + i], er + eb[i]);
+              double out = __dmul_rn(p.alpha, ab);
+              if (use_c) out = __dadd_rn(out, __dmul_rn(p.beta, cv[i]));
+              p.c[(int64_t)col * p.ldc + row] = out;
+              gmax = fmax(gmax, fabs(out));
+            }
+          }
+        }
+      }
+    }
+    if (p.growth != nullptr) {
+      gmax = warp_max(gmax);
+      if (lane == 0 && gmax > 0.0) atomic_max_abs(p.growth, gmax);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
 // ------------------------------------------------------------------ host side
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -374,7 +652,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 int make_slice_map(CUtensorMap* map, const int8_t* base, int64_t inner, int64_t rows,
-                   int64_t ld, int64_t sstride, int nslices) {
+                   int64_t ld, int64_t sstride, int nslices, int box_rows = BM) {
   auto fn = encode_fn();
   OZ_REQUIRE(fn != nullptr, OZ_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
   OZ_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15) == 0, OZ_INVALID_PARAMS,
@@ -383,7 +661,7 @@ int make_slice_map(CUtensorMap* map, const int8_t* base, int64_t inner, int64_t 
              "slice strides must be multiples of 16 bytes");
   cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)nslices};
   cuuint64_t strides[2] = {(cuuint64_t)ld, (cuuint64_t)sstride};
-  cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)BM, 1};
+  cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -434,6 +712,31 @@ void build_groups(Params& p, const int32_t* shift, int npairs, int64_t inner) {
   }
   p.gstart[g] = (uint16_t)npairs;
   p.ngroups = g;
+}
+
+bool use_pair_kernel() {
+  static const bool single = getenv("OZ_GEMM_1CTA") != nullptr;  // A/B switch for tuning
+  return !single;
+}
+
+int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    OZ_CHECK_CUDA(cudaFuncSetAttribute(emu_gemm_pair_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)P_SMEM_BYTES));
+    attr_set = true;
+  }
+  p.num_m_tiles = (int)ceil_div(p.m, P_BM);
+  p.num_n_tiles = (int)ceil_div(p.n, P_BN);
+  p.num_tiles = p.num_m_tiles * p.num_n_tiles;
+  p.nkb = (int)ceil_div(p.inner, BK);
+  int grid = sm_count() & ~1;
+  if (const char* g = getenv("OZ_GEMM_GRID")) grid = atoi(g) > 0 ? (atoi(g) & ~1) : grid;
+  if (grid > 2 * p.num_tiles) grid = 2 * p.num_tiles;
+  emu_gemm_pair_kernel<<<grid, NUM_THREADS, P_SMEM_BYTES, st>>>(ta, tb, p);
+  OZ_CHECK_LAUNCH();
+  return OZ_OK;
 }
 
 int launch(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStream_t st) {
@@ -496,9 +799,11 @@ int gemm_emu_launch(int64_t m, int64_t n, int64_t inner, const int8_t* a_slices,
   p.beta = beta;
   p.growth = growth;
   CUtensorMap ta, tb;
-  OZ_TRY(make_slice_map(&ta, a_slices, inner, m, a_ld, a_sstride, a_nslices));
-  OZ_TRY(make_slice_map(&tb, b_slices, inner, n, b_ld, b_sstride, b_nslices));
-  return launch(ta, tb, p, st);
+  const bool pair = use_pair_kernel();
+  OZ_TRY(make_slice_map(&ta, a_slices, inner, m, a_ld, a_sstride, a_nslices, BM));
+  OZ_TRY(make_slice_map(&tb, b_slices, inner, n, b_ld, b_sstride, b_nslices,
+                        pair ? P_BN / 2 : BN));
+  return pair ? launch_pair(ta, tb, p, st) : launch(ta, tb, p, st);
 }
 
 }  // namespace oz
@@ -541,9 +846,11 @@ extern "C" int oz_gemm_pair_i32(int64_t m, int64_t n, int64_t inner, const int8_
   p.ldo = ldo;
   p.alpha = 1.0;
   CUtensorMap ta, tb;
-  OZ_TRY(make_slice_map(&ta, a_slice, inner, m, a_ld, round_up(m * a_ld, 16), 1));
-  OZ_TRY(make_slice_map(&tb, b_slice, inner, n, b_ld, round_up(n * b_ld, 16), 1));
-  return launch(ta, tb, p, as_stream(stream));
+  const bool pair = use_pair_kernel();
+  OZ_TRY(make_slice_map(&ta, a_slice, inner, m, a_ld, round_up(m * a_ld, 16), 1, BM));
+  OZ_TRY(make_slice_map(&tb, b_slice, inner, n, b_ld, round_up(n * b_ld, 16), 1,
+                        pair ? P_BN / 2 : BN));
+  return pair ? launch_pair(ta, tb, p, as_stream(stream)) : launch(ta, tb, p, as_stream(stream));
 }
 
 // Host-only: expose the exact-level grouping plan (for tests / introspection).
