@@ -36,6 +36,7 @@ constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int BK = 128;  // bytes of K per stage (one 128B swizzle atom)
 constexpr int STAGES = 6;
+constexpr int SGROUP = 3;  // stages released per tcgen05.commit (>= 12 MMAs per commit)
 constexpr int NUM_ACC = 4;
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_THREADS = 384;
@@ -132,6 +133,33 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Warp-uniform issue helpers: the whole warp runs the issue loops (so loop
+// state stays in uniform registers) and elect.sync picks the issuing lane.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+__device__ __forceinline__ void tc_mma_i8_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                                uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          bar)
+      : "memory");
+}
+
 // K-major, 128B-swizzled shared-memory matrix descriptor (8-row groups 1024B apart).
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
@@ -210,62 +238,64 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        int mt, nt;
-        tile_coords(p, t, mt, nt);
-        for (int q = 0; q < p.npairs; ++q) {
-          const int sa = p.pa[q], sb = p.pb[q];
-          for (int kb = 0; kb < p.nkb; ++kb) {
-            mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      int mt, nt;
+      tile_coords(p, t, mt, nt);
+      for (int q = 0; q < p.npairs; ++q) {
+        const int sa = p.pa[q], sb = p.pb[q];
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          if (stage % SGROUP == 0) mbar_wait(smem_u32(&empty[stage / SGROUP]), phase ^ 1);
+          if (elect_one()) {
             const uint32_t fb = smem_u32(&full[stage]);
             mbar_expect_tx(fb, STAGE_BYTES);
             tma_load_3d(smem_u32(smA + stage * TILE_BYTES), &tmA, fb, kb * BK, mt * BM, sa);
             tma_load_3d(smem_u32(smB + stage * TILE_BYTES), &tmB, fb, kb * BK, nt * BN, sb);
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
+          }
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
           }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      uint32_t it = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        for (int g = 0; g < p.ngroups; ++g, ++it) {
-          const uint32_t buf = it % NUM_ACC, aph = (it / NUM_ACC) & 1;
-          mbar_wait(smem_u32(&tempty[buf]), aph ^ 1);
-          tc_fence_after();
-          const uint32_t dtmem = tmem_base + buf * BN;
-          // every pair of an exact group accumulates into the same INT32 tile
-          for (int q = p.gstart[g]; q < p.gstart[g + 1]; ++q) {
-            const bool first_pair = q == p.gstart[g];
-            for (int kb = 0; kb < p.nkb; ++kb) {
-              mbar_wait(smem_u32(&full[stage]), phase);
-              tc_fence_after();
-              const uint32_t a0 = smem_u32(smA + stage * TILE_BYTES);
-              const uint32_t b0 = smem_u32(smB + stage * TILE_BYTES);
+    const uint64_t adesc0 = sdesc(smem_u32(smA));
+    const uint64_t bdesc0 = sdesc(smem_u32(smB));
+    int stage = 0;
+    uint32_t phase = 0;
+    uint32_t it = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (int g = 0; g < p.ngroups; ++g, ++it) {
+        const uint32_t buf = it % NUM_ACC, aph = (it / NUM_ACC) & 1;
+        mbar_wait(smem_u32(&tempty[buf]), aph ^ 1);
+        tc_fence_after();
+        const uint32_t dtmem = tmem_base + buf * BN;
+        // every pair of an exact group accumulates into the same INT32 tile
+        for (int q = p.gstart[g]; q < p.gstart[g + 1]; ++q) {
+          const bool first_pair = q == p.gstart[g];
+          for (int kb = 0; kb < p.nkb; ++kb) {
+            mbar_wait(smem_u32(&full[stage]), phase);
+            tc_fence_after();
+            const uint64_t soff = (uint64_t)((stage * TILE_BYTES) >> 4);
 #pragma unroll
-              for (int kk = 0; kk < BK / 32; ++kk) {
-                tc_mma_i8(dtmem, sdesc(a0 + kk * 32), sdesc(b0 + kk * 32), IDESC,
-                          (first_pair && (kb | kk) == 0) ? 0u : 1u);
-              }
-              tc_commit(smem_u32(&empty[stage]));
-              if (++stage == STAGES) {
-                stage = 0;
-                phase ^= 1;
-              }
+            for (int kk = 0; kk < BK / 32; ++kk) {
+              tc_mma_i8_elect(dtmem, adesc0 + soff + 2 * kk, bdesc0 + soff + 2 * kk, IDESC,
+                              (first_pair && (kb | kk) == 0) ? 0u : 1u);
+            }
+            if (stage % SGROUP == SGROUP - 1) tc_commit_elect(smem_u32(&empty[stage / SGROUP]));
+            __syncwarp();
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
             }
           }
-          tc_commit(smem_u32(&tfull[buf]));
         }
+        tc_commit_elect(smem_u32(&tfull[buf]));
+        __syncwarp();
       }
     }
   } else if (warp >= EPI_WARP0) {
@@ -371,6 +401,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 constexpr int P_BM = 256;
 constexpr int P_BN = 128;
 constexpr int P_STAGES = 8;
+constexpr int P_SGROUP = 4;  // 16 MMAs per tcgen05.commit
 constexpr int P_A_BYTES = 128 * BK;
 constexpr int P_B_BYTES = (P_BN / 2) * BK;
 constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
@@ -409,17 +440,19 @@ __device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap
 }
 __device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
   asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-      " [%0], %1;" ::"r"(bar),
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n\t}" ::"r"(bar),
       "h"((uint16_t)3)
       : "memory");
 }
 __device__ __forceinline__ void tc_mma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                                uint32_t idesc, uint32_t accumulate) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
@@ -482,18 +515,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   }
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = cid; t < p.num_tiles; t += ncl) {
-        int mt, nt;
-        pair_tile_coords(p, t, mt, nt);
-        const int arow = mt * P_BM + (int)rank * 128;
-        const int brow = nt * P_BN + (int)rank * (P_BN / 2);
-        for (int q = 0; q < p.npairs; ++q) {
-          const int sa = p.pa[q], sb = p.pb[q];
-          for (int kb = 0; kb < p.nkb; ++kb) {
-            mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = cid; t < p.num_tiles; t += ncl) {
+      int mt, nt;
+      pair_tile_coords(p, t, mt, nt);
+      const int arow = mt * P_BM + (int)rank * 128;
+      const int brow = nt * P_BN + (int)rank * (P_BN / 2);
+      for (int q = 0; q < p.npairs; ++q) {
+        const int sa = p.pa[q], sb = p.pb[q];
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          if (stage % P_SGROUP == 0) mbar_wait(smem_u32(&empty[stage / P_SGROUP]), phase ^ 1);
+          if (elect_one()) {
             const uint32_t fb = smem_u32(&full[stage]);
             if (leader) mbar_expect_tx(fb, 2 * P_STAGE_BYTES);
             const uint32_t fb_leader = mapa_shared(fb, 0);  // both CTAs signal the leader
@@ -501,17 +534,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                              sa);
             tma_load_3d_pair(smem_u32(smB + stage * P_B_BYTES), &tmB, fb_leader, kb * BK, brow,
                              sb);
-            if (++stage == P_STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
+          }
+          __syncwarp();
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
           }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (leader CTA only)
-    if (leader && lane == 0) {
+    if (leader) {
+      const uint64_t adesc0 = sdesc(smem_u32(smA));
+      const uint64_t bdesc0 = sdesc(smem_u32(smB));
       int stage = 0;
       uint32_t phase = 0;
       uint32_t it = 0;
@@ -526,14 +562,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             for (int kb = 0; kb < p.nkb; ++kb) {
               mbar_wait(smem_u32(&full[stage]), phase);
               tc_fence_after();
-              const uint32_t a0 = smem_u32(smA + stage * P_A_BYTES);
-              const uint32_t b0 = smem_u32(smB + stage * P_B_BYTES);
+              const uint64_t aoff = (uint64_t)((stage * P_A_BYTES) >> 4);
+              const uint64_t boff = (uint64_t)((stage * P_B_BYTES) >> 4);
 #pragma unroll
               for (int kk = 0; kk < BK / 32; ++kk) {
-                tc_mma_i8_pair(dtmem, sdesc(a0 + kk * 32), sdesc(b0 + kk * 32), P_IDESC,
+                tc_mma_i8_pair(dtmem, adesc0 + aoff + 2 * kk, bdesc0 + boff + 2 * kk, P_IDESC,
                                (first_pair && (kb | kk) == 0) ? 0u : 1u);
               }
-              tc_commit_pair(smem_u32(&empty[stage]));
+              if (stage % P_SGROUP == P_SGROUP - 1)
+                tc_commit_pair(smem_u32(&empty[stage / P_SGROUP]));
+              __syncwarp();
               if (++stage == P_STAGES) {
                 stage = 0;
                 phase ^= 1;
@@ -541,6 +579,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             }
           }
           tc_commit_pair(smem_u32(&tfull[buf]));
+          __syncwarp();
         }
       }
     }
