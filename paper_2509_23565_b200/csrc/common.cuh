@@ -78,9 +78,10 @@ __device__ __forceinline__ double pow2(int e) {
 
 // ldexp that is exact (correctly rounded) for every input: multiply by an
 // exactly representable power of two when possible, fall back to ldexp().
+static __device__ __noinline__ double ldexp_slow(double x, int e) { return ldexp(x, e); }
 __device__ __forceinline__ double ldexp_exact(double x, int e) {
   if (e >= -1022 && e <= 1023) return __dmul_rn(x, pow2(e));
-  return ldexp(x, e);
+  return ldexp_slow(x, e);  // out-of-line: keeps unrolled epilogues small
 }
 
 // frexp exponent of |x| (x finite, x != 0): x = m * 2^e with 0.5 <= m < 1.

@@ -66,6 +66,7 @@ struct Params {
   int32_t* debug_out;  // pair-debug mode: raw INT32 product
   int64_t ldo;
   int ngroups;
+  int group_m;  // raster band height in tiles
   uint8_t pa[MAX_PAIRS];
   uint8_t pb[MAX_PAIRS];
   uint16_t gshift[MAX_PAIRS];      // (i+j)*q of the group's pairs
@@ -129,6 +130,18 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
         "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -177,11 +190,11 @@ __device__ __forceinline__ double i32_to_f64(uint32_t v) {
 }
 
 __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mt, int& nt) {
-  const int per_group = GROUP_M * p.num_n_tiles;
+  const int per_group = p.group_m * p.num_n_tiles;
   const int g = t / per_group;
-  const int first_m = g * GROUP_M;
+  const int first_m = g * p.group_m;
   int gm = p.num_m_tiles - first_m;
-  gm = gm < GROUP_M ? gm : GROUP_M;
+  gm = gm < p.group_m ? gm : p.group_m;
   const int r = t - g * per_group;
   mt = first_m + r % gm;
   nt = r / gm;
@@ -425,8 +438,7 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
   return r;
 }
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // TMA into this CTA's shared memory; the transaction bytes land on the
 // leader CTA's barrier (peer bit cleared), as in CUTLASS's 2SM loads.
@@ -461,6 +473,7 @@ __device__ __forceinline__ void pair_tile_coords(const Params& p, int t, int& mt
   tile_coords(p, t, mt, nt);  // same grouped raster, on pair tiles (num_m_tiles in 256 rows)
 }
 
+template <bool kDebug>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     emu_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                          const __grid_constant__ CUtensorMap tmB, const __grid_constant__ Params p) {
@@ -590,6 +603,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const int quad = warp & 3;
     const int half = ew >> 2;
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    // TMEM-slot releases go to the leader's barrier as plain remote arrives:
+    // tcgen05.wait::ld + fence::before_thread_sync already order our reads.
+    const uint32_t tempty_leader = mapa_shared(smem_u32(tempty), 0);
     double gmax = 0.0;
     uint32_t it = 0;
     for (int t = cid; t < p.num_tiles; t += ncl) {
@@ -604,58 +620,60 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const uint32_t buf = it % NUM_ACC, aph = (it / NUM_ACC) & 1;
         mbar_wait(smem_u32(&tfull[buf]), aph);
         tc_fence_after();
-        const double s = pow2(-(int)p.gshift[q]);
         const uint32_t taddr = tmem_base + lane_base + buf * P_BN + half * 64;
-#pragma unroll
-        for (int c = 0; c < 64; c += 16) {
-          uint32_t v[16];
-          tmem_ld16(taddr + c, v);
-          tmem_wait_ld();
-          if (p.debug_out != nullptr) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int col = col0 + c + i;
-              if (row < p.m && col < p.n) p.debug_out[(int64_t)col * p.ldo + row] = (int32_t)v[i];
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) acc[c + i] = fma(i32_to_f64(v[i]), s, acc[c + i]);
-          }
-        }
+        uint32_t v[64];
+        tmem_ld32(taddr, v);
+        tmem_ld32(taddr + 32, v + 32);
+        tmem_wait_ld();
+        // the slot is free as soon as its values sit in registers
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          const uint32_t local = smem_u32(&tempty[buf]);
-          if (leader) mbar_arrive(local);
-          else mbar_arrive_remote(mapa_shared(local, 0));
+        if (lane == 0) mbar_arrive_remote(tempty_leader + buf * 8);
+        if (kDebug) {
+#pragma unroll 4
+          for (int i = 0; i < 64; ++i) {
+            const int col = col0 + i;
+            if (row < p.m && col < p.n) p.debug_out[(int64_t)col * p.ldo + row] = (int32_t)v[i];
+          }
+        } else {
+          const double s = pow2(-(int)p.gshift[q]);
+#pragma unroll
+          for (int i = 0; i < 64; ++i) acc[i] = fma(i32_to_f64(v[i]), s, acc[i]);
         }
       }
-      if (p.debug_out != nullptr) continue;
+      if (kDebug) continue;
       if (row < p.m) {
+        // final pass, 8 columns per (rolled) iteration; the accumulator
+        // registers shift down by 8 after each chunk so indices stay static
         const int er = p.expA[row];
         const bool use_c = p.c_is_input && p.beta != 0.0;
+        const int ncols = min(64, p.n - col0);
+        const int64_t ldc = p.ldc;
+        double* cbase = p.c + (int64_t)col0 * ldc + row;
+        const int32_t* ebase = p.expB + col0;
+#pragma unroll 1
+        for (int c0 = 0; c0 < ncols; c0 += 8) {
+          int eb[8];
+          double cv[8];
+          double* cp = cbase + (int64_t)c0 * ldc;
 #pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 16) {
-          int eb[16];
-          double cv[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int col = col0 + c0 + i;
-            const bool ok = col < p.n;
-            eb[i] = ok ? __ldg(p.expB + col) : 0;
-            cv[i] = (ok && use_c) ? p.c[(int64_t)col * p.ldc + row] : 0.0;
+          for (int i = 0; i < 8; ++i) {
+            const bool ok = c0 + i < ncols;
+            eb[i] = ok ? __ldg(ebase + c0 + i) : 0;
+            cv[i] = (ok && use_c) ? cp[i * ldc] : 0.0;
           }
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int col = col0 + c0 + i;
-            if (col < p.n) {
-              const double ab = ldexp_exact(acc[c0 + i], er + eb[i]);
+          for (int i = 0; i < 8; ++i) {
+            if (c0 + i < ncols) {
+              const double ab = ldexp_exact(acc[i], er + eb[i]);
               double out = __dmul_rn(p.alpha, ab);
               if (use_c) out = __dadd_rn(out, __dmul_rn(p.beta, cv[i]));
-              p.c[(int64_t)col * p.ldc + row] = out;
+              cp[i * ldc] = out;
               gmax = fmax(gmax, fabs(out));
             }
           }
+#pragma unroll
+          for (int i = 0; i < 56; ++i) acc[i] = acc[i + 8];
         }
       }
     }
@@ -761,7 +779,10 @@ bool use_pair_kernel() {
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    OZ_CHECK_CUDA(cudaFuncSetAttribute(emu_gemm_pair_kernel,
+    OZ_CHECK_CUDA(cudaFuncSetAttribute(emu_gemm_pair_kernel<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)P_SMEM_BYTES));
+    OZ_CHECK_CUDA(cudaFuncSetAttribute(emu_gemm_pair_kernel<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)P_SMEM_BYTES));
     attr_set = true;
@@ -770,10 +791,15 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStr
   p.num_n_tiles = (int)ceil_div(p.n, P_BN);
   p.num_tiles = p.num_m_tiles * p.num_n_tiles;
   p.nkb = (int)ceil_div(p.inner, BK);
+  p.group_m = GROUP_M;
+  if (const char* g = getenv("OZ_GEMM_GROUPM")) p.group_m = atoi(g) > 0 ? atoi(g) : GROUP_M;
   int grid = sm_count() & ~1;
   if (const char* g = getenv("OZ_GEMM_GRID")) grid = atoi(g) > 0 ? (atoi(g) & ~1) : grid;
   if (grid > 2 * p.num_tiles) grid = 2 * p.num_tiles;
-  emu_gemm_pair_kernel<<<grid, NUM_THREADS, P_SMEM_BYTES, st>>>(ta, tb, p);
+  if (p.debug_out != nullptr)
+    emu_gemm_pair_kernel<true><<<grid, NUM_THREADS, P_SMEM_BYTES, st>>>(ta, tb, p);
+  else
+    emu_gemm_pair_kernel<false><<<grid, NUM_THREADS, P_SMEM_BYTES, st>>>(ta, tb, p);
   OZ_CHECK_LAUNCH();
   return OZ_OK;
 }
@@ -789,6 +815,7 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStream_t
   p.num_n_tiles = (int)ceil_div(p.n, BN);
   p.num_tiles = p.num_m_tiles * p.num_n_tiles;
   p.nkb = (int)ceil_div(p.inner, BK);
+  p.group_m = GROUP_M;
   int grid = sm_count();
   if (const char* g = getenv("OZ_GEMM_GRID")) grid = atoi(g) > 0 ? atoi(g) : grid;  // tuning knob
   if (grid > p.num_tiles) grid = p.num_tiles;

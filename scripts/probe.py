@@ -53,7 +53,7 @@ def lu_probe(n, nb, backends):
 
 if __name__ == "__main__":
     what = sys.argv[1]
-    if what in ("gemm1", "lu1"):
+    if what in ("gemm1", "lu1", "kern"):
         pass
     elif what == "gemm":
         gemm_probe(int(sys.argv[2]), [int(k) for k in sys.argv[3].split(",")])
@@ -85,3 +85,30 @@ if __name__ == "__main__" and sys.argv[1] == "lu1":
     r = factor_device(a, nb, bk)
     torch.cuda.synchronize()
     print("lu1 done info", int(r[2].item()))
+
+
+if __name__ == "__main__" and sys.argv[1] == "kern":
+    # kern m n K k[,k2..] : device-resident emulated GEMM, per-phase event times
+    m, n, K = (int(v) for v in sys.argv[2:5])
+    ks = [int(v) for v in sys.argv[5].split(",")]
+    a = torch.rand((m, K), dtype=torch.float64, device="cuda") - 0.5
+    b = torch.rand((K, n), dtype=torch.float64, device="cuda") - 0.5
+    out = torch.empty((n, m), dtype=torch.float64, device="cuda").t()
+    for k in ks:
+        bk = oz.GemmBackend.int8(k)
+        npairs = k * (k + 1) // 2
+        for _ in range(2):
+            emulated_into(bk, a, b, -1.0, 1.0, out, True)
+        torch.cuda.synchronize()
+        reps = 5
+        _lib.call("oz_prof_enable", 1)
+        for _ in range(reps):
+            emulated_into(bk, a, b, -1.0, 1.0, out, True)
+        torch.cuda.synchronize()
+        prof = np.zeros(36)
+        _lib.call("oz_prof_summary", prof.ctypes.data)
+        _lib.call("oz_prof_enable", 0)
+        g_ms, s_ms = prof[0] / reps, prof[9] / reps
+        ops = 2.0 * npairs * m * n * K
+        print(f"kern m={m} n={n} K={K} k={k}: gemm {g_ms:.3f} ms {ops/g_ms/1e9:.1f} TOPS int8 "
+              f"({2.0*m*n*K/g_ms/1e9:.1f} TFLOP/s-eq), split {s_ms:.3f} ms", flush=True)
