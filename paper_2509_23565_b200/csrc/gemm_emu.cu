@@ -469,6 +469,32 @@ __device__ __forceinline__ void tc_mma_i8_pair(uint32_t tmem_d, uint64_t adesc, 
       : "memory");
 }
 
+// One K stage (4 MMAs of K=32) of the pair kernel in a single asm block: one
+// elect.sync, descriptors built from their 32-bit low words (the high word —
+// stride, version, swizzle — is constant), so ptxas emits no per-MMA vote or
+// 64-bit address arithmetic.
+__device__ __forceinline__ void tc_mma_i8_pair_stage(uint32_t tmem_d, uint32_t a_lo, uint32_t b_lo,
+                                                     uint32_t hi, uint32_t idesc,
+                                                     uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 da, db;\n\t.reg .b32 al, bl;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "mov.b64 da, {%1, %3};\n\tmov.b64 db, {%2, %3};\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], da, db, %4, p;\n\t"
+      "add.u32 al, %1, 2;\n\tadd.u32 bl, %2, 2;\n\t"
+      "mov.b64 da, {al, %3};\n\tmov.b64 db, {bl, %3};\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], da, db, %4, 1;\n\t"
+      "add.u32 al, %1, 4;\n\tadd.u32 bl, %2, 4;\n\t"
+      "mov.b64 da, {al, %3};\n\tmov.b64 db, {bl, %3};\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], da, db, %4, 1;\n\t"
+      "add.u32 al, %1, 6;\n\tadd.u32 bl, %2, 6;\n\t"
+      "mov.b64 da, {al, %3};\n\tmov.b64 db, {bl, %3};\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], da, db, %4, 1;\n\t}" ::"r"(tmem_d),
+      "r"(a_lo), "r"(b_lo), "r"(hi), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 __device__ __forceinline__ void pair_tile_coords(const Params& p, int t, int& mt, int& nt) {
   tile_coords(p, t, mt, nt);  // same grouped raster, on pair tiles (num_m_tiles in 256 rows)
 }
@@ -561,6 +587,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     if (leader) {
       const uint64_t adesc0 = sdesc(smem_u32(smA));
       const uint64_t bdesc0 = sdesc(smem_u32(smB));
+      const uint32_t a_lo0 = (uint32_t)adesc0, b_lo0 = (uint32_t)bdesc0;
+      const uint32_t desc_hi = (uint32_t)(adesc0 >> 32);  // == bdesc0 >> 32
       int stage = 0;
       uint32_t phase = 0;
       uint32_t it = 0;
@@ -575,13 +603,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             for (int kb = 0; kb < p.nkb; ++kb) {
               mbar_wait(smem_u32(&full[stage]), phase);
               tc_fence_after();
-              const uint64_t aoff = (uint64_t)((stage * P_A_BYTES) >> 4);
-              const uint64_t boff = (uint64_t)((stage * P_B_BYTES) >> 4);
-#pragma unroll
-              for (int kk = 0; kk < BK / 32; ++kk) {
-                tc_mma_i8_pair(dtmem, adesc0 + aoff + 2 * kk, bdesc0 + boff + 2 * kk, P_IDESC,
-                               (first_pair && (kb | kk) == 0) ? 0u : 1u);
-              }
+              static_assert(BK / 32 == 4, "stage issue assumes 4 MMAs per stage");
+              tc_mma_i8_pair_stage(dtmem, a_lo0 + (uint32_t)stage * (P_A_BYTES >> 4),
+                                   b_lo0 + (uint32_t)stage * (P_B_BYTES >> 4), desc_hi, P_IDESC,
+                                   (first_pair && kb == 0) ? 0u : 1u);
               if (stage % P_SGROUP == P_SGROUP - 1)
                 tc_commit_pair(smem_u32(&empty[stage / P_SGROUP]));
               __syncwarp();
