@@ -57,6 +57,10 @@ def parse():
     p.add_argument("--cpu-n", type=int, default=1024)
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--skip-native", action="store_true")
+    p.add_argument("--sweep-k", default="3,4,5,6,7,8,9",
+                   help="splits for the GEMM (D3) and LU k-sweeps; empty string skips them")
+    p.add_argument("--gemm-n", type=int, default=16384, help="D3 standalone DGEMM size")
+    p.add_argument("--sweep-lu-n", type=int, default=16384, help="LU k-sweep size")
     return p.parse_args()
 
 
@@ -175,6 +179,104 @@ def run_reference(args, rank):
                          "sample": sample},
         "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+# ---------------------------------------------------------------- k sweeps
+FP64_NOMINAL_TFLOPS = 37.0   # B200 (HGX) FP64 datasheet figure; not in MEASURED_PEAKS.json
+
+
+def _events():
+    import torch
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+def _time_device(fn, reps):
+    """Mean device time (s) of fn() over reps launches, after one warm-up call."""
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = _events()
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3 / reps
+
+
+def gemm_sweep(n, ks, int8_peak, reps=2):
+    """configs[2] (D3): standalone emulated DGEMM n^3, A = hpl_uniform(n,2),
+    B = hpl_uniform(n,3) generated in HBM, C = A @ B (alpha=1, beta=0), for each
+    k; the timed call is the full gemm() device path (split A, split B, fused
+    tcgen05 GEMM + FP64 recombine).  Native = cuBLAS DGEMM on the same A, B."""
+    import torch
+    import paper_2509_23565_b200 as oz
+    from paper_2509_23565_b200 import _dev, _lib
+    from paper_2509_23565_b200.gemm import emulated_into
+    from paper_2509_23565_b200.matgen import generate_device
+    a = generate_device(0, n, seed=2)
+    b = generate_device(0, n, seed=3)
+    out = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    fl = 2.0 * n ** 3
+    t = _time_device(lambda: _lib.call("oz_dgemm", 0, 0, n, n, n, 1.0, b.data_ptr(), n,
+                                       a.data_ptr(), n, 0.0, out.data_ptr(), n, _dev.stream()),
+                     reps)
+    res = {"workload": f"configs[2]: emulated DGEMM {n}^3, A=hpl_uniform({n},2), "
+                       f"B=hpl_uniform({n},3), device-resident, split+GEMM timed",
+           "native_fp64": {"ms": t * 1e3, "tflops": fl / t / 1e12,
+                           "frac_of_fp64_nominal": fl / t / 1e12 / FP64_NOMINAL_TFLOPS},
+           "emulated": []}
+    for k in ks:
+        bk = oz.GemmBackend.int8(k)
+        npairs = k * (k + 1) // 2
+        t = _time_device(lambda: emulated_into(bk, a, b, 1.0, 0.0, out, False), reps)
+        int8 = npairs * fl / t / 1e12
+        res["emulated"].append({"k": k, "pairs": npairs, "ms": t * 1e3,
+                                "tflops_fp64_equiv": fl / t / 1e12,
+                                "int8_tops": int8, "frac_of_int8_peak": int8 / int8_peak,
+                                "fp64_equiv_roofline_tflops": int8_peak / npairs})
+    del a, b, out
+    torch.cuda.empty_cache()
+    return res
+
+
+def lu_sweep(n, nb, ks):
+    """configs[1] at one size, k = 3..9 plus native FP64: factor + solve of
+    hpl_uniform(n, 99), b = A @ 1, with the HPL scaled residual of each run."""
+    import torch
+    import paper_2509_23565_b200 as oz
+    from paper_2509_23565_b200 import _dev, _lib
+    from paper_2509_23565_b200.matgen import generate_device
+    from paper_2509_23565_b200.solve import _report, _solve_device, factor_device, ipiv_to_perm
+    a0 = generate_device(0, n, seed=99, layout="F")
+    b0 = torch.empty((n,), dtype=torch.float64, device="cuda")
+    _lib.call("oz_row_sums", a0.data_ptr(), n, 1, n, b0.data_ptr(), _dev.stream())
+    work = torch.empty((n, n), dtype=torch.float64, device="cuda").t()
+    norms = torch.zeros((4,), dtype=torch.float64, device="cuda")
+    rows = []
+    for k in list(ks) + [0]:
+        bk = oz.GemmBackend.int8(k) if k else oz.GemmBackend.native()
+        box = {}
+
+        def step():
+            _lib.call("oz_copy2d", a0.data_ptr(), n, n, 1, n, work.data_ptr(), 1, n,
+                      _dev.stream())
+            ipiv, _stats, _info, _ws = factor_device(work, nb, bk)
+            perm = ipiv_to_perm(ipiv.cpu().numpy())
+            dperm = torch.from_numpy(perm).to("cuda", non_blocking=True)
+            box["x"], _ = _solve_device(work, dperm, b0)
+
+        t = _time_device(step, 1)
+        _lib.call("oz_residual_norms", a0.data_ptr(), n, 1, n, box["x"].data_ptr(),
+                  b0.data_ptr(), norms.data_ptr(), _dev.stream())
+        raw, na, nx, nbv = (float(v) for v in norms.cpu().numpy())
+        r = _report(raw, na, nx, nbv, n).scaled_residual
+        rows.append({"k": k if k else "fp64", "ms": t * 1e3, "tflops_fp64_equiv":
+                     flops(n) / t / 1e12, "scaled_residual": r, "passed": r < 16.0})
+    del a0, work
+    torch.cuda.empty_cache()
+    return {"workload": f"configs[1]: U(-1/2,1/2) n={n} nb={nb} factor+solve, b = A @ 1",
+            "runs": rows}
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -302,6 +404,9 @@ def run_ours(args, rank, world):
     if os.path.exists(tpath):
         with open(tpath) as f:
             traffic = json.load(f).get("emu_gemm_dram_bytes_per_launch")
+    ks = [int(v) for v in args.sweep_k.split(",") if v.strip()]
+    gsweep = gemm_sweep(args.gemm_n, ks, peak) if ks else None
+    lsweep = lu_sweep(args.sweep_lu_n, nb, ks) if ks else None
     cpu_times, cores, cpu_resid = cpu_oracle_lu(args.cpu_n, min(nb, args.cpu_n), k, reps=1)
     cpu_v = flops(args.cpu_n) / cpu_times[0] / 1e12
     clocks = clk.summary()
@@ -319,7 +424,7 @@ def run_ours(args, rank, world):
                    "flop_convention": "2/3 n^3 (harness.py:383)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "oz::emu::emu_gemm_kernel (tcgen05 kind::i8 + fused FP64 "
+                     "kernel": "oz::emu::emu_gemm_pair_kernel<false> (tcgen05.mma.cta_group::2 kind::i8 + fused FP64 "
                                "recombine); achieved = INT8 ops (2*pairs*m*n*nb) / event time",
                      "peak_source": f"2 x bf16_tflops_sustained of {peak_kind} "
                                     f"MEASURED_PEAKS.json (dense int8 = 2x bf16 on sm_100)",
@@ -334,6 +439,8 @@ def run_ours(args, rank, world):
         "scaled_residual": resid, "passed": resid < 16.0,
         "native_fp64": native,
         "breakdown": breakdown,
+        "gemm_k_sweep": gsweep,
+        "lu_k_sweep": lsweep,
     }
     print(json.dumps(out), flush=True)
 
