@@ -176,6 +176,69 @@ int oz_generate(int kind, int64_t n, int64_t depth, int64_t block, double alpha,
 int oz_copy2d(const double* src, int64_t rows, int64_t cols, int64_t src_rs, int64_t src_cs,
               double* dst, int64_t dst_rs, int64_t dst_cs, void* stream);
 
+
+/*
+ * Step-level LU (the loop of solve.py:94-140 owned by the caller; used by the
+ * distributed 1 x Q block-cyclic HPL driver).  All take the LU workspace
+ * (oz_lu_workspace_bytes(ws_n, ws_nb, ws_slices) bytes) and its shape.
+ *
+ * oz_lu_ws_init:  zero the workspace's barriers/tags (once per factorization).
+ * oz_lu_panel:    factor the m x jb panel at `a` (its diagonal corner, rows
+ *                 numbered from global row `base`) in place: partial pivoting
+ *                 with np.argmax order, division, outer-product update
+ *                 (solve.py:66-91); interchanges applied to the panel columns
+ *                 only.  ipiv[0..jb) <- global pivot rows; info <- first zero
+ *                 pivot (global column + 1); growth_bits <- max |entry| seen.
+ * oz_laswp:       apply ipiv[0..npiv) (rows k1.., global values) as
+ *                 sequential interchanges to columns [c0a,c1a) U [c0b,c1b)
+ *                 (solve.py:80-82 whole-row swaps; LAPACK dlaswp); npiv <= 1024.
+ * oz_trsm_lunit:  B <- L11^-1 B, L11 unit lower jb x jb (solve.py:123-127).
+ * oz_schur_update: A22 -= A21 @ U12 through backend 0 (cuBLAS DGEMM) or 1
+ *                 (Ozaki-INT8 emulated, pair table as oz_gemm_emu), growth
+ *                 folded into growth_bits (solve.py:130-135).
+ * oz_max_abs_bits: max |a| (upper != 0: only c >= r) folded into *bits.
+ */
+int oz_lu_ws_init(void* workspace, size_t workspace_bytes, int64_t ws_n, int64_t ws_nb,
+                  int ws_slices, void* stream);
+int oz_lu_panel(double* a, int64_t lda, int64_t m, int64_t jb, int64_t base, int32_t* ipiv,
+                int32_t* info, unsigned long long* growth_bits, void* workspace,
+                size_t workspace_bytes, int64_t ws_n, int64_t ws_nb, int ws_slices,
+                void* stream);
+int oz_laswp(double* a, int64_t lda, int64_t c0a, int64_t c1a, int64_t c0b, int64_t c1b,
+             int64_t k1, const int32_t* ipiv, int npiv, void* workspace,
+             size_t workspace_bytes, int64_t ws_n, int64_t ws_nb, int ws_slices, void* stream);
+int oz_trsm_lunit(const double* l11, int64_t ldl, int64_t jb, double* b, int64_t ldb,
+                  int64_t ncols, void* stream);
+int oz_schur_update(int backend, int64_t m, int64_t ncols, int64_t jb, const double* a21,
+                    int64_t lda21, const double* u12, int64_t ldu, double* a22, int64_t lda22,
+                    int num_slices, int slice_bits, int npairs, const int32_t* pair_a,
+                    const int32_t* pair_b, const int32_t* pair_shift,
+                    unsigned long long* growth_bits, void* workspace, size_t workspace_bytes,
+                    int64_t ws_n, int64_t ws_nb, void* stream);
+int oz_max_abs_bits(const double* a, int64_t m, int64_t n, int64_t row_stride,
+                    int64_t col_stride, int upper, unsigned long long* bits, void* stream);
+
+/* One diagonal block of lu_solve's triangular solves (solve.py:152-155), in
+ * place on x[0..nb): unit lower (upper = 0) or upper (upper = 1, *flag <- 1
+ * on a zero diagonal).  workspace: oz_lu_solve_workspace_bytes(nb) bytes. */
+int oz_trsv_block(const double* a, int64_t lda, int64_t nb, int upper, double* x,
+                  int32_t* flag, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Partial products over a block of columns (distributed rhs / residual,
+ * harness.py:126, solve.py:195-198): ax[i] = sum_j a_ij x_j (x null -> 1),
+ * asum[i] = sum_j |a_ij| (asum may be null).  Fixed summation order. */
+int oz_gemv_partial(const double* a, int64_t rows, int64_t cols, int64_t row_stride,
+                    int64_t col_stride, const double* x, double* ax, double* asum,
+                    void* stream);
+
+/* The generators' 1 x Q block-cyclic column slab of process column q
+ * (local column lc = global column ((lc/nb)*Q + q)*nb + lc%nb), column-major
+ * with leading dimension ldo; values identical to oz_generate's. */
+int oz_generate_cyclic(int kind, int64_t n, int64_t depth, int64_t block, double alpha,
+                       uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                       int64_t nb, int64_t Q, int64_t q, int64_t ncols, double* out,
+                       int64_t ldo, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

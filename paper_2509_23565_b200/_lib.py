@@ -49,6 +49,20 @@ _SIGNATURES = {
     "oz_max_abs": [_vp, _i64, _i64, _i64, _i64, _vp, _vp],
     "oz_generate": [_int, _i64, _i64, _i64, _dbl, _u64, _u64, _u64, _u64, _vp, _i64, _i64, _vp],
     "oz_copy2d": [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _vp],
+    # step-level LU (distributed driver, hpl.py)
+    "oz_lu_ws_init": [_vp, C.c_size_t, _i64, _i64, _int, _vp],
+    "oz_lu_panel": [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, C.c_size_t, _i64, _i64,
+                    _int, _vp],
+    "oz_laswp": [_vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _int, _vp, C.c_size_t, _i64, _i64,
+                 _int, _vp],
+    "oz_trsm_lunit": [_vp, _i64, _i64, _vp, _i64, _i64, _vp],
+    "oz_schur_update": [_int, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int, _int, _int,
+                        _vp, _vp, _vp, _vp, _vp, C.c_size_t, _i64, _i64, _vp],
+    "oz_max_abs_bits": [_vp, _i64, _i64, _i64, _i64, _int, _vp, _vp],
+    "oz_trsv_block": [_vp, _i64, _i64, _int, _vp, _vp, _vp, C.c_size_t, _vp],
+    "oz_gemv_partial": [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp],
+    "oz_generate_cyclic": [_int, _i64, _i64, _i64, _dbl, _u64, _u64, _u64, _u64, _i64, _i64,
+                           _i64, _i64, _vp, _i64, _vp],
 }
 _RESTYPES = {
     "oz_launch_count": C.c_longlong,

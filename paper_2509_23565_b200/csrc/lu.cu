@@ -89,8 +89,9 @@ __device__ __forceinline__ bool better(double a1, int p1, double a2, int p2) {
 struct PanelArgs {
   double* a;
   int64_t lda;
-  int64_t r0;  // first row (== first column of the window)
-  int64_t m;   // rows r0..r0+m-1
+  int64_t r0;    // first row (== first column of the window), relative to a's panel origin
+  int64_t m;     // rows r0..r0+m-1
+  int64_t base;  // global row index of the panel origin (ipiv values and info are global)
   int w;       // window width (<= PANEL_W)
   int rows_per_cta;
   int32_t* ipiv;
@@ -281,8 +282,9 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
         const int rt = sh.occ[t];  // relative physical row currently at position t
         const double piv = __ldcg(win + 4 + t);
         if (blockIdx.x == 0) {
-          p.ipiv[p.r0 + t] = (int32_t)(p.r0 + ppos);
-          if (piv == 0.0) atomicCAS(reinterpret_cast<int*>(p.info), 0, (int)(p.r0 + t + 1));
+          p.ipiv[p.r0 + t] = (int32_t)(p.base + p.r0 + ppos);
+          if (piv == 0.0)
+            atomicCAS(reinterpret_cast<int*>(p.info), 0, (int)(p.base + p.r0 + t + 1));
           sh.prow[t] = (int)prow;
         }
         // solve.py:80-82: the pivot row is final; the row at position t takes
@@ -383,6 +385,101 @@ __global__ void laswp_gather_kernel(double* __restrict__ a, int64_t lda, const i
   }
 }
 
+// LAPACK-style sequential interchanges -> one gather list.  ipiv[t] (global
+// row, >= k1 + t) is the row swapped with row k1 + t, applied in order
+// t = 0..npiv-1 (solve.py:80-82 / dlaswp).  One CTA: a single thread replays
+// the swaps on an index map (direct array for the npiv diagonal rows, an
+// open-addressing table for the rows below them), then the CTA emits
+// (dst, src) pairs meaning new_row[dst] = old_row[src].
+constexpr int COMPOSE_MAX = 1024;     // max interchanges per list (panel width)
+constexpr int COMPOSE_HASH = 4096;    // table slots for displaced rows (power of two)
+__global__ void __launch_bounds__(256) compose_ipiv_kernel(const int32_t* __restrict__ ipiv,
+                                                            int npiv, int64_t k1, int32_t* dst,
+                                                            int32_t* src, int32_t* cnt) {
+  __shared__ int32_t top[COMPOSE_MAX];
+  __shared__ int32_t hkey[COMPOSE_HASH];
+  __shared__ int32_t hval[COMPOSE_HASH];
+  __shared__ int32_t npos;
+  for (int i = threadIdx.x; i < npiv; i += blockDim.x) top[i] = i;
+  for (int i = threadIdx.x; i < COMPOSE_HASH; i += blockDim.x) hkey[i] = -1;
+  if (threadIdx.x == 0) npos = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int t = 0; t < npiv; ++t) {
+      const int p = (int)(ipiv[t] - k1);  // relative row, >= t
+      if (p == t) continue;
+      if (p < npiv) {
+        const int v = top[t];
+        top[t] = top[p];
+        top[p] = v;
+      } else {
+        unsigned h = ((unsigned)p * 2654435761u) & (COMPOSE_HASH - 1);
+        while (hkey[h] != -1 && hkey[h] != p) h = (h + 1) & (COMPOSE_HASH - 1);
+        if (hkey[h] == -1) {
+          hkey[h] = p;
+          hval[h] = p;
+        }
+        const int v = top[t];
+        top[t] = hval[h];
+        hval[h] = v;
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < npiv; i += blockDim.x) {
+    if (top[i] != i) {
+      const int slot = atomicAdd(&npos, 1);
+      dst[slot] = (int32_t)(k1 + i);
+      src[slot] = (int32_t)(k1 + top[i]);
+    }
+  }
+  for (int i = threadIdx.x; i < COMPOSE_HASH; i += blockDim.x) {
+    if (hkey[i] >= 0 && hval[i] != hkey[i]) {
+      const int slot = atomicAdd(&npos, 1);
+      dst[slot] = (int32_t)(k1 + hkey[i]);
+      src[slot] = (int32_t)(k1 + hval[i]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *cnt = npos;
+}
+
+// Apply a gather list of up to 2*COMPOSE_MAX entries to columns [c0a,c1a) U
+// [c0b,c1b): the list is staged once per CTA in shared memory; each warp owns
+// one column at a time, reads every source row into its shared staging area,
+// then writes every destination row (all reads before any write: cycles safe).
+constexpr int LSWP_WARPS = 4;
+constexpr int LSWP_MAX = 2 * COMPOSE_MAX;
+constexpr size_t LSWP_SMEM = (size_t)LSWP_MAX * 2 * sizeof(int32_t) +
+                             (size_t)LSWP_WARPS * LSWP_MAX * sizeof(double);
+__global__ void __launch_bounds__(LSWP_WARPS * 32) laswp_list_kernel(
+    double* __restrict__ a, int64_t lda, const int32_t* __restrict__ dst,
+    const int32_t* __restrict__ src, const int32_t* __restrict__ count, int64_t c0a, int64_t c1a,
+    int64_t c0b, int64_t c1b) {
+  extern __shared__ uint8_t lsm[];
+  int32_t* sd = reinterpret_cast<int32_t*>(lsm);
+  int32_t* ss = sd + LSWP_MAX;
+  const int cnt = *count;
+  if (cnt == 0) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* stage = reinterpret_cast<double*>(ss + LSWP_MAX) + (size_t)wid * LSWP_MAX;
+  for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+    sd[e] = dst[e];
+    ss[e] = src[e];
+  }
+  __syncthreads();
+  const int64_t na = c1a - c0a, nbb = c1b - c0b;
+  for (int64_t ci = (int64_t)blockIdx.x * LSWP_WARPS + wid; ci < na + nbb;
+       ci += (int64_t)gridDim.x * LSWP_WARPS) {
+    const int64_t col = ci < na ? c0a + ci : c0b + (ci - na);
+    double* colp = a + col * lda;
+    for (int e = lane; e < cnt; e += 32) stage[e] = colp[ss[e]];
+    __syncwarp();
+    for (int e = lane; e < cnt; e += 32) colp[sd[e]] = stage[e];
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------- small trsm
 // B[0:w, c] <- L^{-1} B[0:w, c], L the unit-lower w x w block (w <= TRSM_W).
 // One thread per right-hand-side column, the column held in registers, L in
@@ -448,13 +545,13 @@ __global__ void max_abs_kernel(const double* __restrict__ a, int64_t m, int64_t 
 // Row-chunked GEMV partials: part[chunk][i] = sum_{j in chunk} a_ij * x_j (x=null -> 1),
 // apart[chunk][i] = sum |a_ij|.  Deterministic (fixed order, no atomics).
 constexpr int GEMV_CHUNK = 1024;
-__global__ void gemv_partial_kernel(const double* __restrict__ a, int64_t n, int64_t rs,
-                                    int64_t cs, const double* __restrict__ x,
+__global__ void gemv_partial_kernel(const double* __restrict__ a, int64_t n, int64_t ncols,
+                                    int64_t rs, int64_t cs, const double* __restrict__ x,
                                     double* __restrict__ part, double* __restrict__ apart) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t j0 = (int64_t)blockIdx.y * GEMV_CHUNK;
   if (i >= n) return;
-  const int64_t j1 = min(n, j0 + GEMV_CHUNK);
+  const int64_t j1 = min(ncols, j0 + GEMV_CHUNK);
   double s = 0.0, sa = 0.0;
   const double* row = a + i * rs;
   for (int64_t j = j0; j < j1; ++j) {
@@ -470,7 +567,8 @@ __global__ void gemv_partial_kernel(const double* __restrict__ a, int64_t n, int
 __global__ void gemv_finish_kernel(const double* __restrict__ part,
                                    const double* __restrict__ apart, int nchunks, int64_t n,
                                    const double* __restrict__ b, double* __restrict__ out,
-                                   unsigned long long* rmax, unsigned long long* amax) {
+                                   unsigned long long* rmax, unsigned long long* amax,
+                                   double* __restrict__ abs_out) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double rr = 0.0, aa = 0.0;
   if (i < n) {
@@ -480,6 +578,7 @@ __global__ void gemv_finish_kernel(const double* __restrict__ part,
       if (apart) sa += apart[c * n + i];
     }
     if (out) out[i] = s;
+    if (abs_out) abs_out[i] = sa;
     if (b) rr = fabs(s - b[i]);
     aa = sa;
   }
@@ -613,6 +712,9 @@ struct LuWs {
   int32_t* swap_dst;
   int32_t* swap_src;
   int32_t* swap_cnt;
+  int32_t* cdst;  // composed whole-panel gather list (compose_ipiv_kernel)
+  int32_t* csrc;
+  int32_t* ccnt;
   unsigned long long* bits;  // [0] observed growth, [1] max|A|
   void* split_aux;
   int32_t* expA;
@@ -639,6 +741,9 @@ size_t lu_ws_layout(int64_t n, int64_t nb, int k, uint8_t* base, LuWs* ws) {
   w.swap_dst = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * SWAP_MAX));
   w.swap_src = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * SWAP_MAX));
   w.swap_cnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * 4));
+  w.cdst = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * LSWP_MAX));
+  w.csrc = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * LSWP_MAX));
+  w.ccnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * 4));
   w.bits = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * 4));
   w.split_aux = take(64);
   w.expA = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * n));
@@ -709,8 +814,9 @@ int trsm_blocked(double* a, int64_t lda, int64_t j, int64_t jb, double* b, int64
   return OZ_OK;
 }
 
-int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int32_t* ipiv,
-                 int32_t* info, const LuWs& ws, cudaStream_t st) {
+int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t base,
+                 int32_t* ipiv, int32_t* info, unsigned long long* growth, const LuWs& ws,
+                 cudaStream_t st) {
   static int max_smem = 0;
   if (!max_smem) {
     int dev = 0;
@@ -738,10 +844,11 @@ int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int32_t* 
   pa.lda = lda;
   pa.r0 = r0;
   pa.m = m;
+  pa.base = base;
   pa.w = w;
   pa.rows_per_cta = R;
   pa.ipiv = ipiv;
-  pa.growth = ws.bits;
+  pa.growth = growth;
   pa.info = info;
   pa.bar = ws.bar;
   pa.cand = ws.cand;
@@ -762,6 +869,90 @@ int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int32_t* 
                                             dim3(PANEL_THREADS), args, panel_smem_bytes(w, R),
                                             st));
   prof_stop(tag, st, PROF_PANEL, (double)m * w);
+  return OZ_OK;
+}
+
+// Apply the sequential interchanges ipiv[0..npiv) of rows k1.. (global ipiv
+// values) to columns [c0a,c1a) U [c0b,c1b) of a: compose once, gather once.
+int laswp_ipiv(double* a, int64_t lda, int64_t c0a, int64_t c1a, int64_t c0b, int64_t c1b,
+               int64_t k1, const int32_t* ipiv, int npiv, const LuWs& ws, cudaStream_t st) {
+  OZ_REQUIRE(npiv >= 0 && npiv <= COMPOSE_MAX, OZ_UNSUPPORTED, "at most %d interchanges per call",
+             COMPOSE_MAX);
+  const int64_t ncols = (c1a - c0a) + (c1b - c0b);
+  if (npiv == 0 || ncols <= 0) return OZ_OK;
+  static bool attr = false;
+  if (!attr) {
+    OZ_CHECK_CUDA(cudaFuncSetAttribute(laswp_list_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)LSWP_SMEM));
+    attr = true;
+  }
+  struct Stop {
+    int tag;
+    cudaStream_t st;
+    ~Stop() { prof_stop(tag, st, PROF_LASWP, 0.0); }
+  } stop{prof_start(st), st};
+  compose_ipiv_kernel<<<1, 256, 0, st>>>(ipiv, npiv, k1, ws.cdst, ws.csrc, ws.ccnt);
+  OZ_CHECK_LAUNCH();
+  int64_t blocks = ceil_div(ncols, LSWP_WARPS);
+  if (blocks > sm_count() * 2) blocks = sm_count() * 2;
+  laswp_list_kernel<<<(unsigned)blocks, LSWP_WARPS * 32, LSWP_SMEM, st>>>(
+      a, lda, ws.cdst, ws.csrc, ws.ccnt, c0a, c1a, c0b, c1b);
+  OZ_CHECK_LAUNCH();
+  return OZ_OK;
+}
+
+// Factor one m x jb column panel in place (solve.py:66-91 for columns
+// j..j+jb of the global matrix): `a` points at the panel's diagonal corner,
+// rows keep the global numbering through `base` (= j).  Interchanges are
+// applied to the panel's own columns only; ipiv[0..jb) receives the global
+// pivot rows, info the first zero pivot (global column + 1), growth the max
+// |entry| seen.  The caller applies ipiv to the other columns (laswp_ipiv).
+int panel_factor(double* a, int64_t lda, int64_t m, int64_t jb, int64_t base, int32_t* ipiv,
+                 int32_t* info, unsigned long long* growth, const LuWs& ws, cudaStream_t st) {
+  for (int64_t jj = 0; jj < jb; jj += PANEL_W) {
+    const int w = (int)((jb - jj) < PANEL_W ? (jb - jj) : PANEL_W);
+    OZ_TRY(panel_window(a, lda, jj, m - jj, w, base, ipiv, info, growth, ws, st));
+    OZ_TRY(apply_list(a, lda, ws, 0, jj, jj + w, jb, st));
+    const int64_t rest = jb - (jj + w);
+    if (rest > 0) {
+      OZ_TRY(trsm_blocked(a, lda, jj, w, a + (jj + w) * lda + jj, lda, rest, st));
+      const int64_t below = m - jj - w;
+      if (below > 0) {
+        const int tag = prof_start(st);
+        OZ_TRY(dgemm(0, 0, below, rest, w, -1.0, a + jj * lda + jj + w, lda,
+                     a + (jj + w) * lda + jj, lda, 1.0, a + (jj + w) * lda + jj + w, lda, st));
+        prof_stop(tag, st, PROF_DGEMM_PANEL, 2.0 * below * rest * w);
+      }
+    }
+  }
+  return OZ_OK;
+}
+
+// A22 (m x ncols) -= A21 (m x jb) @ U12 (jb x ncols) through the selected
+// backend (solve.py:130-134), growth = max |A22| after the update (:135).
+int schur_update(int backend, int64_t m, int64_t ncols, int64_t jb, const double* a21,
+                 int64_t lda21, const double* u12, int64_t ldu, double* a22, int64_t lda22, int k,
+                 int q, int npairs, const int32_t* pa, const int32_t* pb, const int32_t* ps,
+                 unsigned long long* growth, const LuWs& ws, cudaStream_t st) {
+  if (m <= 0 || ncols <= 0) return OZ_OK;
+  if (backend == 0) {
+    const int tag = prof_start(st);
+    OZ_TRY(dgemm(0, 0, m, ncols, jb, -1.0, a21, lda21, u12, ldu, 1.0, a22, lda22, st));
+    prof_stop(tag, st, PROF_DGEMM, 2.0 * m * ncols * jb);
+    return max_abs(a22, m, ncols, 1, lda22, 0, 0, growth, st);
+  }
+  const int64_t ssa = m * ws.ldK, ssb = ncols * ws.ldK;
+  int tag = prof_start(st);
+  OZ_TRY(split_launch(a21, m, jb, 1, lda21, OZ_ROW_SCALED, OZ_PER_VECTOR, k, q, ws.slA, ws.ldK,
+                      ssa, ws.expA, ws.split_aux, st));
+  OZ_TRY(split_launch(u12, jb, ncols, 1, ldu, OZ_COL_SCALED, OZ_PER_VECTOR, k, q, ws.slB, ws.ldK,
+                      ssb, ws.expB, ws.split_aux, st));
+  prof_stop(tag, st, PROF_SPLIT, (double)(m + ncols) * jb * (8.0 + k));
+  tag = prof_start(st);
+  OZ_TRY(gemm_emu_launch(m, ncols, jb, ws.slA, ws.ldK, ssa, k, ws.expA, ws.slB, ws.ldK, ssb, k,
+                         ws.expB, npairs, pa, pb, ps, -1.0, 1.0, a22, lda22, 1, growth, st));
+  prof_stop(tag, st, PROF_EMU_GEMM, 2.0 * npairs * m * ncols * jb);
   return OZ_OK;
 }
 
@@ -790,50 +981,19 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
 
   for (int64_t j = 0; j < n; j += nb) {
     const int64_t jb = nb < n - j ? nb : n - j;
-    // ---- panel (columns j..j+jb) in windows of <= PANEL_W columns
-    for (int64_t jj = j; jj < j + jb; jj += PANEL_W) {
-      const int w = (int)((j + jb - jj) < PANEL_W ? (j + jb - jj) : PANEL_W);
-      OZ_TRY(panel_window(a, lda, jj, n - jj, w, ipiv, info, ws, st));
-      // the window's interchanges on every other column: whole-row swaps
-      // (solve.py:80-82); the window kernel already placed its own columns
-      OZ_TRY(apply_list(a, lda, ws, 0, jj, jj + w, n, st));
-      const int64_t rest = j + jb - (jj + w);
-      if (rest > 0) {
-        OZ_TRY(trsm_blocked(a, lda, jj, w, a + (jj + w) * lda + jj, lda, rest, st));
-        const int64_t below = n - jj - w;
-        if (below > 0) {
-          const int tag = prof_start(st);
-          OZ_TRY(dgemm(0, 0, below, rest, w, -1.0, a + jj * lda + jj + w, lda,
-                       a + (jj + w) * lda + jj, lda, 1.0, a + (jj + w) * lda + jj + w, lda, st));
-          prof_stop(tag, st, PROF_DGEMM_PANEL, 2.0 * below * rest * w);
-        }
-      }
-    }
+    // ---- panel (columns j..j+jb), then its interchanges on every other
+    //      column: whole-row swaps (solve.py:80-82)
+    double* ajj = a + j * lda + j;
+    OZ_TRY(panel_factor(ajj, lda, n - j, jb, j, ipiv + j, info, ws.bits, ws, st));
+    OZ_TRY(laswp_ipiv(a, lda, 0, j, j + jb, n, j, ipiv + j, (int)jb, ws, st));
     const int64_t rest = n - j - jb;
     if (rest > 0) {
       double* a12 = a + (j + jb) * lda + j;
       double* a21 = a + j * lda + (j + jb);
       double* a22 = a + (j + jb) * lda + (j + jb);
       OZ_TRY(trsm_blocked(a, lda, j, jb, a12, lda, rest, st));  // solve.py:123-127
-      if (backend == 0) {                                         // solve.py:130-134 native
-        const int tag = prof_start(st);
-        OZ_TRY(dgemm(0, 0, rest, rest, jb, -1.0, a21, lda, a12, lda, 1.0, a22, lda, st));
-        prof_stop(tag, st, PROF_DGEMM, 2.0 * rest * rest * jb);
-        OZ_TRY(max_abs(a22, rest, rest, 1, lda, 0, 0, ws.bits, st));
-      } else {                                                    // emulated Schur update
-        const int64_t sst = rest * ws.ldK;
-        int tag = prof_start(st);
-        OZ_TRY(split_launch(a21, rest, jb, 1, lda, OZ_ROW_SCALED, OZ_PER_VECTOR, k, q, ws.slA,
-                            ws.ldK, sst, ws.expA, ws.split_aux, st));
-        OZ_TRY(split_launch(a12, jb, rest, 1, lda, OZ_COL_SCALED, OZ_PER_VECTOR, k, q, ws.slB,
-                            ws.ldK, sst, ws.expB, ws.split_aux, st));
-        prof_stop(tag, st, PROF_SPLIT, 2.0 * rest * jb * (8.0 + k));
-        tag = prof_start(st);
-        OZ_TRY(gemm_emu_launch(rest, rest, jb, ws.slA, ws.ldK, sst, k, ws.expA, ws.slB, ws.ldK,
-                               sst, k, ws.expB, npairs, pa, pb, ps, -1.0, 1.0, a22, lda, 1,
-                               ws.bits, st));
-        prof_stop(tag, st, PROF_EMU_GEMM, 2.0 * npairs * rest * rest * jb);
-      }
+      OZ_TRY(schur_update(backend, rest, rest, jb, a21, lda, a12, lda, a22, lda, k, q, npairs,
+                          pa, pb, ps, ws.bits, ws, st));     // solve.py:130-134
     }
     // finalized U rows of this panel: triu(lu[j:j+jb, j:]) (solve.py:135-137)
     OZ_TRY(max_abs(a + j * lda + j, jb, n - j, 1, lda, 1, 0, ws.bits, st));
@@ -874,14 +1034,15 @@ int lu_solve(const double* lu, int64_t n, int64_t lda, const int64_t* perm, cons
 
 int gemv_rows(const double* a, int64_t n, int64_t rs, int64_t cs, const double* x,
               const double* b, double* out, unsigned long long* rmax, unsigned long long* amax,
-              double* part, cudaStream_t st) {
-  const int nchunks = (int)ceil_div(n, GEMV_CHUNK);
-  double* apart = amax ? part + (size_t)nchunks * n : nullptr;
+              double* part, cudaStream_t st, int64_t ncols = -1, double* abs_out = nullptr) {
+  if (ncols < 0) ncols = n;
+  const int nchunks = (int)ceil_div(ncols, GEMV_CHUNK);
+  double* apart = (amax || abs_out) ? part + (size_t)nchunks * n : nullptr;
   dim3 grid((unsigned)ceil_div(n, 128), (unsigned)nchunks);
-  gemv_partial_kernel<<<grid, 128, 0, st>>>(a, n, rs, cs, x, part, apart);
+  gemv_partial_kernel<<<grid, 128, 0, st>>>(a, n, ncols, rs, cs, x, part, apart);
   OZ_CHECK_LAUNCH();
   gemv_finish_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(part, apart, nchunks, n, b, out,
-                                                                 rmax, amax);
+                                                                 rmax, amax, abs_out);
   OZ_CHECK_LAUNCH();
   return OZ_OK;
 }
@@ -971,4 +1132,125 @@ extern "C" int oz_copy2d(const double* src, int64_t rows, int64_t cols, int64_t 
                                                             dst_rs, dst_cs);
   OZ_CHECK_LAUNCH();
   return OZ_OK;
+}
+
+// ============================================================ step-level C ABI
+// The blocked LU as separate steps, for drivers that own the loop (the
+// distributed 1 x Q block-cyclic HPL in hpl.py).  Every call takes the LU
+// workspace plus the (n, nb, num_slices) it was sized with.
+namespace {
+int ws_view(void* ws, size_t ws_bytes, int64_t n, int64_t nb, int k, oz::LuWs* out) {
+  const size_t need = oz::lu_ws_layout(n, nb, k, (uint8_t*)ws, out);
+  OZ_REQUIRE(ws != nullptr && ws_bytes >= need, OZ_INVALID_PARAMS,
+             "workspace too small (%zu < %zu)", ws_bytes, need);
+  return OZ_OK;
+}
+}  // namespace
+
+extern "C" int oz_lu_ws_init(void* ws, size_t ws_bytes, int64_t n, int64_t nb, int num_slices,
+                             void* stream) {
+  using namespace oz;
+  LuWs w;
+  OZ_TRY(ws_view(ws, ws_bytes, n, nb, num_slices, &w));
+  cudaStream_t st = as_stream(stream);
+  OZ_CHECK_CUDA(cudaMemsetAsync(w.bar, 0, sizeof(GridBar), st));
+  OZ_CHECK_CUDA(cudaMemsetAsync(w.cand, 0, sizeof(double) * 2 * 1024 * CAND_STRIDE, st));
+  OZ_CHECK_CUDA(cudaMemsetAsync(w.bits, 0, 4 * sizeof(unsigned long long), st));
+  return OZ_OK;
+}
+
+extern "C" int oz_lu_panel(double* a, int64_t lda, int64_t m, int64_t jb, int64_t base,
+                           int32_t* ipiv, int32_t* info, unsigned long long* growth_bits,
+                           void* ws, size_t ws_bytes, int64_t ws_n, int64_t ws_nb,
+                           int ws_slices, void* stream) {
+  using namespace oz;
+  OZ_REQUIRE(m >= jb && jb >= 1 && jb <= COMPOSE_MAX && lda >= m, OZ_INVALID_PARAMS,
+             "bad panel shape m=%lld jb=%lld lda=%lld", (long long)m, (long long)jb,
+             (long long)lda);
+  LuWs w;
+  OZ_TRY(ws_view(ws, ws_bytes, ws_n, ws_nb, ws_slices, &w));
+  return panel_factor(a, lda, m, jb, base, ipiv, info, growth_bits, w, as_stream(stream));
+}
+
+extern "C" int oz_laswp(double* a, int64_t lda, int64_t c0a, int64_t c1a, int64_t c0b,
+                        int64_t c1b, int64_t k1, const int32_t* ipiv, int npiv, void* ws,
+                        size_t ws_bytes, int64_t ws_n, int64_t ws_nb, int ws_slices,
+                        void* stream) {
+  using namespace oz;
+  OZ_REQUIRE(c0a <= c1a && c0b <= c1b, OZ_INVALID_PARAMS, "bad column ranges");
+  LuWs w;
+  OZ_TRY(ws_view(ws, ws_bytes, ws_n, ws_nb, ws_slices, &w));
+  return laswp_ipiv(a, lda, c0a, c1a, c0b, c1b, k1, ipiv, npiv, w, as_stream(stream));
+}
+
+extern "C" int oz_trsm_lunit(const double* l11, int64_t ldl, int64_t jb, double* b, int64_t ldb,
+                             int64_t ncols, void* stream) {
+  using namespace oz;
+  OZ_REQUIRE(jb >= 1 && ldl >= jb && ldb >= jb, OZ_INVALID_PARAMS, "bad trsm shape");
+  return trsm_blocked(const_cast<double*>(l11), ldl, 0, jb, b, ldb, ncols, as_stream(stream));
+}
+
+extern "C" int oz_schur_update(int backend, int64_t m, int64_t ncols, int64_t jb,
+                               const double* a21, int64_t lda21, const double* u12, int64_t ldu,
+                               double* a22, int64_t lda22, int num_slices, int slice_bits,
+                               int npairs, const int32_t* pair_a, const int32_t* pair_b,
+                               const int32_t* pair_shift, unsigned long long* growth_bits,
+                               void* ws, size_t ws_bytes, int64_t ws_n, int64_t ws_nb,
+                               void* stream) {
+  using namespace oz;
+  OZ_REQUIRE(backend == 0 || backend == 1, OZ_INVALID_PARAMS, "bad backend");
+  OZ_REQUIRE(backend == 0 || (m <= ws_n && ncols <= ws_n && jb <= ws_nb), OZ_INVALID_PARAMS,
+             "schur update larger than the workspace");
+  LuWs w;
+  OZ_TRY(ws_view(ws, ws_bytes, ws_n, ws_nb, backend == 1 ? num_slices : 0, &w));
+  return schur_update(backend, m, ncols, jb, a21, lda21, u12, ldu, a22, lda22, num_slices,
+                      slice_bits, npairs, pair_a, pair_b, pair_shift, growth_bits, w,
+                      as_stream(stream));
+}
+
+// max |a| (optionally only the upper trapezoid c >= r) folded into *bits
+extern "C" int oz_max_abs_bits(const double* a, int64_t m, int64_t n, int64_t row_stride,
+                               int64_t col_stride, int upper, unsigned long long* bits,
+                               void* stream) {
+  return oz::max_abs(a, m, n, row_stride, col_stride, upper, 0, bits, oz::as_stream(stream));
+}
+
+// One diagonal block of a triangular solve, in place on x[0..nb):
+// unit-lower (upper=0) or upper with division (upper=1); flag <- 1 on a zero
+// diagonal.  workspace: oz_lu_solve_workspace_bytes(nb) bytes.
+extern "C" int oz_trsv_block(const double* a, int64_t lda, int64_t nb, int upper, double* x,
+                             int32_t* flag, void* workspace, size_t ws_bytes, void* stream) {
+  using namespace oz;
+  OZ_REQUIRE(ws_bytes >= oz_lu_solve_workspace_bytes(nb), OZ_INVALID_PARAMS,
+             "workspace too small");
+  cudaStream_t st = as_stream(stream);
+  int* sync = reinterpret_cast<int*>(workspace);
+  const int nblk = (int)ceil_div(nb, TRSV_B);
+  OZ_CHECK_CUDA(cudaMemsetAsync(sync, 0, sizeof(int) * (nblk + 1), st));
+  trsv_syncfree_kernel<<<nblk, TRSV_B * TRSV_G, 0, st>>>(a, lda, nb, upper, x, sync + 1, sync,
+                                                         flag);
+  OZ_CHECK_LAUNCH();
+  return OZ_OK;
+}
+
+// Partial row sums over a block of columns: ax[i] = sum_j a_ij x_j (x = null:
+// x_j = 1), asum[i] = sum_j |a_ij| (null: skipped).  Fixed summation order.
+extern "C" int oz_gemv_partial(const double* a, int64_t rows, int64_t cols, int64_t row_stride,
+                               int64_t col_stride, const double* x, double* ax, double* asum,
+                               void* stream) {
+  using namespace oz;
+  if (rows <= 0) return OZ_OK;
+  cudaStream_t st = as_stream(stream);
+  if (cols <= 0) {
+    OZ_CHECK_CUDA(cudaMemsetAsync(ax, 0, sizeof(double) * rows, st));
+    if (asum) OZ_CHECK_CUDA(cudaMemsetAsync(asum, 0, sizeof(double) * rows, st));
+    return OZ_OK;
+  }
+  const int nchunks = (int)ceil_div(cols, GEMV_CHUNK);
+  double* part = nullptr;
+  OZ_CHECK_CUDA(cudaMallocAsync(&part, sizeof(double) * 2 * nchunks * rows, st));
+  int s = gemv_rows(a, rows, row_stride, col_stride, x, nullptr, ax, nullptr, nullptr, part, st,
+                    cols, asum);
+  cudaFreeAsync(part, st);
+  return s;
 }

@@ -1,0 +1,410 @@
+"""Distributed HPL: the blocked LU of solve.py:94-140 and the solve of
+solve.py:143-156 over a 1 x Q block-cyclic process grid, one process per GPU.
+
+Layout: column blocks of width nb are dealt round-robin to the
+Q ranks (global block b lives on rank b % Q as local block b // Q); every
+rank holds all n rows of its columns, column-major, leading dimension n.
+With one process row every pivot search is local to the panel owner, so the
+only data-path collectives are
+
+* the panel broadcast: the owner factors columns j..j+jb (oz_lu_panel:
+  partial pivoting, division, outer-product update — solve.py:66-91) and
+  broadcasts the factored panel rows j..n plus its jb pivot rows;
+* the triangular-solve broadcasts of the updated right-hand side.
+
+Every rank then applies the panel's interchanges to its own columns
+(oz_laswp, whole-row swaps as solve.py:80-82), solves its U12 block
+(oz_trsm_lunit, solve.py:123-127) and updates its trailing columns through
+the configured backend (oz_schur_update: cuBLAS DGEMM or the Ozaki-INT8
+tcgen05 GEMM, solve.py:130-134).  The emulated Schur update is per-element
+identical to the single-GPU one (row exponents come from the whole L21,
+column exponents from each U12 column), so the distributed factors match the
+single-process factors.
+
+The driver only sequences calls: local block operations go through an
+``ops`` object (``DeviceOps`` = the C ABI on the local GPU) and collectives
+through a ``Comm`` (torch.distributed: NCCL on B200s; gloo stages CUDA
+tensors through host memory, which the CPU/1-GPU tests use).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _dev, _lib
+from .errors import InvalidParamsError, SingularPivotError
+from .gemm import BackendKind, GemmBackend, pair_table
+
+__all__ = ["Comm", "DeviceOps", "HplReport", "local_cols_before", "local_ncols",
+           "global_cols", "factor_block_cyclic", "solve_block_cyclic", "hpl_run"]
+
+
+# ------------------------------------------------------------ index maps
+def local_cols_before(g: int, nb: int, Q: int, q: int) -> int:
+    """Number of rank q's columns whose global index is < g (1 x Q grid)."""
+    b, off = divmod(g, nb)
+    cnt = ((b - q + Q - 1) // Q) * nb if b > q else 0
+    if b % Q == q:
+        cnt += off
+    return cnt
+
+
+def local_ncols(n: int, nb: int, Q: int, q: int) -> int:
+    return local_cols_before(n, nb, Q, q)
+
+
+def global_cols(n: int, nb: int, Q: int, q: int) -> np.ndarray:
+    """Global indices of rank q's local columns, in local order."""
+    lc = np.arange(local_ncols(n, nb, Q, q), dtype=np.int64)
+    return ((lc // nb) * Q + q) * nb + lc % nb
+
+
+# ------------------------------------------------------------ collectives
+class Comm:
+    """torch.distributed over a group.  Under gloo, CUDA tensors are staged
+    through host memory (gloo moves host buffers); NCCL moves them in place
+    over NVLink."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        if dist.is_available() and dist.is_initialized():
+            self.rank = dist.get_rank(group)
+            self.size = dist.get_world_size(group)
+            self.stage = dist.get_backend(group) == "gloo"
+        else:
+            self.rank, self.size, self.stage = 0, 1, False
+
+    def _grank(self, r):
+        if self.group is None:
+            return r
+        return self.dist.get_global_rank(self.group, r)
+
+    def bcast(self, t, src: int) -> None:
+        if self.size == 1 or t.numel() == 0:
+            return
+        if self.stage and t.is_cuda:
+            h = t.cpu()
+            self.dist.broadcast(h, self._grank(src), group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.broadcast(t, self._grank(src), group=self.group)
+
+    def allreduce(self, t, op: str) -> None:
+        if self.size == 1:
+            return
+        rop = {"sum": self.dist.ReduceOp.SUM, "max": self.dist.ReduceOp.MAX}[op]
+        if self.stage and t.is_cuda:
+            h = t.cpu()
+            self.dist.all_reduce(h, rop, group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.all_reduce(t, rop, group=self.group)
+
+    def allreduce_values(self, vals, op: str) -> list:
+        """All-reduce a few host scalars (NCCL needs them on the device)."""
+        import torch
+        dev = "cpu" if (self.stage or self.size == 1) else "cuda"
+        t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=dev)
+        self.allreduce(t, op)
+        return [float(v) for v in t.cpu().tolist()]
+
+    def barrier(self) -> None:
+        if self.size > 1:
+            self.dist.barrier(group=self.group)
+
+
+# ------------------------------------------------------------ device ops
+class DeviceOps:
+    """Rank-local block operations on the GPU, all through the C ABI
+    (include/ozb200.h step-level entries).  Owns the local slab (n x ncl,
+    column-major), the broadcast buffers and the LU workspace."""
+
+    def __init__(self, n: int, nb: int, Q: int, q: int, backend: GemmBackend):
+        t = _lib.require_cuda()
+        self.t = t
+        self.n, self.nb, self.Q, self.q = n, nb, Q, q
+        self.ncl = local_ncols(n, nb, Q, q)
+        self.backend = backend
+        self.emulated = backend.kind is BackendKind.EMULATED_INT8
+        if self.emulated:
+            if backend.slice_bits > 7:
+                from .errors import DeviceError
+                raise DeviceError("slice_bits > 7 (int16 slices) is not supported on the GPU path")
+            self.k, self.qbits = backend.splits, backend.slice_bits
+            self.pa, self.pb, self.ps = pair_table(backend)
+        else:
+            self.k, self.qbits = 0, 7
+            self.pa = self.pb = self.ps = np.zeros(1, dtype=np.int32)
+        dev = "cuda"
+        # local slab: torch (ncl, n) row-major == column-major n x ncl, ld = n
+        self.slab = t.empty((max(self.ncl, 1), n), dtype=t.float64, device=dev)
+        self.pbuf = t.empty((n * nb,), dtype=t.float64, device=dev)
+        self.ipiv_buf = t.empty((nb,), dtype=t.int32, device=dev)
+        self.ipiv = t.empty((n,), dtype=t.int32, device=dev)
+        self.info = t.zeros((1,), dtype=t.int32, device=dev)
+        self.bits = t.zeros((2,), dtype=t.int64, device=dev)   # [seen, max|A|] as IEEE bits
+        self.wsb = int(_lib.query("oz_lu_workspace_bytes", n, nb, self.k))
+        self.ws = t.empty((self.wsb,), dtype=t.uint8, device=dev)
+        self.tsb = int(_lib.query("oz_lu_solve_workspace_bytes", nb))
+        self.tws = t.zeros((self.tsb // 4 + 1,), dtype=t.int32, device=dev)
+        self.flag = t.zeros((1,), dtype=t.int32, device=dev)
+
+    # -- addressing
+    def _a(self, lc: int, row: int) -> int:
+        return self.slab.data_ptr() + 8 * (lc * self.n + row)
+
+    def _st(self):
+        return _dev.stream()
+
+    # -- matrix
+    def generate(self, kind: int, seed, depth=1, block=1, alpha=1.0) -> None:
+        from .matgen import pcg64_state
+        state, inc = pcg64_state(seed) if seed is not None else (0, 0)
+        m64 = (1 << 64) - 1
+        _lib.call("oz_generate_cyclic", kind, self.n, depth, block, float(alpha), state >> 64,
+                  state & m64, inc >> 64, inc & m64, self.nb, self.Q, self.q, self.ncl,
+                  self.slab.data_ptr(), self.n, self._st())
+
+    def row_partials(self, x_local=None):
+        """(A_local @ x_local, sum |A_local| per row) over this rank's columns."""
+        t = self.t
+        ax = t.empty((self.n,), dtype=t.float64, device="cuda")
+        asum = t.empty((self.n,), dtype=t.float64, device="cuda")
+        _lib.call("oz_gemv_partial", self.slab.data_ptr(), self.n, self.ncl, 1, self.n,
+                  None if x_local is None else x_local.data_ptr(), ax.data_ptr(),
+                  asum.data_ptr(), self._st())
+        return ax, asum
+
+    def local_view(self):
+        """The local slab as an (n, ncl) column-major tensor view."""
+        return self.slab[:self.ncl].t()
+
+    # -- factorization steps
+    def begin(self) -> None:
+        _lib.call("oz_lu_ws_init", self.ws.data_ptr(), self.wsb, self.n, self.nb, self.k,
+                  self._st())
+        self.info.zero_()
+        self.bits.zero_()
+        if self.ncl:
+            _lib.call("oz_max_abs_bits", self.slab.data_ptr(), self.n, self.ncl, 1, self.n, 0,
+                      self.bits.data_ptr() + 8, self._st())
+
+    def panel(self, lc: int, j: int, jb: int) -> None:
+        _lib.call("oz_lu_panel", self._a(lc, j), self.n, self.n - j, jb, j,
+                  self.ipiv_buf.data_ptr(), self.info.data_ptr(), self.bits.data_ptr(),
+                  self.ws.data_ptr(), self.wsb, self.n, self.nb, self.k, self._st())
+        # triu of the panel's diagonal block: finalized U rows (solve.py:135-137)
+        _lib.call("oz_max_abs_bits", self._a(lc, j), jb, jb, 1, self.n, 1,
+                  self.bits.data_ptr(), self._st())
+        m = self.n - j
+        _lib.call("oz_copy2d", self._a(lc, j), m, jb, 1, self.n, self.pbuf.data_ptr(), 1, m,
+                  self._st())
+
+    def panel_buffers(self, j: int, jb: int):
+        m = self.n - j
+        return self.pbuf[:m * jb], self.ipiv_buf[:jb]
+
+    def record_pivots(self, j: int, jb: int) -> None:
+        self.ipiv[j:j + jb].copy_(self.ipiv_buf[:jb])
+
+    def laswp(self, ranges, j: int, jb: int) -> None:
+        (c0a, c1a), (c0b, c1b) = ranges
+        _lib.call("oz_laswp", self.slab.data_ptr(), self.n, c0a, c1a, c0b, c1b, j,
+                  self.ipiv_buf.data_ptr(), jb, self.ws.data_ptr(), self.wsb, self.n, self.nb,
+                  self.k, self._st())
+
+    def update(self, j: int, jb: int, lstart: int, nt: int) -> None:
+        """U12 <- L11^-1 A12, A22 <- A22 - L21 U12 on local columns lstart.."""
+        m = self.n - j
+        u12 = self._a(lstart, j)
+        _lib.call("oz_trsm_lunit", self.pbuf.data_ptr(), m, jb, u12, self.n, nt, self._st())
+        _lib.call("oz_max_abs_bits", u12, jb, nt, 1, self.n, 0, self.bits.data_ptr(),
+                  self._st())
+        if m - jb > 0:
+            _lib.call("oz_schur_update", 1 if self.emulated else 0, m - jb, nt, jb,
+                      self.pbuf.data_ptr() + 8 * jb, m, u12, self.n, self._a(lstart, j + jb),
+                      self.n, self.k, self.qbits, len(self.pa), self.pa.ctypes.data,
+                      self.pb.ctypes.data, self.ps.ctypes.data, self.bits.data_ptr(),
+                      self.ws.data_ptr(), self.wsb, self.n, self.nb, self._st())
+
+    def finish(self):
+        """-> (ipiv host int32[n], info, seen, max|A|) of this rank."""
+        b = self.bits.cpu().numpy().view(np.float64)
+        return self.ipiv.cpu().numpy(), int(self.info.item()), float(b[0]), float(b[1])
+
+    # -- triangular solves
+    def solve_vector(self, vec_host: np.ndarray):
+        return self.t.from_numpy(np.ascontiguousarray(vec_host, dtype=np.float64)).to("cuda")
+
+    def trsv(self, lc: int, j: int, jb: int, upper: bool, x) -> None:
+        _lib.call("oz_trsv_block", self._a(lc, j), self.n, jb, 1 if upper else 0,
+                  x.data_ptr() + 8 * j, self.flag.data_ptr(), self.tws.data_ptr(), self.tsb,
+                  self._st())
+
+    def gemv_update(self, lc: int, r0: int, r1: int, j: int, jb: int, x) -> None:
+        """x[r0:r1] -= A[r0:r1, local cols lc..lc+jb] @ x[j:j+jb]."""
+        if r1 <= r0:
+            return
+        _lib.call("oz_dgemm", 0, 0, r1 - r0, 1, jb, -1.0, self._a(lc, r0), self.n,
+                  x.data_ptr() + 8 * j, jb, 1.0, x.data_ptr() + 8 * r0, r1 - r0, self._st())
+
+    def zero_diag(self) -> int:
+        return int(self.flag.item())
+
+
+# ------------------------------------------------------------ the driver
+def factor_block_cyclic(ops, comm, n: int, nb: int):
+    """Blocked right-looking LU (solve.py:94-140) of the distributed matrix in
+    ops' local slabs.  Returns (ipiv int32[n] global LAPACK-style, growth)."""
+    Q, q = comm.size, comm.rank
+    ncl = local_ncols(n, nb, Q, q)
+    ops.begin()
+    for jblk in range(-(-n // nb)):
+        j = jblk * nb
+        jb = min(nb, n - j)
+        owner = jblk % Q
+        lc = (jblk // Q) * nb                       # the panel's local column on its owner
+        if q == owner:
+            ops.panel(lc, j, jb)
+        pbuf, ipiv = ops.panel_buffers(j, jb)
+        comm.bcast(pbuf, owner)                     # L11/L21 of the factored panel
+        comm.bcast(ipiv, owner)                     # its jb pivot rows
+        ops.record_pivots(j, jb)
+        if q == owner:
+            ranges = ((0, lc), (lc + jb, ncl))
+        else:
+            ranges = ((0, ncl), (ncl, ncl))
+        ops.laswp(ranges, j, jb)
+        lstart = local_cols_before(j + jb, nb, Q, q)
+        nt = ncl - lstart
+        if nt > 0:
+            ops.update(j, jb, lstart, nt)
+    ipiv, info, seen, top = ops.finish()
+    info, seen, top = comm.allreduce_values([info, seen, top], "max")
+    info = int(info)
+    if info:
+        raise SingularPivotError(f"exact zero pivot column at index {info - 1}")
+    return ipiv, (seen / top if top > 0 else 1.0)
+
+
+def solve_block_cyclic(ops, comm, n: int, nb: int, perm: np.ndarray, b_host: np.ndarray):
+    """x = U^-1 L^-1 b[perm] with the factors distributed by column blocks
+    (solve.py:143-156).  Block b's owner solves its diagonal block and
+    updates the remaining right-hand side, then broadcasts it."""
+    Q, q = comm.size, comm.rank
+    x = ops.solve_vector(np.asarray(b_host, dtype=np.float64)[perm])
+    nblk = -(-n // nb)
+    for jblk in range(nblk):                       # unit lower, forward
+        j = jblk * nb
+        jb = min(nb, n - j)
+        owner = jblk % Q
+        if q == owner:
+            lc = (jblk // Q) * nb
+            ops.trsv(lc, j, jb, False, x)
+            ops.gemv_update(lc, j + jb, n, j, jb, x)
+        comm.bcast(x[j:], owner)
+    for jblk in reversed(range(nblk)):             # upper, backward
+        j = jblk * nb
+        jb = min(nb, n - j)
+        owner = jblk % Q
+        if q == owner:
+            lc = (jblk // Q) * nb
+            ops.trsv(lc, j, jb, True, x)
+            ops.gemv_update(lc, 0, j, j, jb, x)
+        comm.bcast(x[:j + jb], owner)
+    if comm.allreduce_values([ops.zero_diag()], "max")[0]:
+        raise SingularPivotError("zero diagonal entry in U")
+    return x
+
+
+@dataclass
+class HplReport:
+    """One distributed HPL run (the reference's SolveReport fields plus timing)."""
+    n: int
+    nb: int
+    grid: str
+    backend: str
+    scaled_residual: float
+    raw_residual_inf: float
+    norm_a_inf: float
+    norm_x_inf: float
+    norm_b_inf: float
+    growth: float
+    seconds_factor: float
+    seconds_solve: float
+    tflops: float
+
+    @property
+    def passed(self) -> bool:
+        from .solve import PASS_THRESHOLD
+        return self.scaled_residual < PASS_THRESHOLD
+
+
+def _replicated_rhs(ops, comm):
+    ax, _ = ops.row_partials(None)                # b = A @ ones (harness.py:126)
+    comm.allreduce(ax, "sum")
+    return ax
+
+
+def _residual(ops, comm, n, nb, x, b):
+    """||Ax-b||_inf / ((||A||_inf ||x||_inf + ||b||_inf) n eps) with A
+    regenerated in the slabs (solve.py:181-214)."""
+    from .solve import _report
+    gcols = global_cols(n, nb, comm.size, comm.rank)
+    xh = x.cpu().numpy()
+    xl = ops.solve_vector(xh[gcols]) if len(gcols) else None
+    ax, asum = ops.row_partials(xl)
+    comm.allreduce(ax, "sum")
+    comm.allreduce(asum, "sum")
+    r = (ax - b).abs().max().item()
+    return _report(float(r), float(asum.max().item()), float(np.abs(xh).max()),
+                   float(b.abs().max().item()), n)
+
+
+def hpl_run(n: int, nb: int, backend: GemmBackend | None = None, *, matrix: str = "uniform",
+            seed: int = 99, depth: int = 4, block: int = 15, alpha: float = 0.5,
+            comm: Comm | None = None, ops: DeviceOps | None = None) -> HplReport:
+    """Generate the matrix distributed (hpl_uniform or randomized ParaWilk,
+    matgen.py:149-171), b = A @ 1, factor, solve and verify.  Times factor and
+    solve with device events, max over ranks."""
+    from .matgen import GEN_PARAWILK_RANDOMIZED, GEN_UNIFORM
+    import torch
+    if backend is None:
+        backend = GemmBackend.native()
+    comm = comm or Comm()
+    if not 1 <= nb <= min(n, 1024):
+        raise InvalidParamsError(f"nb must be in 1..{min(n, 1024)}, got {nb}")
+    if ops is None:
+        ops = DeviceOps(n, nb, comm.size, comm.rank, backend)
+    kind = GEN_UNIFORM if matrix == "uniform" else GEN_PARAWILK_RANDOMIZED
+    ops.generate(kind, seed, depth, block, alpha)
+    b = _replicated_rhs(ops, comm)
+    comm.barrier()
+    torch.cuda.synchronize()
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    e0.record()
+    ipiv, growth = factor_block_cyclic(ops, comm, n, nb)
+    e1.record()
+    from .solve import ipiv_to_perm
+    perm = ipiv_to_perm(ipiv)
+    x = solve_block_cyclic(ops, comm, n, nb, perm, b.cpu().numpy())
+    e2.record()
+    torch.cuda.synchronize()
+    tf, ts = comm.allreduce_values([e0.elapsed_time(e1) / 1e3, e1.elapsed_time(e2) / 1e3],
+                                   "max")
+    ops.generate(kind, seed, depth, block, alpha)          # A again for the residual
+    rep = _residual(ops, comm, n, nb, x, b)
+    return HplReport(n=n, nb=nb, grid=f"1x{comm.size}", backend=backend.describe(),
+                     scaled_residual=rep.scaled_residual, raw_residual_inf=rep.raw_residual_inf,
+                     norm_a_inf=rep.norm_a_inf, norm_x_inf=rep.norm_x_inf,
+                     norm_b_inf=rep.norm_b_inf, growth=growth, seconds_factor=tf,
+                     seconds_solve=ts, tflops=2.0 * n ** 3 / 3.0 / (tf + ts) / 1e12)
+
+
+del math, time
