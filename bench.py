@@ -25,8 +25,14 @@ Workload (BASELINE.json configs[1], largest size that fits one GPU):
   (oracle/ozaki_oracle.py, numpy + OpenBLAS on the host cores) on a bounded
   sample of the same workload (n=1024, same nb, same k).
 
-N > 1: one process per GPU, each solving its own system (replicas, weak
-scaling); there is no data-path collective in this configuration.
+N > 1: one process per GPU solving ONE distributed system (hpl.py): the
+matrix is dealt to the N ranks in 1 x N block-cyclic column blocks, the panel
+owner factors and NCCL-broadcasts each panel and its pivots, every rank
+applies the interchanges and updates its own trailing columns.  Weak scaling
+in memory: n = 32768 * sqrt(N) (rounded to nb) keeps the per-GPU slab fixed;
+value = (2/3) n^3 / max-over-ranks step time for the whole job.
+(BENCH_DIST_BACKEND=gloo runs the same path with several ranks on one GPU,
+for testing only.)
 """
 
 from __future__ import annotations
@@ -52,7 +58,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--n", type=int, default=32768)
-    p.add_argument("--nb", type=int, default=512)
+    p.add_argument("--nb", type=int, default=1024)
     p.add_argument("--k", type=int, default=7)
     p.add_argument("--cpu-n", type=int, default=1024)
     p.add_argument("--e2e-steps", type=int, default=2)
@@ -61,6 +67,8 @@ def parse():
                    help="splits for the GEMM (D3) and LU k-sweeps; empty string skips them")
     p.add_argument("--gemm-n", type=int, default=16384, help="D3 standalone DGEMM size")
     p.add_argument("--sweep-lu-n", type=int, default=16384, help="LU k-sweep size")
+    p.add_argument("--dist-n", type=int, default=0,
+                   help="N>1: global order (default n*sqrt(N) rounded to nb: fixed HBM per GPU)")
     return p.parse_args()
 
 
@@ -279,6 +287,124 @@ def lu_sweep(n, nb, ks):
             "runs": rows}
 
 
+# ---------------------------------------------------------------- N > 1
+def run_distributed(args, rank, world):
+    """configs[3]/[4] shape on N GPUs: distributed HPL LU + solve, 1 x N
+    block-cyclic columns (hpl.py), NCCL panel/pivot broadcasts.  Weak scaling
+    in memory: n = n1 * sqrt(N) keeps the per-GPU slab at n1^2 * 8 bytes."""
+    import math
+
+    import numpy as np
+    import torch
+
+    import paper_2509_23565_b200 as oz
+    from paper_2509_23565_b200 import _lib, hpl
+
+    nb, k = args.nb, args.k
+    n = args.dist_n or int(round(args.n * math.sqrt(world) / nb)) * nb
+    dev = torch.cuda.current_device()
+    comm = hpl.Comm()
+    prob = hpl.HplProblem(n, nb, oz.GemmBackend.int8(k), comm=comm)
+    for _ in range(args.warmup):
+        prob.step()
+    torch.cuda.synchronize()
+    launches0 = _lib.load().oz_launch_count()
+    _lib.call("oz_prof_enable", 1)
+    with ClockSampler(dev) as clk:
+        comm.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = _events()
+        e0.record()
+        for _ in range(args.steps):
+            x = prob.step()
+        e1.record()
+        torch.cuda.synchronize()
+        comm.barrier()
+    launches = _lib.load().oz_launch_count() - launches0
+    prof = np.zeros(36)
+    _lib.call("oz_prof_summary", prof.ctypes.data)
+    _lib.call("oz_prof_enable", 0)
+    ms = comm.allreduce_values([e0.elapsed_time(e1) / args.steps], "max")[0]
+    value = flops(n) / (ms / 1e3) / 1e12
+    rep = prob.verify(x)
+
+    # e2e through the public driver: every rank uploads its column slab from
+    # pinned host memory, factors, solves, and reads x back, inside the clock
+    host_slab = torch.empty(prob.a0.shape, dtype=torch.float64, pin_memory=True)
+    host_slab.copy_(prob.a0)
+    torch.cuda.synchronize()
+    e2e = None
+    if args.e2e_steps > 0:
+        comm.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            prob.ops.slab.copy_(host_slab, non_blocking=True)
+            xh = prob.factor_solve().cpu()
+        torch.cuda.synchronize()
+        te = comm.allreduce_values([(time.perf_counter() - t0) / args.e2e_steps], "max")[0]
+        e2e = {"value": flops(n) / te / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": int(host_slab.numel() * 8) * world,
+               "d2h_bytes_per_step": int(xh.numel() * 8) * world, "ms_per_step": te * 1e3,
+               "api": "paper_2509_23565_b200.hpl.HplProblem (slab H2D from pinned host, "
+                      "factor_block_cyclic, solve_block_cyclic, x D2H)"}
+    del host_slab
+
+    native = None
+    if not args.skip_native:
+        nprob = hpl.HplProblem(n, nb, oz.GemmBackend.native(), comm=comm)
+        nprob.step()
+        torch.cuda.synchronize()
+        comm.barrier()
+        f0, f1 = _events()
+        f0.record()
+        xn = nprob.step()
+        f1.record()
+        torch.cuda.synchronize()
+        tn = comm.allreduce_values([f0.elapsed_time(f1) / 1e3], "max")[0]
+        native = {"value": flops(n) / tn / 1e12, "ms_per_step": tn * 1e3,
+                  "scaled_residual": nprob.verify(xn).scaled_residual}
+        del nprob
+    if rank != 0:
+        return
+    peaks, peak_kind = load_peaks()
+    peak = 2.0 * float(peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"])
+    gemm_ms, gemm_ops = prof[0], prof[2]
+    achieved = gemm_ops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    kinds = ["emu_gemm", "panel", "schur_dgemm", "split", "laswp", "trsm", "solve", "other",
+             "swap_compose", "panel_dgemm", "trsm_dgemm", "-"]
+    breakdown = {kinds[i]: {"ms_per_step": prof[3 * i] / args.steps,
+                            "launches_per_step": prof[3 * i + 1] / args.steps}
+                 for i in range(12) if prof[3 * i + 1] > 0}
+    cpu_times, cores, cpu_resid = cpu_oracle_lu(args.cpu_n, min(nb, args.cpu_n), k, reps=1)
+    cpu_v = flops(args.cpu_n) / cpu_times[0] / 1e12
+    print(json.dumps({
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": f"f64 emulated via int8 slices (k={k}) -> int32 tensor cores -> f64 recombine",
+        "data": "synthetic (hpl_uniform(n, 99) generated on device per rank, bit-identical "
+                "to numpy)",
+        "config": {"workload": f"configs[3]/[4] shape: distributed HPL LU+solve U(-1/2,1/2) "
+                               f"n={n}, k={k}, 1x{world} block-cyclic, NCCL panel broadcast",
+                   "n": n, "nb": nb, "k": k, "grid": f"1x{world}",
+                   "parallelism": f"block-cyclic 1x{world}",
+                   "l2": "inputs >> 126 MB L2; no flush needed",
+                   "flop_convention": "2/3 n^3 (harness.py:383)",
+                   "weak_scaling": "n = n1*sqrt(N): per-GPU slab fixed"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": None,
+                     "kernel": "oz::emu::emu_gemm_pair_kernel<false> on rank 0",
+                     "peak_source": f"2 x bf16_tflops_sustained of {peak_kind} "
+                                    f"MEASURED_PEAKS.json"},
+        "cpu_baseline": {"value": cpu_v, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                         "sample": f"oracle LU factor+solve U(-1/2,1/2) n={args.cpu_n} on host "
+                                   f"cores (residual {cpu_resid:.4g})"},
+        "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+        "scaled_residual": rep.scaled_residual, "passed": rep.passed, "growth": prob.growth,
+        "native_fp64": native, "breakdown_rank0": breakdown,
+    }), flush=True)
+
+
 # ---------------------------------------------------------------- GPU arm
 def run_ours(args, rank, world):
     import numpy as np
@@ -454,12 +580,20 @@ def main():
         run_reference(args, rank)
         return
     import torch
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        be = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if be == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(be)
     try:
-        run_ours(args, rank, world)
+        if world > 1:
+            run_distributed(args, rank, world)
+        else:
+            run_ours(args, rank, world)
     finally:
         if world > 1:
             import torch.distributed as dist

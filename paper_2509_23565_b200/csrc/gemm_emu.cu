@@ -67,6 +67,7 @@ struct Params {
   int64_t ldo;
   int ngroups;
   int group_m;  // raster band height in tiles
+  int experiment;  // tuning only (OZ_GEMM_EXPERIMENT): 1 = skip FP64 math, 2 = also skip final pass
   uint8_t pa[MAX_PAIRS];
   uint8_t pb[MAX_PAIRS];
   uint16_t gshift[MAX_PAIRS];      // (i+j)*q of the group's pairs
@@ -421,6 +422,7 @@ constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
 constexpr size_t P_SMEM_BYTES = 1024 + (size_t)P_STAGES * P_STAGE_BYTES + 256;
 constexpr uint32_t P_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(P_BN >> 3) << 17) |
                              ((uint32_t)(P_BM >> 4) << 24);
+constexpr int FP_CHUNK = 8;  // final-pass columns with loads in flight at once
 constexpr int P_EPI_ARRIVALS = 2 * (NUM_THREADS / 32 - EPI_WARP0);
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -660,16 +662,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             const int col = col0 + i;
             if (row < p.m && col < p.n) p.debug_out[(int64_t)col * p.ldo + row] = (int32_t)v[i];
           }
-        } else {
+        } else if (p.experiment == 0) {
           const double s = pow2(-(int)p.gshift[q]);
 #pragma unroll
           for (int i = 0; i < 64; ++i) acc[i] = fma(i32_to_f64(v[i]), s, acc[i]);
         }
       }
-      if (kDebug) continue;
+      if (kDebug || p.experiment >= 2) continue;
       if (row < p.m) {
-        // final pass, 8 columns per (rolled) iteration; the accumulator
-        // registers shift down by 8 after each chunk so indices stay static
+        // final pass, FP_CHUNK columns per (rolled) iteration; the accumulator
+        // registers shift down by FP_CHUNK after each chunk so indices stay static
         const int er = p.expA[row];
         const bool use_c = p.c_is_input && p.beta != 0.0;
         const int ncols = min(64, p.n - col0);
@@ -677,18 +679,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         double* cbase = p.c + (int64_t)col0 * ldc + row;
         const int32_t* ebase = p.expB + col0;
 #pragma unroll 1
-        for (int c0 = 0; c0 < ncols; c0 += 8) {
-          int eb[8];
-          double cv[8];
+        for (int c0 = 0; c0 < ncols; c0 += FP_CHUNK) {
+          int eb[FP_CHUNK];
+          double cv[FP_CHUNK];
           double* cp = cbase + (int64_t)c0 * ldc;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < FP_CHUNK; ++i) {
             const bool ok = c0 + i < ncols;
             eb[i] = ok ? __ldg(ebase + c0 + i) : 0;
             cv[i] = (ok && use_c) ? cp[i * ldc] : 0.0;
           }
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < FP_CHUNK; ++i) {
             if (c0 + i < ncols) {
               const double ab = ldexp_exact(acc[i], er + eb[i]);
               double out = __dmul_rn(p.alpha, ab);
@@ -698,7 +700,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             }
           }
 #pragma unroll
-          for (int i = 0; i < 56; ++i) acc[i] = acc[i + 8];
+          for (int i = 0; i < 64 - FP_CHUNK; ++i) acc[i] = acc[i + FP_CHUNK];
         }
       }
     }
@@ -818,6 +820,7 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStr
   p.nkb = (int)ceil_div(p.inner, BK);
   p.group_m = GROUP_M;
   if (const char* g = getenv("OZ_GEMM_GROUPM")) p.group_m = atoi(g) > 0 ? atoi(g) : GROUP_M;
+  if (const char* e = getenv("OZ_GEMM_EXPERIMENT")) p.experiment = atoi(e);
   int grid = sm_count() & ~1;
   if (const char* g = getenv("OZ_GEMM_GRID")) grid = atoi(g) > 0 ? (atoi(g) & ~1) : grid;
   if (grid > 2 * p.num_tiles) grid = 2 * p.num_tiles;

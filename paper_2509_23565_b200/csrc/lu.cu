@@ -473,8 +473,22 @@ __global__ void __launch_bounds__(LSWP_WARPS * 32) laswp_list_kernel(
        ci += (int64_t)gridDim.x * LSWP_WARPS) {
     const int64_t col = ci < na ? c0a + ci : c0b + (ci - na);
     double* colp = a + col * lda;
-    for (int e = lane; e < cnt; e += 32) stage[e] = colp[ss[e]];
+    // 8 independent scattered loads in flight per lane
+    for (int e0 = lane; e0 < cnt; e0 += 32 * 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + 32 * u;
+        v[u] = e < cnt ? colp[ss[e]] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + 32 * u;
+        if (e < cnt) stage[e] = v[u];
+      }
+    }
     __syncwarp();
+#pragma unroll 8
     for (int e = lane; e < cnt; e += 32) colp[sd[e]] = stage[e];
     __syncwarp();
   }
@@ -908,10 +922,27 @@ int laswp_ipiv(double* a, int64_t lda, int64_t c0a, int64_t c1a, int64_t c0b, in
 // applied to the panel's own columns only; ipiv[0..jb) receives the global
 // pivot rows, info the first zero pivot (global column + 1), growth the max
 // |entry| seen.  The caller applies ipiv to the other columns (laswp_ipiv).
+// Widest window (<= PANEL_W) whose m-row slab fits in the shared memory of
+// max_ctas CTAs: tall panels (distributed runs, m ~ 1e5) use narrower windows.
+int panel_width_for(int64_t m, int max_ctas) {
+  int dev = 0, smem = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const int64_t cap = (int64_t)smem - (int64_t)sizeof(PanelShared) - 1024;
+  const int64_t rows = ceil_div(m, max_ctas);
+  int64_t w = (cap / rows - (int64_t)sizeof(int)) / (int64_t)sizeof(double);
+  if (w > PANEL_W) w = PANEL_W;
+  if (w >= 16) w &= ~7;  // keep the window a multiple of 8 columns
+  return (int)w;
+}
+
 int panel_factor(double* a, int64_t lda, int64_t m, int64_t jb, int64_t base, int32_t* ipiv,
                  int32_t* info, unsigned long long* growth, const LuWs& ws, cudaStream_t st) {
-  for (int64_t jj = 0; jj < jb; jj += PANEL_W) {
-    const int w = (int)((jb - jj) < PANEL_W ? (jb - jj) : PANEL_W);
+  const int wmax = panel_width_for(m, sm_count());
+  OZ_REQUIRE(wmax >= 1, OZ_UNSUPPORTED, "a panel of %lld rows does not fit on chip",
+             (long long)m);
+  for (int64_t jj = 0; jj < jb; jj += wmax) {
+    const int w = (int)((jb - jj) < wmax ? (jb - jj) : wmax);
     OZ_TRY(panel_window(a, lda, jj, m - jj, w, base, ipiv, info, growth, ws, st));
     OZ_TRY(apply_list(a, lda, ws, 0, jj, jj + w, jb, st));
     const int64_t rest = jb - (jj + w);

@@ -39,7 +39,7 @@ from . import _dev, _lib
 from .errors import InvalidParamsError, SingularPivotError
 from .gemm import BackendKind, GemmBackend, pair_table
 
-__all__ = ["Comm", "DeviceOps", "HplReport", "local_cols_before", "local_ncols",
+__all__ = ["Comm", "DeviceOps", "HplReport", "HplProblem", "local_cols_before", "local_ncols",
            "global_cols", "factor_block_cyclic", "solve_block_cyclic", "hpl_run"]
 
 
@@ -367,39 +367,73 @@ def _residual(ops, comm, n, nb, x, b):
                    float(b.abs().max().item()), n)
 
 
+class HplProblem:
+    """One distributed HPL problem kept resident: the generated matrix (a
+    pristine copy of every rank's slab), the replicated b = A @ 1, and the
+    buffers of the factorization.  ``step()`` = restore + factor + solve."""
+
+    def __init__(self, n: int, nb: int, backend: GemmBackend | None = None, *,
+                 matrix: str = "uniform", seed: int = 99, depth: int = 4, block: int = 15,
+                 alpha: float = 0.5, comm: Comm | None = None, ops: DeviceOps | None = None):
+        from .matgen import GEN_PARAWILK_RANDOMIZED, GEN_UNIFORM
+        self.backend = backend or GemmBackend.native()
+        self.comm = comm or Comm()
+        if not 1 <= nb <= min(n, 1024):
+            raise InvalidParamsError(f"nb must be in 1..{min(n, 1024)}, got {nb}")
+        self.n, self.nb = n, nb
+        self.ops = ops or DeviceOps(n, nb, self.comm.size, self.comm.rank, self.backend)
+        self.gen = (GEN_UNIFORM if matrix == "uniform" else GEN_PARAWILK_RANDOMIZED, seed, depth,
+                    block, alpha)
+        self.ops.generate(*self.gen)
+        self.b = _replicated_rhs(self.ops, self.comm)
+        self.a0 = self.ops.slab.clone() if isinstance(self.ops, DeviceOps) else None
+        self.growth = None
+
+    def restore(self) -> None:
+        if self.a0 is not None:
+            self.ops.slab.copy_(self.a0)
+        else:
+            self.ops.generate(*self.gen)
+
+    def factor_solve(self):
+        from .solve import ipiv_to_perm
+        ipiv, self.growth = factor_block_cyclic(self.ops, self.comm, self.n, self.nb)
+        return solve_block_cyclic(self.ops, self.comm, self.n, self.nb, ipiv_to_perm(ipiv),
+                                  self.b.cpu().numpy())
+
+    def step(self):
+        self.restore()
+        return self.factor_solve()
+
+    def verify(self, x):
+        self.restore()
+        return _residual(self.ops, self.comm, self.n, self.nb, x, self.b)
+
+
 def hpl_run(n: int, nb: int, backend: GemmBackend | None = None, *, matrix: str = "uniform",
             seed: int = 99, depth: int = 4, block: int = 15, alpha: float = 0.5,
             comm: Comm | None = None, ops: DeviceOps | None = None) -> HplReport:
     """Generate the matrix distributed (hpl_uniform or randomized ParaWilk,
     matgen.py:149-171), b = A @ 1, factor, solve and verify.  Times factor and
     solve with device events, max over ranks."""
-    from .matgen import GEN_PARAWILK_RANDOMIZED, GEN_UNIFORM
     import torch
-    if backend is None:
-        backend = GemmBackend.native()
-    comm = comm or Comm()
-    if not 1 <= nb <= min(n, 1024):
-        raise InvalidParamsError(f"nb must be in 1..{min(n, 1024)}, got {nb}")
-    if ops is None:
-        ops = DeviceOps(n, nb, comm.size, comm.rank, backend)
-    kind = GEN_UNIFORM if matrix == "uniform" else GEN_PARAWILK_RANDOMIZED
-    ops.generate(kind, seed, depth, block, alpha)
-    b = _replicated_rhs(ops, comm)
+    prob = HplProblem(n, nb, backend, matrix=matrix, seed=seed, depth=depth, block=block,
+                      alpha=alpha, comm=comm, ops=ops)
+    comm, backend = prob.comm, prob.backend
+    prob.restore()
     comm.barrier()
     torch.cuda.synchronize()
     e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
     e0.record()
-    ipiv, growth = factor_block_cyclic(ops, comm, n, nb)
-    e1.record()
     from .solve import ipiv_to_perm
-    perm = ipiv_to_perm(ipiv)
-    x = solve_block_cyclic(ops, comm, n, nb, perm, b.cpu().numpy())
+    ipiv, growth = factor_block_cyclic(prob.ops, comm, n, nb)
+    e1.record()
+    x = solve_block_cyclic(prob.ops, comm, n, nb, ipiv_to_perm(ipiv), prob.b.cpu().numpy())
     e2.record()
     torch.cuda.synchronize()
     tf, ts = comm.allreduce_values([e0.elapsed_time(e1) / 1e3, e1.elapsed_time(e2) / 1e3],
                                    "max")
-    ops.generate(kind, seed, depth, block, alpha)          # A again for the residual
-    rep = _residual(ops, comm, n, nb, x, b)
+    rep = prob.verify(x)
     return HplReport(n=n, nb=nb, grid=f"1x{comm.size}", backend=backend.describe(),
                      scaled_residual=rep.scaled_residual, raw_residual_inf=rep.raw_residual_inf,
                      norm_a_inf=rep.norm_a_inf, norm_x_inf=rep.norm_x_inf,
