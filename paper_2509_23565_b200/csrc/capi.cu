@@ -80,15 +80,18 @@ int sm_count() {
 // One cuBLAS handle per (device, host thread): handles are not thread-safe to
 // share while switching streams, and the reference harness may call from a
 // thread pool (harness.py:56-72).
-static cublasHandle_t cublas_handle() {
-  static thread_local std::unordered_map<int, cublasHandle_t> handles;
+// One handle per (device, stream): cuBLAS keeps a per-handle workspace, so
+// streams that run concurrently (the LU look-ahead) must not share one.
+static cublasHandle_t cublas_handle(cudaStream_t st) {
+  static thread_local std::unordered_map<uint64_t, cublasHandle_t> handles;
   int dev = 0;
   cudaGetDevice(&dev);
-  auto it = handles.find(dev);
+  const uint64_t key = ((uint64_t)dev << 56) ^ (uint64_t)(uintptr_t)st;
+  auto it = handles.find(key);
   if (it != handles.end()) return it->second;
   cublasHandle_t h = nullptr;
   if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
-  handles[dev] = h;
+  handles[key] = h;
   return h;
 }
 
@@ -96,7 +99,7 @@ int dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha,
           int64_t lda, const double* b, int64_t ldb, double beta, double* c, int64_t ldc,
           cudaStream_t st) {
   if (m == 0 || n == 0) return OZ_OK;
-  cublasHandle_t h = cublas_handle();
+  cublasHandle_t h = cublas_handle(st);
   OZ_REQUIRE(h != nullptr, OZ_CUDA_ERROR, "cublasCreate failed");
   OZ_REQUIRE(cublasSetStream(h, st) == CUBLAS_STATUS_SUCCESS, OZ_CUDA_ERROR,
              "cublasSetStream failed");

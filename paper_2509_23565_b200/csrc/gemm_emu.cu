@@ -803,7 +803,8 @@ bool use_pair_kernel() {
   return !single;
 }
 
-int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStream_t st) {
+int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStream_t st,
+                int max_ctas = 0) {
   static bool attr_set = false;
   if (!attr_set) {
     OZ_CHECK_CUDA(cudaFuncSetAttribute(emu_gemm_pair_kernel<false>,
@@ -823,6 +824,8 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStr
   if (const char* e = getenv("OZ_GEMM_EXPERIMENT")) p.experiment = atoi(e);
   int grid = sm_count() & ~1;
   if (const char* g = getenv("OZ_GEMM_GRID")) grid = atoi(g) > 0 ? (atoi(g) & ~1) : grid;
+  if (max_ctas > 0 && grid > (max_ctas & ~1)) grid = max_ctas & ~1;
+  if (grid < 2) grid = 2;
   if (grid > 2 * p.num_tiles) grid = 2 * p.num_tiles;
   if (p.debug_out != nullptr)
     emu_gemm_pair_kernel<true><<<grid, NUM_THREADS, P_SMEM_BYTES, st>>>(ta, tb, p);
@@ -860,7 +863,7 @@ int gemm_emu_launch(int64_t m, int64_t n, int64_t inner, const int8_t* a_slices,
                     const int32_t* b_exps, int npairs, const int32_t* pair_a,
                     const int32_t* pair_b, const int32_t* pair_shift, double alpha, double beta,
                     double* c, int64_t ldc, int c_is_input, unsigned long long* growth,
-                    cudaStream_t st) {
+                    cudaStream_t st, int max_ctas) {
   using namespace emu;
   OZ_REQUIRE(m >= 1 && n >= 1 && inner >= 1, OZ_INVALID_PARAMS, "empty GEMM");
   OZ_REQUIRE(m < (1ll << 31) && n < (1ll << 31), OZ_INVALID_PARAMS, "dimension too large");
@@ -897,7 +900,7 @@ int gemm_emu_launch(int64_t m, int64_t n, int64_t inner, const int8_t* a_slices,
   OZ_TRY(make_slice_map(&ta, a_slices, inner, m, a_ld, a_sstride, a_nslices, BM));
   OZ_TRY(make_slice_map(&tb, b_slices, inner, n, b_ld, b_sstride, b_nslices,
                         pair ? P_BN / 2 : BN));
-  return pair ? launch_pair(ta, tb, p, st) : launch(ta, tb, p, st);
+  return pair ? launch_pair(ta, tb, p, st, max_ctas) : launch(ta, tb, p, st);
 }
 
 }  // namespace oz
@@ -914,7 +917,7 @@ extern "C" int oz_gemm_emu(int64_t m, int64_t n, int64_t inner, const int8_t* a_
   const int s = oz::gemm_emu_launch(m, n, inner, a_slices, a_ld, a_sstride, a_nslices, a_exps,
                                     b_slices, b_ld, b_sstride, b_nslices, b_exps, npairs, pair_a,
                                     pair_b, pair_shift, alpha, beta, c, ldc, c_is_input,
-                                    growth_max, st);
+                                    growth_max, st, 0);
   oz::prof_stop(tag, st, oz::PROF_EMU_GEMM, 2.0 * npairs * (double)m * n * inner);
   return s;
 }

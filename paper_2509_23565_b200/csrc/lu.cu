@@ -42,7 +42,7 @@ int gemm_emu_launch(int64_t m, int64_t n, int64_t inner, const int8_t* a_slices,
                     const int32_t* b_exps, int npairs, const int32_t* pair_a,
                     const int32_t* pair_b, const int32_t* pair_shift, double alpha, double beta,
                     double* c, int64_t ldc, int c_is_input, unsigned long long* growth,
-                    cudaStream_t st);
+                    cudaStream_t st, int max_ctas);
 
 namespace {
 
@@ -830,7 +830,7 @@ int trsm_blocked(double* a, int64_t lda, int64_t j, int64_t jb, double* b, int64
 
 int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t base,
                  int32_t* ipiv, int32_t* info, unsigned long long* growth, const LuWs& ws,
-                 cudaStream_t st) {
+                 cudaStream_t st, int max_ctas) {
   static int max_smem = 0;
   if (!max_smem) {
     int dev = 0;
@@ -840,7 +840,7 @@ int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t b
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        max_smem - (int)sizeof(PanelShared) - 1024));
   }
-  const int sms = sm_count();
+  const int sms = max_ctas > 0 && max_ctas < sm_count() ? max_ctas : sm_count();
   const size_t cap = (size_t)max_smem - sizeof(PanelShared) - 1024;
   int G = (int)ceil_div(m, 256);
   if (G > sms) G = sms;
@@ -937,13 +937,15 @@ int panel_width_for(int64_t m, int max_ctas) {
 }
 
 int panel_factor(double* a, int64_t lda, int64_t m, int64_t jb, int64_t base, int32_t* ipiv,
-                 int32_t* info, unsigned long long* growth, const LuWs& ws, cudaStream_t st) {
-  const int wmax = panel_width_for(m, sm_count());
+                 int32_t* info, unsigned long long* growth, const LuWs& ws, cudaStream_t st,
+                 int max_ctas = 0) {
+  const int ctas = max_ctas > 0 && max_ctas < sm_count() ? max_ctas : sm_count();
+  const int wmax = panel_width_for(m, ctas);
   OZ_REQUIRE(wmax >= 1, OZ_UNSUPPORTED, "a panel of %lld rows does not fit on chip",
              (long long)m);
   for (int64_t jj = 0; jj < jb; jj += wmax) {
     const int w = (int)((jb - jj) < wmax ? (jb - jj) : wmax);
-    OZ_TRY(panel_window(a, lda, jj, m - jj, w, base, ipiv, info, growth, ws, st));
+    OZ_TRY(panel_window(a, lda, jj, m - jj, w, base, ipiv, info, growth, ws, st, ctas));
     OZ_TRY(apply_list(a, lda, ws, 0, jj, jj + w, jb, st));
     const int64_t rest = jb - (jj + w);
     if (rest > 0) {
@@ -960,30 +962,97 @@ int panel_factor(double* a, int64_t lda, int64_t m, int64_t jb, int64_t base, in
   return OZ_OK;
 }
 
-// A22 (m x ncols) -= A21 (m x jb) @ U12 (jb x ncols) through the selected
-// backend (solve.py:130-134), growth = max |A22| after the update (:135).
+// The Schur update A22 (m x ncols) -= A21 (m x jb) @ U12 (jb x ncols) through
+// the selected backend (solve.py:130-134), growth = max |A22| after the
+// update (:135).  Split once (schur_split), then update any column range
+// [c0, c1) of A22 (schur_cols) — the look-ahead updates the next panel's
+// columns first and the rest on fewer SMs.
+struct Schur {
+  int backend;
+  int64_t m, ncols, jb;
+  const double* a21;
+  int64_t lda21;
+  const double* u12;
+  int64_t ldu;
+  double* a22;
+  int64_t lda22;
+  int k, q, npairs;
+  const int32_t *pa, *pb, *ps;
+  unsigned long long* growth;
+};
+
+int schur_split(const Schur& s, const LuWs& ws, cudaStream_t st) {
+  if (s.backend == 0 || s.m <= 0 || s.ncols <= 0) return OZ_OK;
+  const int tag = prof_start(st);
+  OZ_TRY(split_launch(s.a21, s.m, s.jb, 1, s.lda21, OZ_ROW_SCALED, OZ_PER_VECTOR, s.k, s.q, ws.slA,
+                      ws.ldK, s.m * ws.ldK, ws.expA, ws.split_aux, st));
+  OZ_TRY(split_launch(s.u12, s.jb, s.ncols, 1, s.ldu, OZ_COL_SCALED, OZ_PER_VECTOR, s.k, s.q,
+                      ws.slB, ws.ldK, s.ncols * ws.ldK, ws.expB, ws.split_aux, st));
+  prof_stop(tag, st, PROF_SPLIT, (double)(s.m + s.ncols) * s.jb * (8.0 + s.k));
+  return OZ_OK;
+}
+
+int schur_cols(const Schur& s, int64_t c0, int64_t c1, const LuWs& ws, cudaStream_t st,
+               int max_ctas = 0) {
+  const int64_t nc = c1 - c0;
+  if (s.m <= 0 || nc <= 0) return OZ_OK;
+  double* c = s.a22 + c0 * s.lda22;
+  if (s.backend == 0) {
+    const int tag = prof_start(st);
+    OZ_TRY(dgemm(0, 0, s.m, nc, s.jb, -1.0, s.a21, s.lda21, s.u12 + c0 * s.ldu, s.ldu, 1.0, c,
+                 s.lda22, st));
+    prof_stop(tag, st, PROF_DGEMM, 2.0 * s.m * nc * s.jb);
+    return max_abs(c, s.m, nc, 1, s.lda22, 0, 0, s.growth, st);
+  }
+  const int tag = prof_start(st);
+  OZ_TRY(gemm_emu_launch(s.m, nc, s.jb, ws.slA, ws.ldK, s.m * ws.ldK, s.k, ws.expA,
+                         ws.slB + c0 * ws.ldK, ws.ldK, s.ncols * ws.ldK, s.k, ws.expB + c0,
+                         s.npairs, s.pa, s.pb, s.ps, -1.0, 1.0, c, s.lda22, 1, s.growth, st,
+                         max_ctas));
+  prof_stop(tag, st, PROF_EMU_GEMM, 2.0 * s.npairs * s.m * nc * s.jb);
+  return OZ_OK;
+}
+
 int schur_update(int backend, int64_t m, int64_t ncols, int64_t jb, const double* a21,
                  int64_t lda21, const double* u12, int64_t ldu, double* a22, int64_t lda22, int k,
                  int q, int npairs, const int32_t* pa, const int32_t* pb, const int32_t* ps,
                  unsigned long long* growth, const LuWs& ws, cudaStream_t st) {
-  if (m <= 0 || ncols <= 0) return OZ_OK;
-  if (backend == 0) {
-    const int tag = prof_start(st);
-    OZ_TRY(dgemm(0, 0, m, ncols, jb, -1.0, a21, lda21, u12, ldu, 1.0, a22, lda22, st));
-    prof_stop(tag, st, PROF_DGEMM, 2.0 * m * ncols * jb);
-    return max_abs(a22, m, ncols, 1, lda22, 0, 0, growth, st);
+  const Schur s{backend, m, ncols, jb, a21, lda21, u12, ldu, a22, lda22, k, q, npairs, pa, pb,
+                ps, growth};
+  OZ_TRY(schur_split(s, ws, st));
+  return schur_cols(s, 0, ncols, ws, st);
+}
+
+// Look-ahead (depth 1): the next panel is factored on a side stream with
+// OZ_LOOKAHEAD_SMS CTAs (default 40; 0 disables) while the rest of the Schur
+// update runs on the remaining SMs.
+int lookahead_sms() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("OZ_LOOKAHEAD_SMS");
+    v = e ? atoi(e) : 40;
+    if (v < 0) v = 0;
+    v &= ~1;
   }
-  const int64_t ssa = m * ws.ldK, ssb = ncols * ws.ldK;
-  int tag = prof_start(st);
-  OZ_TRY(split_launch(a21, m, jb, 1, lda21, OZ_ROW_SCALED, OZ_PER_VECTOR, k, q, ws.slA, ws.ldK,
-                      ssa, ws.expA, ws.split_aux, st));
-  OZ_TRY(split_launch(u12, jb, ncols, 1, ldu, OZ_COL_SCALED, OZ_PER_VECTOR, k, q, ws.slB, ws.ldK,
-                      ssb, ws.expB, ws.split_aux, st));
-  prof_stop(tag, st, PROF_SPLIT, (double)(m + ncols) * jb * (8.0 + k));
-  tag = prof_start(st);
-  OZ_TRY(gemm_emu_launch(m, ncols, jb, ws.slA, ws.ldK, ssa, k, ws.expA, ws.slB, ws.ldK, ssb, k,
-                         ws.expB, npairs, pa, pb, ps, -1.0, 1.0, a22, lda22, 1, growth, st));
-  prof_stop(tag, st, PROF_EMU_GEMM, 2.0 * npairs * m * ncols * jb);
+  return v;
+}
+
+struct SideStream {
+  cudaStream_t st = nullptr;
+  cudaEvent_t ready = nullptr, done = nullptr;
+};
+int side_stream(SideStream** out) {
+  static thread_local std::vector<SideStream> per_dev;
+  int dev = 0;
+  OZ_CHECK_CUDA(cudaGetDevice(&dev));
+  if ((int)per_dev.size() <= dev) per_dev.resize(dev + 1);
+  SideStream& s = per_dev[dev];
+  if (!s.st) {
+    OZ_CHECK_CUDA(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
+    OZ_CHECK_CUDA(cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming));
+    OZ_CHECK_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+  }
+  *out = &s;
   return OZ_OK;
 }
 
@@ -1010,12 +1079,15 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
   OZ_CHECK_CUDA(cudaMemsetAsync(info, 0, sizeof(int32_t), st));
   OZ_TRY(max_abs(a, n, n, 1, lda, 0, 0, ws.bits + 1, st));
 
+  const int la_sms = lookahead_sms();
+  SideStream* side = nullptr;
+  if (la_sms > 0) OZ_TRY(side_stream(&side));
+  // panel 0; every later panel is factored at the end of the previous step
+  OZ_TRY(panel_factor(a, lda, n, nb < n ? nb : n, 0, ipiv, info, ws.bits, ws, st));
   for (int64_t j = 0; j < n; j += nb) {
     const int64_t jb = nb < n - j ? nb : n - j;
-    // ---- panel (columns j..j+jb), then its interchanges on every other
-    //      column: whole-row swaps (solve.py:80-82)
-    double* ajj = a + j * lda + j;
-    OZ_TRY(panel_factor(ajj, lda, n - j, jb, j, ipiv + j, info, ws.bits, ws, st));
+    // ---- the panel's interchanges on every other column: whole-row swaps
+    //      (solve.py:80-82)
     OZ_TRY(laswp_ipiv(a, lda, 0, j, j + jb, n, j, ipiv + j, (int)jb, ws, st));
     const int64_t rest = n - j - jb;
     if (rest > 0) {
@@ -1023,8 +1095,25 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
       double* a21 = a + j * lda + (j + jb);
       double* a22 = a + (j + jb) * lda + (j + jb);
       OZ_TRY(trsm_blocked(a, lda, j, jb, a12, lda, rest, st));  // solve.py:123-127
-      OZ_TRY(schur_update(backend, rest, rest, jb, a21, lda, a12, lda, a22, lda, k, q, npairs,
-                          pa, pb, ps, ws.bits, ws, st));     // solve.py:130-134
+      const Schur sc{backend, rest, rest, jb, a21, lda, a12, lda, a22, lda, k, q, npairs, pa, pb,
+                     ps, ws.bits};
+      OZ_TRY(schur_split(sc, ws, st));                         // solve.py:130-134
+      // the next panel's columns first, then its factorization (look-ahead)
+      const int64_t jb2 = nb < rest ? nb : rest;
+      OZ_TRY(schur_cols(sc, 0, jb2, ws, st));
+      double* p2 = a + (j + jb) * lda + (j + jb);
+      if (side != nullptr && rest > jb2) {
+        OZ_CHECK_CUDA(cudaEventRecord(side->ready, st));
+        OZ_CHECK_CUDA(cudaStreamWaitEvent(side->st, side->ready, 0));
+        OZ_TRY(panel_factor(p2, lda, rest, jb2, j + jb, ipiv + j + jb, info, ws.bits, ws,
+                            side->st, la_sms));
+        OZ_CHECK_CUDA(cudaEventRecord(side->done, side->st));
+        OZ_TRY(schur_cols(sc, jb2, rest, ws, st, sm_count() - la_sms));
+        OZ_CHECK_CUDA(cudaStreamWaitEvent(st, side->done, 0));
+      } else {
+        OZ_TRY(schur_cols(sc, jb2, rest, ws, st));
+        OZ_TRY(panel_factor(p2, lda, rest, jb2, j + jb, ipiv + j + jb, info, ws.bits, ws, st));
+      }
     }
     // finalized U rows of this panel: triu(lu[j:j+jb, j:]) (solve.py:135-137)
     OZ_TRY(max_abs(a + j * lda + j, jb, n - j, 1, lda, 1, 0, ws.bits, st));
