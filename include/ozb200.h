@@ -215,6 +215,21 @@ int oz_schur_update(int backend, int64_t m, int64_t ncols, int64_t jb, const dou
                     const int32_t* pair_b, const int32_t* pair_shift,
                     unsigned long long* growth_bits, void* workspace, size_t workspace_bytes,
                     int64_t ws_n, int64_t ws_nb, void* stream);
+/* The same update in two calls for look-ahead drivers: oz_schur_split splits
+ * A21 (row-scaled) and U12 (column-scaled) into the workspace once (backend 1;
+ * a no-op for backend 0), oz_schur_cols then updates columns [c0, c1) of A22
+ * on at most max_ctas CTAs (0 = all SMs). */
+int oz_schur_split(int backend, int64_t m, int64_t ncols, int64_t jb, const double* a21,
+                   int64_t lda21, const double* u12, int64_t ldu, int num_slices, int slice_bits,
+                   void* workspace, size_t workspace_bytes, int64_t ws_n, int64_t ws_nb,
+                   void* stream);
+int oz_schur_cols(int backend, int64_t m, int64_t ncols, int64_t jb, const double* a21,
+                  int64_t lda21, const double* u12, int64_t ldu, double* a22, int64_t lda22,
+                  int num_slices, int slice_bits, int npairs, const int32_t* pair_a,
+                  const int32_t* pair_b, const int32_t* pair_shift,
+                  unsigned long long* growth_bits, int64_t c0, int64_t c1, int max_ctas,
+                  void* workspace, size_t workspace_bytes, int64_t ws_n, int64_t ws_nb,
+                  void* stream);
 int oz_max_abs_bits(const double* a, int64_t m, int64_t n, int64_t row_stride,
                     int64_t col_stride, int upper, unsigned long long* bits, void* stream);
 

@@ -59,6 +59,10 @@ _SIGNATURES = {
     "oz_schur_update": [_int, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int, _int, _int,
                         _vp, _vp, _vp, _vp, _vp, C.c_size_t, _i64, _i64, _vp],
     "oz_max_abs_bits": [_vp, _i64, _i64, _i64, _i64, _int, _vp, _vp],
+    "oz_schur_split": [_int, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _int, _int, _vp, C.c_size_t,
+                       _i64, _i64, _vp],
+    "oz_schur_cols": [_int, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int, _int, _int,
+                      _vp, _vp, _vp, _vp, _i64, _i64, _int, _vp, C.c_size_t, _i64, _i64, _vp],
     "oz_trsv_block": [_vp, _i64, _i64, _int, _vp, _vp, _vp, C.c_size_t, _vp],
     "oz_gemv_partial": [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp],
     "oz_generate_cyclic": [_int, _i64, _i64, _i64, _dbl, _u64, _u64, _u64, _u64, _i64, _i64,

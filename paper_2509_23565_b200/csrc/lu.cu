@@ -1374,3 +1374,41 @@ extern "C" int oz_gemv_partial(const double* a, int64_t rows, int64_t cols, int6
   cudaFreeAsync(part, st);
   return s;
 }
+
+// The Schur update in two calls (look-ahead drivers): split A21/U12 once,
+// then update column ranges [c0, c1) of A22, optionally on at most max_ctas
+// CTAs (0 = all SMs) so a concurrent panel or collective keeps some SMs.
+extern "C" int oz_schur_split(int backend, int64_t m, int64_t ncols, int64_t jb,
+                              const double* a21, int64_t lda21, const double* u12, int64_t ldu,
+                              int num_slices, int slice_bits, void* ws, size_t ws_bytes,
+                              int64_t ws_n, int64_t ws_nb, void* stream) {
+  using namespace oz;
+  OZ_REQUIRE(backend == 0 || backend == 1, OZ_INVALID_PARAMS, "bad backend");
+  if (backend == 0) return OZ_OK;
+  OZ_REQUIRE(m <= ws_n && ncols <= ws_n && jb <= ws_nb, OZ_INVALID_PARAMS,
+             "schur update larger than the workspace");
+  LuWs w;
+  OZ_TRY(ws_view(ws, ws_bytes, ws_n, ws_nb, num_slices, &w));
+  const Schur s{backend, m, ncols, jb, a21, lda21, u12, ldu, nullptr, 0, num_slices, slice_bits,
+                0, nullptr, nullptr, nullptr, nullptr};
+  return schur_split(s, w, as_stream(stream));
+}
+
+extern "C" int oz_schur_cols(int backend, int64_t m, int64_t ncols, int64_t jb,
+                             const double* a21, int64_t lda21, const double* u12, int64_t ldu,
+                             double* a22, int64_t lda22, int num_slices, int slice_bits,
+                             int npairs, const int32_t* pair_a, const int32_t* pair_b,
+                             const int32_t* pair_shift, unsigned long long* growth_bits,
+                             int64_t c0, int64_t c1, int max_ctas, void* ws, size_t ws_bytes,
+                             int64_t ws_n, int64_t ws_nb, void* stream) {
+  using namespace oz;
+  OZ_REQUIRE(backend == 0 || backend == 1, OZ_INVALID_PARAMS, "bad backend");
+  OZ_REQUIRE(0 <= c0 && c0 <= c1 && c1 <= ncols, OZ_INVALID_PARAMS, "bad column range");
+  OZ_REQUIRE(backend == 0 || (m <= ws_n && ncols <= ws_n && jb <= ws_nb), OZ_INVALID_PARAMS,
+             "schur update larger than the workspace");
+  LuWs w;
+  OZ_TRY(ws_view(ws, ws_bytes, ws_n, ws_nb, backend == 1 ? num_slices : 0, &w));
+  const Schur s{backend, m, ncols, jb, a21, lda21, u12, ldu, a22, lda22, num_slices, slice_bits,
+                npairs, pair_a, pair_b, pair_shift, growth_bits};
+  return schur_cols(s, c0, c1, w, as_stream(stream), max_ctas);
+}

@@ -95,6 +95,16 @@ class Comm:
         else:
             self.dist.broadcast(t, self._grank(src), group=self.group)
 
+    def bcast_async(self, t, src: int):
+        """Start a broadcast without making the compute stream wait (NCCL);
+        returns a handle with .wait(), or None when it already completed."""
+        if self.size == 1 or t.numel() == 0:
+            return None
+        if self.stage and t.is_cuda:
+            self.bcast(t, src)
+            return None
+        return self.dist.broadcast(t, self._grank(src), group=self.group, async_op=True)
+
     def allreduce(self, t, op: str) -> None:
         if self.size == 1:
             return
@@ -117,6 +127,12 @@ class Comm:
     def barrier(self) -> None:
         if self.size > 1:
             self.dist.barrier(group=self.group)
+
+
+def _sm_count() -> int:
+    out = np.zeros(1, dtype=np.int32)
+    _lib.call("oz_sm_count", out.ctypes.data)
+    return int(out[0])
 
 
 # ------------------------------------------------------------ device ops
@@ -144,8 +160,11 @@ class DeviceOps:
         dev = "cuda"
         # local slab: torch (ncl, n) row-major == column-major n x ncl, ld = n
         self.slab = t.empty((max(self.ncl, 1), n), dtype=t.float64, device=dev)
-        self.pbuf = t.empty((n * nb,), dtype=t.float64, device=dev)
-        self.ipiv_buf = t.empty((nb,), dtype=t.int32, device=dev)
+        # two panel slots: panel j+1 is factored (look-ahead) while panel j's
+        # L21 still feeds the trailing update
+        self.pbuf = [t.empty((n * nb,), dtype=t.float64, device=dev) for _ in range(2)]
+        self.ipiv_buf = [t.empty((nb,), dtype=t.int32, device=dev) for _ in range(2)]
+        self.sms = int(_sm_count())
         self.ipiv = t.empty((n,), dtype=t.int32, device=dev)
         self.info = t.zeros((1,), dtype=t.int32, device=dev)
         self.bits = t.zeros((2,), dtype=t.int64, device=dev)   # [seen, max|A|] as IEEE bits
@@ -195,43 +214,57 @@ class DeviceOps:
             _lib.call("oz_max_abs_bits", self.slab.data_ptr(), self.n, self.ncl, 1, self.n, 0,
                       self.bits.data_ptr() + 8, self._st())
 
-    def panel(self, lc: int, j: int, jb: int) -> None:
+    def panel(self, lc: int, j: int, jb: int, slot: int = 0) -> None:
         _lib.call("oz_lu_panel", self._a(lc, j), self.n, self.n - j, jb, j,
-                  self.ipiv_buf.data_ptr(), self.info.data_ptr(), self.bits.data_ptr(),
+                  self.ipiv_buf[slot].data_ptr(), self.info.data_ptr(), self.bits.data_ptr(),
                   self.ws.data_ptr(), self.wsb, self.n, self.nb, self.k, self._st())
         # triu of the panel's diagonal block: finalized U rows (solve.py:135-137)
         _lib.call("oz_max_abs_bits", self._a(lc, j), jb, jb, 1, self.n, 1,
                   self.bits.data_ptr(), self._st())
         m = self.n - j
-        _lib.call("oz_copy2d", self._a(lc, j), m, jb, 1, self.n, self.pbuf.data_ptr(), 1, m,
-                  self._st())
+        _lib.call("oz_copy2d", self._a(lc, j), m, jb, 1, self.n, self.pbuf[slot].data_ptr(), 1,
+                  m, self._st())
 
-    def panel_buffers(self, j: int, jb: int):
+    def panel_buffers(self, j: int, jb: int, slot: int = 0):
         m = self.n - j
-        return self.pbuf[:m * jb], self.ipiv_buf[:jb]
+        return self.pbuf[slot][:m * jb], self.ipiv_buf[slot][:jb]
 
-    def record_pivots(self, j: int, jb: int) -> None:
-        self.ipiv[j:j + jb].copy_(self.ipiv_buf[:jb])
+    def record_pivots(self, j: int, jb: int, slot: int = 0) -> None:
+        self.ipiv[j:j + jb].copy_(self.ipiv_buf[slot][:jb])
 
-    def laswp(self, ranges, j: int, jb: int) -> None:
+    def laswp(self, ranges, j: int, jb: int, slot: int = 0) -> None:
         (c0a, c1a), (c0b, c1b) = ranges
         _lib.call("oz_laswp", self.slab.data_ptr(), self.n, c0a, c1a, c0b, c1b, j,
-                  self.ipiv_buf.data_ptr(), jb, self.ws.data_ptr(), self.wsb, self.n, self.nb,
-                  self.k, self._st())
+                  self.ipiv_buf[slot].data_ptr(), jb, self.ws.data_ptr(), self.wsb, self.n,
+                  self.nb, self.k, self._st())
 
-    def update(self, j: int, jb: int, lstart: int, nt: int) -> None:
-        """U12 <- L11^-1 A12, A22 <- A22 - L21 U12 on local columns lstart.."""
+    def trsm_split(self, j: int, jb: int, lstart: int, nt: int, slot: int = 0) -> None:
+        """U12 <- L11^-1 A12 on local columns lstart..lstart+nt, then split
+        L21 / U12 for the trailing update."""
         m = self.n - j
+        pb = self.pbuf[slot].data_ptr()
         u12 = self._a(lstart, j)
-        _lib.call("oz_trsm_lunit", self.pbuf.data_ptr(), m, jb, u12, self.n, nt, self._st())
+        _lib.call("oz_trsm_lunit", pb, m, jb, u12, self.n, nt, self._st())
         _lib.call("oz_max_abs_bits", u12, jb, nt, 1, self.n, 0, self.bits.data_ptr(),
                   self._st())
         if m - jb > 0:
-            _lib.call("oz_schur_update", 1 if self.emulated else 0, m - jb, nt, jb,
-                      self.pbuf.data_ptr() + 8 * jb, m, u12, self.n, self._a(lstart, j + jb),
-                      self.n, self.k, self.qbits, len(self.pa), self.pa.ctypes.data,
-                      self.pb.ctypes.data, self.ps.ctypes.data, self.bits.data_ptr(),
-                      self.ws.data_ptr(), self.wsb, self.n, self.nb, self._st())
+            _lib.call("oz_schur_split", 1 if self.emulated else 0, m - jb, nt, jb, pb + 8 * jb, m,
+                      u12, self.n, self.k, self.qbits, self.ws.data_ptr(), self.wsb, self.n,
+                      self.nb, self._st())
+
+    def schur_cols(self, j: int, jb: int, lstart: int, nt: int, c0: int, c1: int,
+                   slot: int = 0, reserve_sms: int = 0) -> None:
+        """A22 -= L21 U12 on trailing local columns lstart+c0 .. lstart+c1."""
+        m = self.n - j
+        if m - jb <= 0 or c1 <= c0:
+            return
+        max_ctas = self.sms - reserve_sms if reserve_sms > 0 else 0
+        _lib.call("oz_schur_cols", 1 if self.emulated else 0, m - jb, nt, jb,
+                  self.pbuf[slot].data_ptr() + 8 * jb, m, self._a(lstart, j), self.n,
+                  self._a(lstart, j + jb), self.n, self.k, self.qbits, len(self.pa),
+                  self.pa.ctypes.data, self.pb.ctypes.data, self.ps.ctypes.data,
+                  self.bits.data_ptr(), c0, c1, max_ctas, self.ws.data_ptr(), self.wsb, self.n,
+                  self.nb, self._st())
 
     def finish(self):
         """-> (ipiv host int32[n], info, seen, max|A|) of this rank."""
@@ -259,32 +292,75 @@ class DeviceOps:
 
 
 # ------------------------------------------------------------ the driver
-def factor_block_cyclic(ops, comm, n: int, nb: int):
+def factor_block_cyclic(ops, comm, n: int, nb: int, lookahead: bool = True,
+                        reserve_sms: int = 16):
     """Blocked right-looking LU (solve.py:94-140) of the distributed matrix in
-    ops' local slabs.  Returns (ipiv int32[n] global LAPACK-style, growth)."""
+    ops' local slabs.  Returns (ipiv int32[n] global LAPACK-style, growth).
+
+    Look-ahead (depth 1): the owner of panel b+1 updates that panel's columns
+    first, factors it into the other panel slot and starts its broadcast
+    (asynchronously on NCCL) before updating the rest of its columns on
+    sms - reserve_sms CTAs, so the other ranks find panel b+1 ready when they
+    finish step b.  The arithmetic is identical with or without it."""
     Q, q = comm.size, comm.rank
     ncl = local_ncols(n, nb, Q, q)
+    nblk = -(-n // nb)
     ops.begin()
-    for jblk in range(-(-n // nb)):
+    sends = {}                                   # slot -> in-flight early broadcast handles
+    early = set()                                # panels already factored and sent
+
+    def factor_and_send(b, lc, slot, async_ok):
+        jj = b * nb
+        jjb = min(nb, n - jj)
+        for h in sends.pop(slot, ()):            # the slot's previous send must be done
+            h.wait()
+        ops.panel(lc, jj, jjb, slot)
+        if async_ok:
+            pb, ip = ops.panel_buffers(jj, jjb, slot)
+            sends[slot] = [h for h in (comm.bcast_async(pb, q), comm.bcast_async(ip, q)) if h]
+            early.add(b)
+
+    if q == 0:
+        factor_and_send(0, 0, 0, False)
+    for jblk in range(nblk):
         j = jblk * nb
         jb = min(nb, n - j)
         owner = jblk % Q
-        lc = (jblk // Q) * nb                       # the panel's local column on its owner
-        if q == owner:
-            ops.panel(lc, j, jb)
-        pbuf, ipiv = ops.panel_buffers(j, jb)
-        comm.bcast(pbuf, owner)                     # L11/L21 of the factored panel
-        comm.bcast(ipiv, owner)                     # its jb pivot rows
-        ops.record_pivots(j, jb)
+        slot = jblk % 2
+        lc = (jblk // Q) * nb                   # the panel's local column on its owner
+        if jblk not in early:                    # receive (or, on the owner, send) now
+            pbuf, ipiv = ops.panel_buffers(j, jb, slot)
+            comm.bcast(pbuf, owner)              # L11/L21 of the factored panel
+            comm.bcast(ipiv, owner)              # its jb pivot rows
+        ops.record_pivots(j, jb, slot)
         if q == owner:
             ranges = ((0, lc), (lc + jb, ncl))
         else:
             ranges = ((0, ncl), (ncl, ncl))
-        ops.laswp(ranges, j, jb)
+        ops.laswp(ranges, j, jb, slot)
         lstart = local_cols_before(j + jb, nb, Q, q)
         nt = ncl - lstart
+        nxt = jblk + 1
+        mine_next = nxt < nblk and nxt % Q == q
         if nt > 0:
-            ops.update(j, jb, lstart, nt)
+            ops.trsm_split(j, jb, lstart, nt, slot)
+            if mine_next:
+                jb2 = min(nb, n - nxt * nb)       # the next panel = my first trailing columns
+                ops.schur_cols(j, jb, lstart, nt, 0, jb2, slot)
+                if lookahead:
+                    factor_and_send(nxt, lstart, nxt % 2, Q > 1)
+                    ops.schur_cols(j, jb, lstart, nt, jb2, nt, slot,
+                                   reserve_sms if Q > 1 else 0)
+                else:
+                    ops.schur_cols(j, jb, lstart, nt, jb2, nt, slot)
+                    factor_and_send(nxt, lstart, nxt % 2, False)
+            else:
+                ops.schur_cols(j, jb, lstart, nt, 0, nt, slot)
+        elif mine_next:                          # pragma: no cover (no trailing columns)
+            factor_and_send(nxt, lstart, nxt % 2, False)
+    for hs in sends.values():
+        for h in hs:
+            h.wait()
     ipiv, info, seen, top = ops.finish()
     info, seen, top = comm.allreduce_values([info, seen, top], "max")
     info = int(info)

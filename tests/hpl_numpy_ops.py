@@ -24,8 +24,8 @@ class NumpyOps:
         self.ncl = local_ncols(self.n, nb, Q, q)
         self.gcols = global_cols(self.n, nb, Q, q)
         self.slab = np.asfortranarray(a_full[:, self.gcols])
-        self.pbuf = torch.zeros(self.n * nb, dtype=torch.float64)
-        self.ipiv_buf = torch.zeros(nb, dtype=torch.int32)
+        self.pbuf = [torch.zeros(self.n * nb, dtype=torch.float64) for _ in range(2)]
+        self.ipiv_buf = [torch.zeros(nb, dtype=torch.int32) for _ in range(2)]
         self.ipiv = np.zeros(self.n, dtype=np.int32)
         self.flag = 0
 
@@ -44,7 +44,7 @@ class NumpyOps:
         self.seen = 0.0
         self.top = float(np.abs(self.slab).max()) if self.ncl else 0.0
 
-    def panel(self, lc, j, jb):
+    def panel(self, lc, j, jb, slot=0):
         n = self.n
         a = self.slab
         for t in range(j, j + jb):                               # solve.py:75-90
@@ -54,7 +54,7 @@ class NumpyOps:
                 self.info = t + 1
             if p != t:
                 a[[t, p], lc:lc + jb] = a[[p, t], lc:lc + jb]
-            self.ipiv_buf[t - j] = p
+            self.ipiv_buf[slot][t - j] = p
             if t + 1 < n:
                 a[t + 1:, c] /= a[t, c]
                 if t + 1 < j + jb:
@@ -62,20 +62,20 @@ class NumpyOps:
                     self.seen = max(self.seen, float(np.abs(a[t + 1:, c + 1:lc + jb]).max()))
         self.seen = max(self.seen, float(np.abs(np.triu(a[j:j + jb, lc:lc + jb])).max()))
         m = n - j
-        self.pbuf[:m * jb] = torch.from_numpy(a[j:, lc:lc + jb].ravel(order="F").copy())
+        self.pbuf[slot][:m * jb] = torch.from_numpy(a[j:, lc:lc + jb].ravel(order="F").copy())
 
-    def panel_buffers(self, j, jb):
+    def panel_buffers(self, j, jb, slot=0):
         m = self.n - j
-        return self.pbuf[:m * jb], self.ipiv_buf[:jb]
+        return self.pbuf[slot][:m * jb], self.ipiv_buf[slot][:jb]
 
-    def record_pivots(self, j, jb):
-        self.ipiv[j:j + jb] = self.ipiv_buf[:jb].numpy()
+    def record_pivots(self, j, jb, slot=0):
+        self.ipiv[j:j + jb] = self.ipiv_buf[slot][:jb].numpy()
 
-    def laswp(self, ranges, j, jb):
+    def laswp(self, ranges, j, jb, slot=0):
         cols = np.r_[ranges[0][0]:ranges[0][1], ranges[1][0]:ranges[1][1]].astype(np.int64)
         if cols.size == 0:
             return
-        piv = self.ipiv_buf[:jb].numpy()
+        piv = self.ipiv_buf[slot][:jb].numpy()
         for t in range(jb):
             p = int(piv[t])
             if p != j + t:
@@ -83,18 +83,28 @@ class NumpyOps:
                 self.slab[j + t, cols] = self.slab[p, cols]
                 self.slab[p, cols] = tmp
 
-    def update(self, j, jb, lstart, nt):
+    def _panel(self, j, jb, slot):
         m = self.n - j
-        pan = self.pbuf[:m * jb].numpy().reshape((jb, m)).T      # F-order m x jb
+        return self.pbuf[slot][:m * jb].numpy().reshape((jb, m)).T   # F-order m x jb
+
+    def trsm_split(self, j, jb, lstart, nt, slot=0):
+        pan = self._panel(j, jb, slot)
         a = self.slab
         u12 = solve_triangular(pan[:jb, :jb], a[j:j + jb, lstart:lstart + nt], lower=True,
                                unit_diagonal=True, check_finite=False)
         a[j:j + jb, lstart:lstart + nt] = u12
         self.seen = max(self.seen, float(np.abs(u12).max()))
-        if m - jb > 0:
-            a[j + jb:, lstart:lstart + nt] = orc.gemm(-1.0, pan[jb:, :], u12, 1.0,
-                                                      a[j + jb:, lstart:lstart + nt], k=self.k)
-            self.seen = max(self.seen, float(np.abs(a[j + jb:, lstart:lstart + nt]).max()))
+
+    def schur_cols(self, j, jb, lstart, nt, c0, c1, slot=0, reserve_sms=0):
+        m = self.n - j
+        if m - jb <= 0 or c1 <= c0:
+            return
+        pan = self._panel(j, jb, slot)
+        a = self.slab
+        cols = slice(lstart + c0, lstart + c1)
+        a[j + jb:, cols] = orc.gemm(-1.0, pan[jb:, :], a[j:j + jb, cols], 1.0, a[j + jb:, cols],
+                                    k=self.k)
+        self.seen = max(self.seen, float(np.abs(a[j + jb:, cols]).max()))
 
     def finish(self):
         return self.ipiv.copy(), self.info, self.seen, self.top

@@ -40,7 +40,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, n, nb, k, seed, out):
+def _worker(rank, world, port, n, nb, k, seed, out, lookahead=True):
     import torch.distributed as dist
 
     from hpl_numpy_ops import NumpyOps
@@ -54,7 +54,7 @@ def _worker(rank, world, port, n, nb, k, seed, out):
         comm = hpl.Comm()
         ops = NumpyOps(a, nb, world, rank, k)
         b = a @ np.ones(n)
-        ipiv, growth = hpl.factor_block_cyclic(ops, comm, n, nb)
+        ipiv, growth = hpl.factor_block_cyclic(ops, comm, n, nb, lookahead=lookahead)
         factored = ops.slab.copy()
         from paper_2509_23565_b200.solve import ipiv_to_perm
         perm = ipiv_to_perm(ipiv)
@@ -64,9 +64,10 @@ def _worker(rank, world, port, n, nb, k, seed, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,nb,world,k", [(96, 16, 2, 7), (100, 16, 3, 7), (90, 12, 2, None),
-                                          (70, 8, 3, 3)])
-def test_distributed_lu_matches_oracle(n, nb, world, k):
+@pytest.mark.parametrize("n,nb,world,k,la", [(96, 16, 2, 7, True), (100, 16, 3, 7, True),
+                                             (90, 12, 2, None, True), (70, 8, 3, 3, True),
+                                             (100, 16, 3, 7, False)])
+def test_distributed_lu_matches_oracle(n, nb, world, k, la):
     from oracle import ozaki_oracle as orc
     here = os.path.dirname(os.path.abspath(__file__))
     root = os.path.dirname(here)
@@ -75,7 +76,7 @@ def test_distributed_lu_matches_oracle(n, nb, world, k):
     ctx = mp.get_context("spawn")
     out = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, nb, k, 5, out))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, nb, k, 5, out, la))
              for r in range(world)]
     for p in procs:
         p.start()
