@@ -936,6 +936,42 @@ int panel_width_for(int64_t m, int max_ctas) {
   return (int)w;
 }
 
+// Recursive panel factorization of panel columns [c0, c1) (rows c0..m-1 of
+// the panel's local coordinates).  Leaves of at most wmax columns are one
+// cooperative window kernel each, whose interchanges are applied at once to
+// every other panel column; an inner node factors its left half, updates the
+// right half with trsm + one DGEMM of depth (mid - c0), then factors the right
+// half.  Same arithmetic class as solve.py:75-90 (bit-exact inside a leaf,
+// blocked FP64 updates across leaves) but the in-panel updates are GEMMs of
+// depth nb/2, nb/4, ... instead of nb/wmax rank-wmax updates.
+int panel_rec(double* a, int64_t lda, int64_t m, int64_t jb, int64_t c0, int64_t c1, int wmax,
+              int64_t base, int32_t* ipiv, int32_t* info, unsigned long long* growth,
+              const LuWs& ws, cudaStream_t st, int ctas) {
+  const int64_t w = c1 - c0;
+  if (w <= wmax) {
+    OZ_TRY(panel_window(a, lda, c0, m - c0, (int)w, base, ipiv, info, growth, ws, st, ctas));
+    return apply_list(a, lda, ws, 0, c0, c1, jb, st);
+  }
+  int64_t mid = c0 + ((w / 2 + wmax - 1) / wmax) * wmax;
+  if (mid >= c1) mid = c0 + wmax;
+  OZ_TRY(panel_rec(a, lda, m, jb, c0, mid, wmax, base, ipiv, info, growth, ws, st, ctas));
+  const int64_t kk = mid - c0, right = c1 - mid;
+  OZ_TRY(trsm_blocked(a, lda, c0, kk, a + mid * lda + c0, lda, right, st));
+  if (m - mid > 0) {
+    const int tag = prof_start(st);
+    OZ_TRY(dgemm(0, 0, m - mid, right, kk, -1.0, a + c0 * lda + mid, lda, a + mid * lda + c0,
+                 lda, 1.0, a + mid * lda + mid, lda, st));
+    prof_stop(tag, st, PROF_DGEMM_PANEL, 2.0 * (m - mid) * right * kk);
+  }
+  return panel_rec(a, lda, m, jb, mid, c1, wmax, base, ipiv, info, growth, ws, st, ctas);
+}
+
+// Factor one m x jb column panel in place (solve.py:66-91 for columns
+// j..j+jb of the global matrix): `a` points at the panel's diagonal corner,
+// rows keep the global numbering through `base` (= j).  Interchanges are
+// applied to the panel's own columns only; ipiv[0..jb) receives the global
+// pivot rows, info the first zero pivot (global column + 1), growth the max
+// |entry| seen.  The caller applies ipiv to the other columns (laswp_ipiv).
 int panel_factor(double* a, int64_t lda, int64_t m, int64_t jb, int64_t base, int32_t* ipiv,
                  int32_t* info, unsigned long long* growth, const LuWs& ws, cudaStream_t st,
                  int max_ctas = 0) {
@@ -943,23 +979,7 @@ int panel_factor(double* a, int64_t lda, int64_t m, int64_t jb, int64_t base, in
   const int wmax = panel_width_for(m, ctas);
   OZ_REQUIRE(wmax >= 1, OZ_UNSUPPORTED, "a panel of %lld rows does not fit on chip",
              (long long)m);
-  for (int64_t jj = 0; jj < jb; jj += wmax) {
-    const int w = (int)((jb - jj) < wmax ? (jb - jj) : wmax);
-    OZ_TRY(panel_window(a, lda, jj, m - jj, w, base, ipiv, info, growth, ws, st, ctas));
-    OZ_TRY(apply_list(a, lda, ws, 0, jj, jj + w, jb, st));
-    const int64_t rest = jb - (jj + w);
-    if (rest > 0) {
-      OZ_TRY(trsm_blocked(a, lda, jj, w, a + (jj + w) * lda + jj, lda, rest, st));
-      const int64_t below = m - jj - w;
-      if (below > 0) {
-        const int tag = prof_start(st);
-        OZ_TRY(dgemm(0, 0, below, rest, w, -1.0, a + jj * lda + jj + w, lda,
-                     a + (jj + w) * lda + jj, lda, 1.0, a + (jj + w) * lda + jj + w, lda, st));
-        prof_stop(tag, st, PROF_DGEMM_PANEL, 2.0 * below * rest * w);
-      }
-    }
-  }
-  return OZ_OK;
+  return panel_rec(a, lda, m, jb, 0, jb, wmax, base, ipiv, info, growth, ws, st, ctas);
 }
 
 // The Schur update A22 (m x ncols) -= A21 (m x jb) @ U12 (jb x ncols) through
