@@ -114,6 +114,14 @@ __device__ __forceinline__ long long ld_relaxed(const long long* p) {
 __device__ __forceinline__ void st_release(long long* p, long long v) {
   asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 // candidate record: [0] |v| (double), [1] pos (low 32) | tag (high 32), [2] physical
 // row, [4..4+w) row values.  Data first, tag last (release store).
 
@@ -224,19 +232,18 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
         irec[1] = br >= 0 ? pos[br] : 0x7fffffff;
         irec[2] = br >= 0 ? row_lo + br : -1;
       }
-      __threadfence();
+      // the warp's record stores are ordered before lane 0's release-add by
+      // the warp barrier (one release instead of a GPU-scope fence per lane)
       __syncwarp();
-      if (lane == 0) atomicAdd(&p.bar->count, 1u);
+      if (lane == 0) red_release_add(&p.bar->count, 1u);
       if (p.dbg && lane == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 0, (unsigned long long)(_n - _tp)); _tp = _n; }
       // ---- wait for all CTAs (counter reaches G*(t+1)), reduce all records
       if (lane == 0) {
         const unsigned target = gridDim.x * (unsigned)(t + 1);
-        volatile unsigned* ctr = &p.bar->count;
-        while (*ctr < target) {
+        while (ld_acquire_u32(&p.bar->count) < target) {
         }
       }
       __syncwarp();
-      __threadfence();
       if (p.dbg && lane == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 1, (unsigned long long)(_n - _tp)); _tp = _n; }
       constexpr int PER = 5;  // up to 160 CTAs
       double av[PER];
@@ -397,6 +404,7 @@ __global__ void __launch_bounds__(256) compose_ipiv_kernel(const int32_t* __rest
                                                             int npiv, int64_t k1, int32_t* dst,
                                                             int32_t* src, int32_t* cnt) {
   __shared__ int32_t top[COMPOSE_MAX];
+  __shared__ int32_t slot[COMPOSE_MAX];  // per swap: index into top (< npiv) or hash slot
   __shared__ int32_t hkey[COMPOSE_HASH];
   __shared__ int32_t hval[COMPOSE_HASH];
   __shared__ int32_t npos;
@@ -404,40 +412,47 @@ __global__ void __launch_bounds__(256) compose_ipiv_kernel(const int32_t* __rest
   for (int i = threadIdx.x; i < COMPOSE_HASH; i += blockDim.x) hkey[i] = -1;
   if (threadIdx.x == 0) npos = 0;
   __syncthreads();
+  // 1. (parallel) give every displaced row below the diagonal block a table slot
+  for (int t = threadIdx.x; t < npiv; t += blockDim.x) {
+    const int p = (int)(ipiv[t] - k1);  // relative row, >= t
+    if (p < npiv) {
+      slot[t] = p;
+    } else {
+      unsigned h = ((unsigned)p * 2654435761u) & (COMPOSE_HASH - 1);
+      while (true) {
+        const int prev = atomicCAS(&hkey[h], -1, p);
+        if (prev == -1 || prev == p) break;
+        h = (h + 1) & (COMPOSE_HASH - 1);
+      }
+      hval[h] = p;  // identical value from every thread that maps p here
+      slot[t] = COMPOSE_MAX + (int)h;
+    }
+  }
+  __syncthreads();
+  // 2. (one thread) replay the swaps in order on the index map, no probing
   if (threadIdx.x == 0) {
     for (int t = 0; t < npiv; ++t) {
-      const int p = (int)(ipiv[t] - k1);  // relative row, >= t
-      if (p == t) continue;
-      if (p < npiv) {
-        const int v = top[t];
-        top[t] = top[p];
-        top[p] = v;
-      } else {
-        unsigned h = ((unsigned)p * 2654435761u) & (COMPOSE_HASH - 1);
-        while (hkey[h] != -1 && hkey[h] != p) h = (h + 1) & (COMPOSE_HASH - 1);
-        if (hkey[h] == -1) {
-          hkey[h] = p;
-          hval[h] = p;
-        }
-        const int v = top[t];
-        top[t] = hval[h];
-        hval[h] = v;
-      }
+      const int sl = slot[t];
+      if (sl == t) continue;
+      int* other = sl < COMPOSE_MAX ? &top[sl] : &hval[sl - COMPOSE_MAX];
+      const int v = top[t];
+      top[t] = *other;
+      *other = v;
     }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < npiv; i += blockDim.x) {
     if (top[i] != i) {
-      const int slot = atomicAdd(&npos, 1);
-      dst[slot] = (int32_t)(k1 + i);
-      src[slot] = (int32_t)(k1 + top[i]);
+      const int at = atomicAdd(&npos, 1);
+      dst[at] = (int32_t)(k1 + i);
+      src[at] = (int32_t)(k1 + top[i]);
     }
   }
   for (int i = threadIdx.x; i < COMPOSE_HASH; i += blockDim.x) {
     if (hkey[i] >= 0 && hval[i] != hkey[i]) {
-      const int slot = atomicAdd(&npos, 1);
-      dst[slot] = (int32_t)(k1 + hkey[i]);
-      src[slot] = (int32_t)(k1 + hval[i]);
+      const int at = atomicAdd(&npos, 1);
+      dst[at] = (int32_t)(k1 + hkey[i]);
+      src[at] = (int32_t)(k1 + hval[i]);
     }
   }
   __syncthreads();
