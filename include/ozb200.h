@@ -127,7 +127,9 @@ int oz_dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k, double alp
  * Blocked right-looking LU with partial pivoting (solve.py:66-140) on a
  * column-major n x n matrix, in place.  backend 0 = native FP64 Schur update
  * (cuBLAS DGEMM), 1 = Ozaki-INT8 emulated Schur update with the given pair
- * table.  ipiv (device int32[n]) receives LAPACK-style 0-based row
+ * table and per-vector exponents, 2 = the same with one exponent per operand
+ * (ScalingMode.GLOBAL, split.py:131-134); the step-level entries below take
+ * the same codes.  ipiv (device int32[n]) receives LAPACK-style 0-based row
  * interchanges; `stats` (device double[4]) receives {observed max, max|A|, -, -}
  * for the growth factor; `info` (device int32) = first zero-pivot column + 1 or 0.
  */

@@ -1019,9 +1019,11 @@ struct Schur {
 int schur_split(const Schur& s, const LuWs& ws, cudaStream_t st) {
   if (s.backend == 0 || s.m <= 0 || s.ncols <= 0) return OZ_OK;
   const int tag = prof_start(st);
-  OZ_TRY(split_launch(s.a21, s.m, s.jb, 1, s.lda21, OZ_ROW_SCALED, OZ_PER_VECTOR, s.k, s.q, ws.slA,
+  // backend 1: per-vector exponents, 2: one exponent per operand (GLOBAL, split.py:131-134)
+  const int mode = s.backend == 2 ? OZ_GLOBAL : OZ_PER_VECTOR;
+  OZ_TRY(split_launch(s.a21, s.m, s.jb, 1, s.lda21, OZ_ROW_SCALED, mode, s.k, s.q, ws.slA,
                       ws.ldK, s.m * ws.ldK, ws.expA, ws.split_aux, st));
-  OZ_TRY(split_launch(s.u12, s.jb, s.ncols, 1, s.ldu, OZ_COL_SCALED, OZ_PER_VECTOR, s.k, s.q,
+  OZ_TRY(split_launch(s.u12, s.jb, s.ncols, 1, s.ldu, OZ_COL_SCALED, mode, s.k, s.q,
                       ws.slB, ws.ldK, s.ncols * ws.ldK, ws.expB, ws.split_aux, st));
   prof_stop(tag, st, PROF_SPLIT, (double)(s.m + s.ncols) * s.jb * (8.0 + s.k));
   return OZ_OK;
@@ -1103,9 +1105,9 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
              (long long)n, (long long)nb);
   OZ_REQUIRE(nb <= SWAP_MAX / 2, OZ_UNSUPPORTED, "lu_block > %d not supported", SWAP_MAX / 2);
   OZ_REQUIRE(lda >= n, OZ_INVALID_PARAMS, "lda < n");
-  OZ_REQUIRE(backend == 0 || backend == 1, OZ_INVALID_PARAMS, "bad backend");
+  OZ_REQUIRE(backend >= 0 && backend <= 2, OZ_INVALID_PARAMS, "bad backend %d", backend);
   LuWs ws;
-  const size_t need = lu_ws_layout(n, nb, backend == 1 ? k : 0, (uint8_t*)workspace, &ws);
+  const size_t need = lu_ws_layout(n, nb, backend != 0 ? k : 0, (uint8_t*)workspace, &ws);
   OZ_REQUIRE(ws_bytes >= need, OZ_INVALID_PARAMS, "workspace too small (%zu < %zu)", ws_bytes,
              need);
   OZ_CHECK_CUDA(cudaMemsetAsync(ws.bar, 0, sizeof(GridBar), st));
@@ -1353,11 +1355,11 @@ extern "C" int oz_schur_update(int backend, int64_t m, int64_t ncols, int64_t jb
                                void* ws, size_t ws_bytes, int64_t ws_n, int64_t ws_nb,
                                void* stream) {
   using namespace oz;
-  OZ_REQUIRE(backend == 0 || backend == 1, OZ_INVALID_PARAMS, "bad backend");
+  OZ_REQUIRE(backend >= 0 && backend <= 2, OZ_INVALID_PARAMS, "bad backend %d", backend);
   OZ_REQUIRE(backend == 0 || (m <= ws_n && ncols <= ws_n && jb <= ws_nb), OZ_INVALID_PARAMS,
              "schur update larger than the workspace");
   LuWs w;
-  OZ_TRY(ws_view(ws, ws_bytes, ws_n, ws_nb, backend == 1 ? num_slices : 0, &w));
+  OZ_TRY(ws_view(ws, ws_bytes, ws_n, ws_nb, backend != 0 ? num_slices : 0, &w));
   return schur_update(backend, m, ncols, jb, a21, lda21, u12, ldu, a22, lda22, num_slices,
                       slice_bits, npairs, pair_a, pair_b, pair_shift, growth_bits, w,
                       as_stream(stream));
@@ -1418,7 +1420,7 @@ extern "C" int oz_schur_split(int backend, int64_t m, int64_t ncols, int64_t jb,
                               int num_slices, int slice_bits, void* ws, size_t ws_bytes,
                               int64_t ws_n, int64_t ws_nb, void* stream) {
   using namespace oz;
-  OZ_REQUIRE(backend == 0 || backend == 1, OZ_INVALID_PARAMS, "bad backend");
+  OZ_REQUIRE(backend >= 0 && backend <= 2, OZ_INVALID_PARAMS, "bad backend %d", backend);
   if (backend == 0) return OZ_OK;
   OZ_REQUIRE(m <= ws_n && ncols <= ws_n && jb <= ws_nb, OZ_INVALID_PARAMS,
              "schur update larger than the workspace");
@@ -1437,12 +1439,12 @@ extern "C" int oz_schur_cols(int backend, int64_t m, int64_t ncols, int64_t jb,
                              int64_t c0, int64_t c1, int max_ctas, void* ws, size_t ws_bytes,
                              int64_t ws_n, int64_t ws_nb, void* stream) {
   using namespace oz;
-  OZ_REQUIRE(backend == 0 || backend == 1, OZ_INVALID_PARAMS, "bad backend");
+  OZ_REQUIRE(backend >= 0 && backend <= 2, OZ_INVALID_PARAMS, "bad backend %d", backend);
   OZ_REQUIRE(0 <= c0 && c0 <= c1 && c1 <= ncols, OZ_INVALID_PARAMS, "bad column range");
   OZ_REQUIRE(backend == 0 || (m <= ws_n && ncols <= ws_n && jb <= ws_nb), OZ_INVALID_PARAMS,
              "schur update larger than the workspace");
   LuWs w;
-  OZ_TRY(ws_view(ws, ws_bytes, ws_n, ws_nb, backend == 1 ? num_slices : 0, &w));
+  OZ_TRY(ws_view(ws, ws_bytes, ws_n, ws_nb, backend != 0 ? num_slices : 0, &w));
   const Schur s{backend, m, ncols, jb, a21, lda21, u12, ldu, a22, lda22, num_slices, slice_bits,
                 npairs, pair_a, pair_b, pair_shift, growth_bits};
   return schur_cols(s, c0, c1, w, as_stream(stream), max_ctas);

@@ -148,6 +148,8 @@ class DeviceOps:
         self.ncl = local_ncols(n, nb, Q, q)
         self.backend = backend
         self.emulated = backend.kind is BackendKind.EMULATED_INT8
+        from .solve import _backend_code
+        self.code = _backend_code(backend)
         if self.emulated:
             if backend.slice_bits > 7:
                 from .errors import DeviceError
@@ -248,7 +250,7 @@ class DeviceOps:
         _lib.call("oz_max_abs_bits", u12, jb, nt, 1, self.n, 0, self.bits.data_ptr(),
                   self._st())
         if m - jb > 0:
-            _lib.call("oz_schur_split", 1 if self.emulated else 0, m - jb, nt, jb, pb + 8 * jb, m,
+            _lib.call("oz_schur_split", self.code, m - jb, nt, jb, pb + 8 * jb, m,
                       u12, self.n, self.k, self.qbits, self.ws.data_ptr(), self.wsb, self.n,
                       self.nb, self._st())
 
@@ -259,7 +261,7 @@ class DeviceOps:
         if m - jb <= 0 or c1 <= c0:
             return
         max_ctas = self.sms - reserve_sms if reserve_sms > 0 else 0
-        _lib.call("oz_schur_cols", 1 if self.emulated else 0, m - jb, nt, jb,
+        _lib.call("oz_schur_cols", self.code, m - jb, nt, jb,
                   self.pbuf[slot].data_ptr() + 8 * jb, m, self._a(lstart, j), self.n,
                   self._a(lstart, j + jb), self.n, self.k, self.qbits, len(self.pa),
                   self.pa.ctypes.data, self.pb.ctypes.data, self.ps.ctypes.data,

@@ -160,6 +160,15 @@ def _count_flops(counter: FlopCounter, n: int, nb: int, backend: GemmBackend) ->
                 counter.add_f64(npairs * rest * rest + 2 * k * (rest * jb + jb * rest))
 
 
+def _backend_code(backend: GemmBackend) -> int:
+    """C-ABI Schur backend: 0 native, 1 emulated per-vector, 2 emulated GLOBAL
+    scaling (split.py:131-134)."""
+    if backend.kind is not BackendKind.EMULATED_INT8:
+        return 0
+    from .split import ScalingMode
+    return 2 if backend.scaling is ScalingMode.GLOBAL else 1
+
+
 def factor_device(a_cm, nb: int, backend: GemmBackend):
     """In-place LU of a column-major CUDA matrix.  Returns (ipiv tensor,
     stats tensor, info tensor) without synchronizing."""
@@ -182,7 +191,7 @@ def factor_device(a_cm, nb: int, backend: GemmBackend):
     ipiv = t.empty((n,), dtype=t.int32, device="cuda")
     stats = t.zeros((4,), dtype=t.float64, device="cuda")
     info = t.zeros((1,), dtype=t.int32, device="cuda")
-    _lib.call("oz_lu_factor", a_cm.data_ptr(), n, int(a_cm.stride(1)), nb, 1 if emulated else 0,
+    _lib.call("oz_lu_factor", a_cm.data_ptr(), n, int(a_cm.stride(1)), nb, _backend_code(backend),
               k, backend.slice_bits, len(pa), pa.ctypes.data, pb.ctypes.data, sh.ctypes.data,
               ipiv.data_ptr(), stats.data_ptr(), info.data_ptr(), ws.data_ptr(), ws_bytes,
               _dev.stream())

@@ -169,3 +169,23 @@ def test_uniform_2048_nb256_verdicts():
         res[name] = oz.solve_system(a, b, 256, bk)[1].scaled_residual
     assert res["fp64"] < 1.0 and res["k7"] < 16.0 and res["k6"] >= 16.0, res
     assert 0.5 <= res["k6"] / 65.12 <= 2.0 and 0.5 <= res["k7"] / 0.5967 <= 2.0, res
+
+
+@pytest.mark.parametrize("k", [5, 7])
+def test_emulated_lu_global_scaling_matches_oracle(k):
+    """Schur updates with ScalingMode.GLOBAL (one exponent per operand,
+    split.py:131-134): identical pivots and factors close to the oracle LU
+    run with mode=GLOBAL (the emulated products are bit-exact; the FP64
+    panel/trsm parts are pinned to tolerance, test_solve.py:61-66)."""
+    oz = _oz()
+    from oracle import ozaki_oracle as orc
+    from paper_2509_23565_b200.split import ScalingMode
+    a = np.random.default_rng(3).random((300, 300)) - 0.5
+    bk = oz.GemmBackend.int8(k, scaling=ScalingMode.GLOBAL)
+    f = oz.lu_factor(a, 64, bk)
+    lu_ref, perm_ref, _ = orc.lu_factor(a, 64, k, mode=orc.GLOBAL)
+    assert np.array_equal(f.pivots, perm_ref)
+    assert np.abs(f.lu - lu_ref).max() <= 2.0**-30
+    # and it differs from per-vector scaling (the mode really reaches the kernel)
+    g = oz.lu_factor(a, 64, oz.GemmBackend.int8(k))
+    assert not np.array_equal(f.lu, g.lu)
