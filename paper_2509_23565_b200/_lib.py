@@ -14,7 +14,8 @@ import threading
 from .errors import STATUS_TO_ERROR, DeviceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libozb200.so")
+# OZ_LIB_PATH selects an alternative in-tree build (A/B tuning of kernel variants)
+LIB_PATH = os.environ.get("OZ_LIB_PATH") or os.path.join(_HERE, "libozb200.so")
 
 _i64 = C.c_int64
 _i32 = C.c_int32

@@ -184,11 +184,16 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   return d;
 }
 
-// exact int32 -> double on the FP64 pipe (magic-number trick)
+// exact int32 -> double: the magic-number trick (one DADD on the FP64 pipe)
+// or the I2F.F64 conversion (OZ_CVT=1 build), chosen by measurement
+#ifdef OZ_CVT_I2F
+__device__ __forceinline__ double i32_to_f64(uint32_t v) { return __int2double_rn((int)v); }
+#else
 __device__ __forceinline__ double i32_to_f64(uint32_t v) {
   const double d = __hiloint2double(0x43300000, (int)(v ^ 0x80000000u));
   return __dsub_rn(d, 4503601774854144.0);  // 2^52 + 2^31
 }
+#endif
 
 __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mt, int& nt) {
   const int per_group = p.group_m * p.num_n_tiles;

@@ -59,25 +59,6 @@ struct GridBar {
   unsigned gen;
 };
 
-__device__ __forceinline__ void grid_sync(GridBar* bar, unsigned nblocks) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned* vgen = &bar->gen;
-    const unsigned g = *vgen;
-    __threadfence();
-    if (atomicAdd(&bar->count, 1u) == nblocks - 1) {
-      atomicExch(&bar->count, 0u);
-      __threadfence();
-      atomicAdd(&bar->gen, 1u);
-    } else {
-      while (*vgen == g) {
-      }
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 // np.argmax(|col|) order: larger magnitude wins, ties -> smaller logical position;
 // NaN counts as the maximum (numpy returns the first NaN).
 __device__ __forceinline__ bool better(double a1, int p1, double a2, int p2) {
@@ -106,14 +87,6 @@ struct PanelArgs {
   unsigned long long* dbg;  // optional per-phase cycle counters (OZ_PANEL_TIMING)
 };
 
-__device__ __forceinline__ long long ld_relaxed(const long long* p) {
-  long long v;
-  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(long long* p, long long v) {
-  asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -633,7 +606,6 @@ __global__ void __launch_bounds__(TRSV_B * TRSV_G) trsv_syncfree_kernel(
     int* ticket, int32_t* zero_diag) {
   __shared__ int s_blk;
   __shared__ double s_acc[TRSV_G][TRSV_B];
-  __shared__ double s_x[TRSV_B];
   __shared__ double s_diag[TRSV_B][TRSV_B + 1];
   const int tid = threadIdx.x, r = tid % TRSV_B, grp = tid / TRSV_B;
   const int nblk = (int)((n + TRSV_B - 1) / TRSV_B);
