@@ -674,35 +674,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
       }
       if (kDebug || p.experiment >= 2) continue;
-      if (row < p.m) {
-        // final pass, FP_CHUNK columns per (rolled) iteration; the accumulator
-        // registers shift down by FP_CHUNK after each chunk so indices stay static
-        const int er = p.expA[row];
+      {
+        // every lane runs the loop (the exponent shuffles need the full warp);
+        // rows past m only skip their loads and stores
+        // final pass: out = alpha * ldexp(acc, er + eb) + beta * C, written
+        // once.  FP_CHUNK columns per (rolled) iteration with the accumulator
+        // registers shifted down so indices stay static; the column exponents
+        // come from two coalesced loads + a warp shuffle per column; the LU's
+        // alpha = -1, beta = 1 case is C - ab (bit-identical, one DADD).
+        const bool row_ok = row < p.m;
+        const int er = row_ok ? p.expA[row] : 0;
         const bool use_c = p.c_is_input && p.beta != 0.0;
+        const bool lu_form = use_c && p.alpha == -1.0 && p.beta == 1.0;
         const int ncols = min(64, p.n - col0);
         const int64_t ldc = p.ldc;
-        double* cbase = p.c + (int64_t)col0 * ldc + row;
-        const int32_t* ebase = p.expB + col0;
+        double* cp = p.c + (int64_t)col0 * ldc + row;
+        const int eb_lo = lane < ncols ? __ldg(p.expB + col0 + lane) : 0;
+        const int eb_hi = lane + 32 < ncols ? __ldg(p.expB + col0 + 32 + lane) : 0;
 #pragma unroll 1
         for (int c0 = 0; c0 < ncols; c0 += FP_CHUNK) {
-          int eb[FP_CHUNK];
           double cv[FP_CHUNK];
-          double* cp = cbase + (int64_t)c0 * ldc;
+          {
+            const double* cq = cp;
 #pragma unroll
-          for (int i = 0; i < FP_CHUNK; ++i) {
-            const bool ok = c0 + i < ncols;
-            eb[i] = ok ? __ldg(ebase + c0 + i) : 0;
-            cv[i] = (ok && use_c) ? cp[i * ldc] : 0.0;
+            for (int i = 0; i < FP_CHUNK; ++i) {
+              cv[i] = (use_c && row_ok && c0 + i < ncols) ? *cq : 0.0;
+              cq += ldc;
+            }
           }
 #pragma unroll
           for (int i = 0; i < FP_CHUNK; ++i) {
-            if (c0 + i < ncols) {
-              const double ab = ldexp_exact(acc[i], er + eb[i]);
-              double out = __dmul_rn(p.alpha, ab);
-              if (use_c) out = __dadd_rn(out, __dmul_rn(p.beta, cv[i]));
-              cp[i * ldc] = out;
+            const int c = c0 + i;
+            const int eb = __shfl_sync(0xffffffffu, c < 32 ? eb_lo : eb_hi, c & 31);
+            if (row_ok && c < ncols) {
+              const double ab = ldexp_exact(acc[i], er + eb);
+              double out;
+              if (lu_form) {
+                out = __dsub_rn(cv[i], ab);
+              } else {
+                out = __dmul_rn(p.alpha, ab);
+                if (use_c) out = __dadd_rn(out, __dmul_rn(p.beta, cv[i]));
+              }
+              *cp = out;
               gmax = fmax(gmax, fabs(out));
             }
+            cp += ldc;
           }
 #pragma unroll
           for (int i = 0; i < 64 - FP_CHUNK; ++i) acc[i] = acc[i + FP_CHUNK];
