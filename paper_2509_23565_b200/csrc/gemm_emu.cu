@@ -840,8 +840,11 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStr
   p.num_n_tiles = (int)ceil_div(p.n, P_BN);
   p.num_tiles = p.num_m_tiles * p.num_n_tiles;
   p.nkb = (int)ceil_div(p.inner, BK);
-  p.group_m = GROUP_M;
-  if (const char* g = getenv("OZ_GEMM_GROUPM")) p.group_m = atoi(g) > 0 ? atoi(g) : GROUP_M;
+  // raster band: long-K products (standalone DGEMM) keep only 2 m-tiles of A
+  // in flight so the concurrently streamed slices stay L2-resident; the LU's
+  // K = nb updates prefer wide bands (measured, scripts/sweep_groupm.sh)
+  p.group_m = p.inner >= 4096 ? 2 : GROUP_M;
+  if (const char* g = getenv("OZ_GEMM_GROUPM")) p.group_m = atoi(g) > 0 ? atoi(g) : p.group_m;
   if (const char* e = getenv("OZ_GEMM_EXPERIMENT")) p.experiment = atoi(e);
   int grid = sm_count() & ~1;
   if (const char* g = getenv("OZ_GEMM_GRID")) grid = atoi(g) > 0 ? (atoi(g) & ~1) : grid;
