@@ -61,7 +61,7 @@ def parse():
     p.add_argument("--nb", type=int, default=1024)
     p.add_argument("--k", type=int, default=7)
     p.add_argument("--cpu-n", type=int, default=1024)
-    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--skip-native", action="store_true")
     p.add_argument("--sweep-k", default="3,4,5,6,7,8,9",
                    help="splits for the GEMM (D3) and LU k-sweeps; empty string skips them")
@@ -472,23 +472,6 @@ def run_ours(args, rank, world):
     raw, na, nx, nbv = (float(v) for v in norms.cpu().numpy())
     resid = _report(raw, na, nx, nbv, n).scaled_residual
 
-    # ---- native FP64 comparator (cuBLAS DGEMM Schur update), one timed step
-    native = None
-    if not args.skip_native:
-        step(oz.GemmBackend.native())
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        xn, _ = step(oz.GemmBackend.native())
-        e1.record()
-        torch.cuda.synchronize()
-        _lib.call("oz_residual_norms", a0.data_ptr(), n, 1, n, xn.data_ptr(), b0.data_ptr(),
-                  norms.data_ptr(), _dev.stream())
-        raw, na, nx, nbv = (float(v) for v in norms.cpu().numpy())
-        tn = e0.elapsed_time(e1) / 1e3
-        native = {"value": flops(n) / tn / 1e12, "ms_per_step": tn * 1e3,
-                  "scaled_residual": _report(raw, na, nx, nbv, n).scaled_residual}
-
     # ---- e2e through the public API on pinned host buffers
     e2e = None
     if args.e2e_steps > 0:
@@ -513,6 +496,23 @@ def run_ours(args, rank, world):
                "ms_per_step": te * 1e3, "scaled_residual": rep.scaled_residual,
                "api": "paper_2509_23565_b200.solve_system(pinned host A, b)"}
         del a_host
+
+    # ---- native FP64 comparator (cuBLAS DGEMM Schur update), one timed step
+    native = None
+    if not args.skip_native:
+        step(oz.GemmBackend.native())
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        xn, _ = step(oz.GemmBackend.native())
+        e1.record()
+        torch.cuda.synchronize()
+        _lib.call("oz_residual_norms", a0.data_ptr(), n, 1, n, xn.data_ptr(), b0.data_ptr(),
+                  norms.data_ptr(), _dev.stream())
+        raw, na, nx, nbv = (float(v) for v in norms.cpu().numpy())
+        tn = e0.elapsed_time(e1) / 1e3
+        native = {"value": flops(n) / tn / 1e12, "ms_per_step": tn * 1e3,
+                  "scaled_residual": _report(raw, na, nx, nbv, n).scaled_residual}
 
     if rank != 0:
         return

@@ -53,7 +53,7 @@ def lu_probe(n, nb, backends):
 
 if __name__ == "__main__":
     what = sys.argv[1]
-    if what in ("gemm1", "lu1", "kern"):
+    if what in ("gemm1", "lu1", "kern", "e2e"):
         pass
     elif what == "gemm":
         gemm_probe(int(sys.argv[2]), [int(k) for k in sys.argv[3].split(",")])
@@ -112,3 +112,27 @@ if __name__ == "__main__" and sys.argv[1] == "kern":
         ops = 2.0 * npairs * m * n * K
         print(f"kern m={m} n={n} K={K} k={k}: gemm {g_ms:.3f} ms {ops/g_ms/1e9:.1f} TOPS int8 "
               f"({2.0*m*n*K/g_ms/1e9:.1f} TFLOP/s-eq), split {s_ms:.3f} ms", flush=True)
+
+
+if __name__ == "__main__" and sys.argv[1] == "e2e":
+    # e2e n nb: solve_system on pinned host buffers, with the H2D copy timed alone
+    n, nb = int(sys.argv[2]), int(sys.argv[3])
+    a0 = generate_device(0, n, seed=99)
+    a_host = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+    a_host.copy_(a0)
+    b_host = torch.empty((n,), dtype=torch.float64, pin_memory=True)
+    b_host.copy_(a0.sum(1))
+    del a0
+    torch.cuda.synchronize()
+    for rep in range(3):
+        t0 = time.perf_counter()
+        d = a_host.to("cuda", non_blocking=True)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        del d
+        xh, r = oz.solve_system(a_host, b_host, nb, oz.GemmBackend.int8(7))
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        print(f"e2e n={n}: H2D alone {1e3*(t1-t0):.1f} ms ({8*n*n/(t1-t0)/1e9:.1f} GB/s), "
+              f"solve_system {1e3*(t2-t1):.1f} ms (factor+solve {1e3*r.seconds:.1f} ms), "
+              f"resid {r.scaled_residual:.3g}", flush=True)
