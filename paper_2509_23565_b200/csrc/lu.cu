@@ -1032,18 +1032,39 @@ int schur_update(int backend, int64_t m, int64_t ncols, int64_t jb, const double
   return schur_cols(s, 0, ncols, ws, st);
 }
 
-// Look-ahead (depth 1): the next panel is factored on a side stream with
-// OZ_LOOKAHEAD_SMS CTAs (default 40; 0 disables) while the rest of the Schur
-// update runs on the remaining SMs.
+// Look-ahead (depth 1): the next panel is factored on a side stream with S
+// CTAs while the rest of the Schur update runs on the other SMs.
+// OZ_LOOKAHEAD_SMS: 0 disables, a positive value fixes S, unset (-1) sizes S
+// per step so the panel (latency floor ~3 us per column plus ~0.011 us per
+// row per CTA) and the GEMM (~2.3 POPS on the full chip) take equal time.
 int lookahead_sms() {
-  static int v = -1;
-  if (v < 0) {
+  static int v = -2;
+  if (v == -2) {
     const char* e = getenv("OZ_LOOKAHEAD_SMS");
-    v = e ? atoi(e) : 40;
-    if (v < 0) v = 0;
-    v &= ~1;
+    v = e ? atoi(e) : -1;
+    if (v < -1) v = -1;
+    if (v > 0) v &= ~1;
   }
   return v;
+}
+
+int lookahead_split(int setting, int64_t m, int64_t nb, int npairs, int sms) {
+  if (setting >= 0) return setting;
+  if (npairs <= 0) return 40;  // native DGEMM Schur update: fixed split (measured best)
+  const double ops = 2.0 * npairs * (double)m * (double)m * (double)nb;
+  const double rate = 2.3e15;  // emulated INT8 ops/s on the full chip
+  int best = 16;
+  double best_t = 1e30;
+  for (int s = 16; s <= sms / 2; s += 8) {
+    const double tp = nb * (3e-6 + 1.1e-8 * (double)m / s);
+    const double tg = ops / (rate * (double)(sms - s) / sms);
+    const double t = tp > tg ? tp : tg;
+    if (t < best_t) {
+      best_t = t;
+      best = s;
+    }
+  }
+  return best;
 }
 
 struct SideStream {
@@ -1088,9 +1109,9 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
   OZ_CHECK_CUDA(cudaMemsetAsync(info, 0, sizeof(int32_t), st));
   OZ_TRY(max_abs(a, n, n, 1, lda, 0, 0, ws.bits + 1, st));
 
-  const int la_sms = lookahead_sms();
+  const int la_setting = lookahead_sms();
   SideStream* side = nullptr;
-  if (la_sms > 0) OZ_TRY(side_stream(&side));
+  if (la_setting != 0) OZ_TRY(side_stream(&side));
   // panel 0; every later panel is factored at the end of the previous step
   OZ_TRY(panel_factor(a, lda, n, nb < n ? nb : n, 0, ipiv, info, ws.bits, ws, st));
   for (int64_t j = 0; j < n; j += nb) {
@@ -1112,6 +1133,8 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
       OZ_TRY(schur_cols(sc, 0, jb2, ws, st));
       double* p2 = a + (j + jb) * lda + (j + jb);
       if (side != nullptr && rest > jb2) {
+        const int la_sms = lookahead_split(la_setting, rest, jb, backend != 0 ? npairs : 0,
+                                           sm_count());
         OZ_CHECK_CUDA(cudaEventRecord(side->ready, st));
         OZ_CHECK_CUDA(cudaStreamWaitEvent(side->st, side->ready, 0));
         OZ_TRY(panel_factor(p2, lda, rest, jb2, j + jb, ipiv + j + jb, info, ws.bits, ws,
