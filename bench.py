@@ -149,8 +149,11 @@ def cpu_oracle_lu(n, nb, k, reps=1):
     """Time the CPU restatement of the reference (oracle) on a bounded sample."""
     import numpy as np
     from oracle import ozaki_oracle as orc
+    limiter = None
     try:
-        from threadpoolctl import threadpool_info
+        # torchrun sets OMP_NUM_THREADS=1; the CPU baseline uses every host core
+        from threadpoolctl import threadpool_info, threadpool_limits
+        limiter = threadpool_limits(limits=os.cpu_count() or 1)
         cores = max([int(i.get("num_threads", 1)) for i in threadpool_info()] or [1])
     except Exception:  # pragma: no cover
         cores = os.cpu_count() or 1
@@ -163,6 +166,8 @@ def cpu_oracle_lu(n, nb, k, reps=1):
         x = orc.lu_solve(lu, perm, b)
         times.append(time.perf_counter() - t0)
         resid = orc.residual(a, x, b)[0]
+    if limiter is not None:
+        limiter.restore_original_limits()
     return times, cores, resid
 
 
