@@ -217,7 +217,7 @@ def _time_device(fn, reps):
     return e0.elapsed_time(e1) / 1e3 / reps
 
 
-def gemm_sweep(n, ks, int8_peak, reps=2):
+def gemm_sweep(n, ks, int8_peak, reps=2, comm=None):
     """configs[2] (D3): standalone emulated DGEMM n^3, A = hpl_uniform(n,2),
     B = hpl_uniform(n,3) generated in HBM, C = A @ B (alpha=1, beta=0), for each
     k; the timed call is the full gemm() device path (split A, split B, fused
@@ -227,27 +227,37 @@ def gemm_sweep(n, ks, int8_peak, reps=2):
     from paper_2509_23565_b200 import _dev, _lib
     from paper_2509_23565_b200.gemm import emulated_into
     from paper_2509_23565_b200.matgen import generate_device
-    a = generate_device(0, n, seed=2)
+    from paper_2509_23565_b200.dist import row_shard
+    world = comm.size if comm is not None else 1
+    rank = comm.rank if comm is not None else 0
+    lo, hi = row_shard(n, world, rank)            # N > 1: rows of A and C, B replicated
+    mrows = hi - lo
+    a = generate_device(0, n, seed=2)[lo:hi]
     b = generate_device(0, n, seed=3)
-    out = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    out = torch.empty((mrows, n), dtype=torch.float64, device="cuda")
     fl = 2.0 * n ** 3
-    t = _time_device(lambda: _lib.call("oz_dgemm", 0, 0, n, n, n, 1.0, b.data_ptr(), n,
-                                       a.data_ptr(), n, 0.0, out.data_ptr(), n, _dev.stream()),
-                     reps)
+
+    def tmax(fn):
+        t = _time_device(fn, reps)
+        return comm.allreduce_values([t], "max")[0] if comm is not None else t
+
+    t = tmax(lambda: _lib.call("oz_dgemm", 0, 0, n, mrows, n, 1.0, b.data_ptr(), n,
+                               a.data_ptr(), n, 0.0, out.data_ptr(), n, _dev.stream()))
     res = {"workload": f"configs[2]: emulated DGEMM {n}^3, A=hpl_uniform({n},2), "
                        f"B=hpl_uniform({n},3), device-resident, split+GEMM timed",
+           "n_gpus": world, "sharding": "rows of A and C per rank, B replicated, no exchange",
            "native_fp64": {"ms": t * 1e3, "tflops": fl / t / 1e12,
-                           "frac_of_fp64_nominal": fl / t / 1e12 / FP64_NOMINAL_TFLOPS},
+                           "frac_of_fp64_nominal": fl / t / 1e12 / world / FP64_NOMINAL_TFLOPS},
            "emulated": []}
     for k in ks:
         bk = oz.GemmBackend.int8(k)
         npairs = k * (k + 1) // 2
-        t = _time_device(lambda: emulated_into(bk, a, b, 1.0, 0.0, out, False), reps)
-        int8 = npairs * fl / t / 1e12
+        t = tmax(lambda: emulated_into(bk, a, b, 1.0, 0.0, out, False))
+        int8 = npairs * fl / t / 1e12 / world       # per-GPU fraction of the roofline
         res["emulated"].append({"k": k, "pairs": npairs, "ms": t * 1e3,
                                 "tflops_fp64_equiv": fl / t / 1e12,
-                                "int8_tops": int8, "frac_of_int8_peak": int8 / int8_peak,
-                                "fp64_equiv_roofline_tflops": int8_peak / npairs})
+                                "int8_tops_per_gpu": int8, "frac_of_int8_peak": int8 / int8_peak,
+                                "fp64_equiv_roofline_tflops": world * int8_peak / npairs})
     del a, b, out
     torch.cuda.empty_cache()
     return res
@@ -369,10 +379,15 @@ def run_distributed(args, rank, world):
         native = {"value": flops(n) / tn / 1e12, "ms_per_step": tn * 1e3,
                   "scaled_residual": nprob.verify(xn).scaled_residual}
         del nprob
-    if rank != 0:
-        return
     peaks, peak_kind = load_peaks()
     peak = 2.0 * float(peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"])
+    growth = prob.growth
+    del prob
+    torch.cuda.empty_cache()
+    ks = [int(v) for v in args.sweep_k.split(",") if v.strip()]
+    gsweep = gemm_sweep(args.gemm_n, ks, peak, comm=comm) if ks else None
+    if rank != 0:
+        return
     gemm_ms, gemm_ops = prof[0], prof[2]
     achieved = gemm_ops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     kinds = ["emu_gemm", "panel", "schur_dgemm", "split", "laswp", "trsm", "solve", "other",
@@ -405,8 +420,9 @@ def run_distributed(args, rank, world):
                          "sample": f"oracle LU factor+solve U(-1/2,1/2) n={args.cpu_n} on host "
                                    f"cores (residual {cpu_resid:.4g})"},
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
-        "scaled_residual": rep.scaled_residual, "passed": rep.passed, "growth": prob.growth,
+        "scaled_residual": rep.scaled_residual, "passed": rep.passed, "growth": growth,
         "native_fp64": native, "breakdown_rank0": breakdown,
+        "gemm_k_sweep": gsweep,
     }), flush=True)
 
 
