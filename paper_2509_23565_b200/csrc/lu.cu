@@ -1067,6 +1067,19 @@ int lookahead_split(int setting, int64_t m, int64_t nb, int npairs, int sms) {
   return best;
 }
 
+// OZ_LU_TRACE=1: per-step event timeline of the driver on stderr (tuning only)
+struct LuTrace {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;
+  void mark(cudaStream_t st) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.push_back(e);
+  }
+};
+
 struct SideStream {
   cudaStream_t st = nullptr;
   cudaEvent_t ready = nullptr, done = nullptr;
@@ -1114,23 +1127,30 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
   if (la_setting != 0) OZ_TRY(side_stream(&side));
   // panel 0; every later panel is factored at the end of the previous step
   OZ_TRY(panel_factor(a, lda, n, nb < n ? nb : n, 0, ipiv, info, ws.bits, ws, st));
+  LuTrace tr;
+  tr.on = getenv("OZ_LU_TRACE") != nullptr;
   for (int64_t j = 0; j < n; j += nb) {
     const int64_t jb = nb < n - j ? nb : n - j;
+    tr.mark(st);  // 0 step start
     // ---- the panel's interchanges on every other column: whole-row swaps
     //      (solve.py:80-82)
     OZ_TRY(laswp_ipiv(a, lda, 0, j, j + jb, n, j, ipiv + j, (int)jb, ws, st));
+    tr.mark(st);  // 1 after laswp
     const int64_t rest = n - j - jb;
     if (rest > 0) {
       double* a12 = a + (j + jb) * lda + j;
       double* a21 = a + j * lda + (j + jb);
       double* a22 = a + (j + jb) * lda + (j + jb);
       OZ_TRY(trsm_blocked(a, lda, j, jb, a12, lda, rest, st));  // solve.py:123-127
+      tr.mark(st);  // 2 after trsm
       const Schur sc{backend, rest, rest, jb, a21, lda, a12, lda, a22, lda, k, q, npairs, pa, pb,
                      ps, ws.bits};
       OZ_TRY(schur_split(sc, ws, st));                         // solve.py:130-134
+      tr.mark(st);  // 3 after split
       // the next panel's columns first, then its factorization (look-ahead)
       const int64_t jb2 = nb < rest ? nb : rest;
       OZ_TRY(schur_cols(sc, 0, jb2, ws, st));
+      tr.mark(st);  // 4 after GEMM on the next panel's columns
       double* p2 = a + (j + jb) * lda + (j + jb);
       if (side != nullptr && rest > jb2) {
         const int la_sms = lookahead_split(la_setting, rest, jb, backend != 0 ? npairs : 0,
@@ -1140,7 +1160,9 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
         OZ_TRY(panel_factor(p2, lda, rest, jb2, j + jb, ipiv + j + jb, info, ws.bits, ws,
                             side->st, la_sms));
         OZ_CHECK_CUDA(cudaEventRecord(side->done, side->st));
+        tr.mark(side->st);  // 5 side stream: panel done
         OZ_TRY(schur_cols(sc, jb2, rest, ws, st, sm_count() - la_sms));
+        tr.mark(st);  // 6 after the rest of the GEMM
         OZ_CHECK_CUDA(cudaStreamWaitEvent(st, side->done, 0));
       } else {
         OZ_TRY(schur_cols(sc, jb2, rest, ws, st));
@@ -1149,6 +1171,20 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
     }
     // finalized U rows of this panel: triu(lu[j:j+jb, j:]) (solve.py:135-137)
     OZ_TRY(max_abs(a + j * lda + j, jb, n - j, 1, lda, 1, 0, ws.bits, st));
+  }
+  if (tr.on) {
+    cudaStreamSynchronize(st);
+    // 7 marks per full step: start, laswp, trsm, split, gemm_a, side_done, gemm_b
+    fprintf(stderr, "step    m  laswp  trsm  split gemm_a  panel(side) gemm_b  total [ms]\n");
+    for (size_t i = 0; i + 7 <= tr.ev.size(); i += 7) {
+      float t[7];
+      for (int q2 = 1; q2 < 7; ++q2) cudaEventElapsedTime(&t[q2], tr.ev[i], tr.ev[i + q2]);
+      const float total = i + 7 < tr.ev.size() ? [&] { float x; cudaEventElapsedTime(&x, tr.ev[i], tr.ev[i + 7]); return x; }() : t[6];
+      fprintf(stderr, "%4zu %6lld %6.2f %5.2f %6.2f %6.2f %11.2f %6.2f %6.2f\n", i / 7,
+              (long long)(n - (int64_t)(i / 7) * nb - nb), t[1], t[2] - t[1], t[3] - t[2],
+              t[4] - t[3], t[5] - t[4], t[6] - t[4], total);
+    }
+    for (auto e : tr.ev) cudaEventDestroy(e);
   }
   if (unsigned long long* dbg = panel_dbg()) {
     // debug: per-phase cycles of the panel steps, summed over all CTAs
