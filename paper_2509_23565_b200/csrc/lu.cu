@@ -988,17 +988,30 @@ struct Schur {
   unsigned long long* growth;
 };
 
-int schur_split(const Schur& s, const LuWs& ws, cudaStream_t st) {
+// Split A21 (row-scaled) and the U12 columns [c0, c1) (column-scaled) into the
+// slice stacks; a column range of U12 can be split on its own for per-vector
+// scaling (each column has its own exponent), not for GLOBAL (one exponent
+// over all of U12).
+int schur_split_part(const Schur& s, bool with_a, int64_t c0, int64_t c1, const LuWs& ws,
+                     cudaStream_t st) {
   if (s.backend == 0 || s.m <= 0 || s.ncols <= 0) return OZ_OK;
   const int tag = prof_start(st);
   // backend 1: per-vector exponents, 2: one exponent per operand (GLOBAL, split.py:131-134)
   const int mode = s.backend == 2 ? OZ_GLOBAL : OZ_PER_VECTOR;
-  OZ_TRY(split_launch(s.a21, s.m, s.jb, 1, s.lda21, OZ_ROW_SCALED, mode, s.k, s.q, ws.slA,
-                      ws.ldK, s.m * ws.ldK, ws.expA, ws.split_aux, st));
-  OZ_TRY(split_launch(s.u12, s.jb, s.ncols, 1, s.ldu, OZ_COL_SCALED, mode, s.k, s.q,
-                      ws.slB, ws.ldK, s.ncols * ws.ldK, ws.expB, ws.split_aux, st));
-  prof_stop(tag, st, PROF_SPLIT, (double)(s.m + s.ncols) * s.jb * (8.0 + s.k));
+  if (with_a)
+    OZ_TRY(split_launch(s.a21, s.m, s.jb, 1, s.lda21, OZ_ROW_SCALED, mode, s.k, s.q, ws.slA,
+                        ws.ldK, s.m * ws.ldK, ws.expA, ws.split_aux, st));
+  if (c1 > c0)
+    OZ_TRY(split_launch(s.u12 + c0 * s.ldu, s.jb, c1 - c0, 1, s.ldu, OZ_COL_SCALED, mode, s.k,
+                        s.q, ws.slB + c0 * ws.ldK, ws.ldK, s.ncols * ws.ldK, ws.expB + c0,
+                        ws.split_aux, st));
+  prof_stop(tag, st, PROF_SPLIT,
+            (double)((with_a ? s.m : 0) + (c1 - c0)) * s.jb * (8.0 + s.k));
   return OZ_OK;
+}
+
+int schur_split(const Schur& s, const LuWs& ws, cudaStream_t st) {
+  return schur_split_part(s, true, 0, s.ncols, ws, st);
 }
 
 int schur_cols(const Schur& s, int64_t c0, int64_t c1, const LuWs& ws, cudaStream_t st,
@@ -1131,28 +1144,36 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
   tr.on = getenv("OZ_LU_TRACE") != nullptr;
   for (int64_t j = 0; j < n; j += nb) {
     const int64_t jb = nb < n - j ? nb : n - j;
-    tr.mark(st);  // 0 step start
-    // ---- the panel's interchanges on every other column: whole-row swaps
-    //      (solve.py:80-82)
-    OZ_TRY(laswp_ipiv(a, lda, 0, j, j + jb, n, j, ipiv + j, (int)jb, ws, st));
-    tr.mark(st);  // 1 after laswp
     const int64_t rest = n - j - jb;
+    const int64_t jb2 = nb < rest ? nb : rest;  // the next panel's width
+    double* a12 = a + (j + jb) * lda + j;
+    double* a21 = a + j * lda + (j + jb);
+    double* a22 = a + (j + jb) * lda + (j + jb);
+    const Schur sc{backend, rest, rest, jb, a21, lda, a12, lda, a22, lda, k, q, npairs, pa, pb,
+                   ps, ws.bits};
+    // Look-ahead with the next panel's columns on the critical path only:
+    // swaps, trsm, split and Schur update of those jb2 columns, then the next
+    // panel on the side stream while the rest of this step (swaps of the other
+    // columns, trsm, split and update of the remaining columns) runs beside it.
+    // GLOBAL scaling needs all of U12 for its one exponent: no column split.
+    const bool la = side != nullptr && rest > jb2 && backend != 2;
+    tr.mark(st);  // 0 step start
+    // ---- the panel's interchanges: whole-row swaps (solve.py:80-82)
+    if (la)
+      OZ_TRY(laswp_ipiv(a, lda, j + jb, j + jb + jb2, 0, 0, j, ipiv + j, (int)jb, ws, st));
+    else
+      OZ_TRY(laswp_ipiv(a, lda, 0, j, j + jb, n, j, ipiv + j, (int)jb, ws, st));
+    tr.mark(st);  // 1 after laswp
     if (rest > 0) {
-      double* a12 = a + (j + jb) * lda + j;
-      double* a21 = a + j * lda + (j + jb);
-      double* a22 = a + (j + jb) * lda + (j + jb);
-      OZ_TRY(trsm_blocked(a, lda, j, jb, a12, lda, rest, st));  // solve.py:123-127
+      // trsm U12 = L11^-1 A12 (solve.py:123-127), split, Schur update (:130-134)
+      OZ_TRY(trsm_blocked(a, lda, j, jb, a12, lda, la ? jb2 : rest, st));
       tr.mark(st);  // 2 after trsm
-      const Schur sc{backend, rest, rest, jb, a21, lda, a12, lda, a22, lda, k, q, npairs, pa, pb,
-                     ps, ws.bits};
-      OZ_TRY(schur_split(sc, ws, st));                         // solve.py:130-134
+      OZ_TRY(schur_split_part(sc, true, 0, la ? jb2 : rest, ws, st));
       tr.mark(st);  // 3 after split
-      // the next panel's columns first, then its factorization (look-ahead)
-      const int64_t jb2 = nb < rest ? nb : rest;
       OZ_TRY(schur_cols(sc, 0, jb2, ws, st));
-      tr.mark(st);  // 4 after GEMM on the next panel's columns
+      tr.mark(st);  // 4 after the update of the next panel's columns
       double* p2 = a + (j + jb) * lda + (j + jb);
-      if (side != nullptr && rest > jb2) {
+      if (la) {
         const int la_sms = lookahead_split(la_setting, rest, jb, backend != 0 ? npairs : 0,
                                            sm_count());
         OZ_CHECK_CUDA(cudaEventRecord(side->ready, st));
@@ -1161,12 +1182,17 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
                             side->st, la_sms));
         OZ_CHECK_CUDA(cudaEventRecord(side->done, side->st));
         tr.mark(side->st);  // 5 side stream: panel done
+        OZ_TRY(laswp_ipiv(a, lda, 0, j, j + jb + jb2, n, j, ipiv + j, (int)jb, ws, st));
+        OZ_TRY(trsm_blocked(a, lda, j, jb, a12 + jb2 * lda, lda, rest - jb2, st));
+        OZ_TRY(schur_split_part(sc, false, jb2, rest, ws, st));
         OZ_TRY(schur_cols(sc, jb2, rest, ws, st, sm_count() - la_sms));
-        tr.mark(st);  // 6 after the rest of the GEMM
+        tr.mark(st);  // 6 after the rest of the step
         OZ_CHECK_CUDA(cudaStreamWaitEvent(st, side->done, 0));
       } else {
         OZ_TRY(schur_cols(sc, jb2, rest, ws, st));
+        tr.mark(st);  // 5 (no look-ahead): after the rest of the update
         OZ_TRY(panel_factor(p2, lda, rest, jb2, j + jb, ipiv + j + jb, info, ws.bits, ws, st));
+        tr.mark(st);  // 6 (no look-ahead): after the next panel
       }
     }
     // finalized U rows of this panel: triu(lu[j:j+jb, j:]) (solve.py:135-137)
