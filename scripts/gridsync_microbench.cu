@@ -31,6 +31,7 @@ __global__ void k(unsigned* ctr, double* rec, int steps, double* out) {
         red_release_add(ctr, 1u);
         const unsigned target = gridDim.x * (unsigned)(t + 1);
         while (ld_acquire(ctr) < target) {
+          if (MODE >= 10) __nanosleep(MODE == 10 ? 32 : 128);
         }
       }
       __syncwarp();
@@ -40,7 +41,8 @@ __global__ void k(unsigned* ctr, double* rec, int steps, double* out) {
         for (int i = 0; i < 5; ++i) {
           const int g = lane + 32 * i;
           if (g < (int)gridDim.x) {
-            const double v = MODE == 8 ? rec[((size_t)(t & 1) * gridDim.x + g) * 68]  // weak ld (L1 path)
+            const double v = MODE >= 10 ? __ldcg(rec + ((size_t)(t & 1) * gridDim.x + g) * 68)
+                           : MODE == 8 ? rec[((size_t)(t & 1) * gridDim.x + g) * 68]  // weak ld (L1 path)
                            : MODE == 9 ? *(volatile double*)&rec[((size_t)(t & 1) * gridDim.x + g) * 68]
                            : MODE == 6 ? __ldcg(rec + 2 * 160 * 68 + 2 * 160 * 2 + g * 16)  // never written
                            : MODE == 7 ? __ldcg(rec + ((size_t)(t & 1) * gridDim.x + blockIdx.x) * 68 + i)  // own record
@@ -70,7 +72,7 @@ int main() {
   cudaMemset(rec, 0, 2 * 160 * 68 * 8 + 2 * 160 * 16 + 160 * 16 * 8);
   cudaMalloc(&out, 8);
   const int steps = 2000;
-  for (int mode : {0, 2, 8, 9})
+  for (int mode : {0, 2, 10, 11})
     for (int G : {8, 32, 64, 128, 148}) {
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0);
@@ -78,7 +80,7 @@ int main() {
       for (int rep = 0; rep < 2; ++rep) {
         cudaMemset(ctr, 0, 4);
         void* args[] = {&ctr, &rec, (void*)&steps, &out};
-        void* fn = mode == 0 ? (void*)k<0> : mode == 2 ? (void*)k<2> : mode == 8 ? (void*)k<8> : (void*)k<9>;
+        void* fn = mode == 0 ? (void*)k<0> : mode == 2 ? (void*)k<2> : mode == 10 ? (void*)k<10> : (void*)k<11>;
         cudaEventRecord(e0);
         cudaLaunchCooperativeKernel(fn, dim3(G), dim3(256), args, 0, 0);
         cudaEventRecord(e1);
@@ -87,7 +89,7 @@ int main() {
       float ms;
       cudaEventElapsedTime(&ms, e0, e1);
       printf("mode=%d (%s) G=%3d: %.2f us per step\n", mode,
-             mode == 0 ? "counter only" : mode == 2 ? "ld.cg headers" : mode == 8 ? "weak ld headers" : "volatile ld headers",
+             mode == 0 ? "counter only" : mode == 2 ? "ld.cg headers" : mode == 10 ? "headers, 32ns backoff" : "headers, 128ns backoff",
              G, ms * 1e3 / steps);
     }
   return 0;
