@@ -10,16 +10,19 @@
 // applied once at the end (exact power-of-two scaling) — bit-identical to the
 // reference whenever no intermediate over/underflows.
 //
-// Kernel design (sm_100a):
-//   * persistent CTAs (one per SM), grouped raster over 128x128 output tiles;
-//   * loop order tile -> pair -> K: one INT32 product per pair lands in a TMEM
-//     accumulator (tcgen05.mma.cta_group::1.kind::i8, M=128, N=128, K=32),
-//     double-buffered so the epilogue of pair p overlaps the MMAs of pair p+1;
+// Kernel design (sm_100a), emu_gemm_pair_kernel:
+//   * CTA pairs (__cluster_dims__(2), tcgen05.mma.cta_group::2.kind::i8,
+//     M=256, N=128, K=32): each CTA stages its own 128 rows of A and half of
+//     B, so B is shared across the pair; one persistent pair per two SMs walks
+//     a grouped raster of 256x128 output tiles;
+//   * loop order tile -> exact-level group -> pair -> K; each group's INT32
+//     sum lands in one of 4 TMEM accumulators (128 columns each), so the
+//     epilogue of one group overlaps the MMAs of the next;
 //   * operands are K-major int8 slice tiles (128 rows x 128 bytes) staged by
-//     TMA (cp.async.bulk.tensor.3d, 128B swizzle) through a 6-stage mbarrier ring;
-//   * warp roles: w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
-//     w4..w11 epilogue (each owns 32 TMEM lanes x 64 columns and keeps its
-//     64 FP64 accumulators in registers for the whole pair loop);
+//     TMA (cp.async.bulk.tensor.3d, 128B swizzle) through an 8-stage ring;
+//   * warp roles: w8 TMA producer, w9 MMA issuer (leader CTA), w10 TMEM
+//     allocator, w0..w7 epilogue (each owns 32 TMEM lanes x 64 columns and
+//     keeps its 64 FP64 accumulators in registers for the whole pair loop);
 //   * the FP64 recombine, alpha/beta epilogue (C read once, written once) and
 //     the optional growth max (solve.py:135) are fused in the epilogue.
 #include <cuda.h>
@@ -32,24 +35,15 @@
 namespace oz {
 namespace emu {
 
-constexpr int BM = 128;
-constexpr int BN = 128;
-constexpr int BK = 128;  // bytes of K per stage (one 128B swizzle atom)
-constexpr int STAGES = 6;
-constexpr int SGROUP = 3;  // stages released per tcgen05.commit (>= 12 MMAs per commit)
+constexpr int BM = 128;   // rows of A per CTA (TMA box)
+constexpr int BK = 128;   // bytes of K per stage (one 128B swizzle atom)
 constexpr int NUM_ACC = 4;
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_THREADS = 384;
-constexpr int EPI_WARP0 = 4;
+constexpr int EPI_WARPS = 8;
 constexpr int MAX_PAIRS = 256;
-constexpr int TILE_BYTES = BM * BK;  // == BN * BK
-constexpr int STAGE_BYTES = 2 * TILE_BYTES;
 constexpr int GROUP_M = 16;
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + 256;
 
-// instruction descriptor: D=S32, A=B=signed int8, both K-major, M=128, N=128
-constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
 
 struct Params {
   int m, n, inner;
@@ -94,42 +88,11 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
-                                            int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
-      : "memory");
-}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   bar)
-               : "memory");
-}
-__device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                          uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-        "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
   asm volatile(
@@ -156,24 +119,6 @@ __device__ __forceinline__ bool elect_one() {
       : "=r"(pred));
   return pred != 0;
 }
-__device__ __forceinline__ void tc_mma_i8_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                                uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void tc_commit_elect(uint32_t bar) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
-          bar)
-      : "memory");
-}
-
 // K-major, 128B-swizzled shared-memory matrix descriptor (8-row groups 1024B apart).
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
@@ -206,209 +151,6 @@ __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mt, int
   nt = r / gm;
 }
 
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    emu_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                    const __grid_constant__ CUtensorMap tmB, const __grid_constant__ Params p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint8_t* smA = smem;
-  uint8_t* smB = smem + STAGES * TILE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + STAGES;
-  uint64_t* tfull = bars + 2 * STAGES;
-  uint64_t* tempty = bars + 2 * STAGES + NUM_ACC;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 2 * NUM_ACC);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), 1);
-    }
-    for (int b = 0; b < NUM_ACC; ++b) {
-      mbar_init(smem_u32(&tfull[b]), 1);
-      mbar_init(smem_u32(&tempty[b]), (NUM_THREADS / 32 - EPI_WARP0));
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp < EPI_WARP0) {
-    // warpgroup 0 (producer / MMA / allocator) donates registers to the epilogue
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
-  }
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      int mt, nt;
-      tile_coords(p, t, mt, nt);
-      for (int q = 0; q < p.npairs; ++q) {
-        const int sa = p.pa[q], sb = p.pb[q];
-        for (int kb = 0; kb < p.nkb; ++kb) {
-          if (stage % SGROUP == 0) mbar_wait(smem_u32(&empty[stage / SGROUP]), phase ^ 1);
-          if (elect_one()) {
-            const uint32_t fb = smem_u32(&full[stage]);
-            mbar_expect_tx(fb, STAGE_BYTES);
-            tma_load_3d(smem_u32(smA + stage * TILE_BYTES), &tmA, fb, kb * BK, mt * BM, sa);
-            tma_load_3d(smem_u32(smB + stage * TILE_BYTES), &tmB, fb, kb * BK, nt * BN, sb);
-          }
-          __syncwarp();
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------- MMA issuer
-    const uint64_t adesc0 = sdesc(smem_u32(smA));
-    const uint64_t bdesc0 = sdesc(smem_u32(smB));
-    int stage = 0;
-    uint32_t phase = 0;
-    uint32_t it = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      for (int g = 0; g < p.ngroups; ++g, ++it) {
-        const uint32_t buf = it % NUM_ACC, aph = (it / NUM_ACC) & 1;
-        mbar_wait(smem_u32(&tempty[buf]), aph ^ 1);
-        tc_fence_after();
-        const uint32_t dtmem = tmem_base + buf * BN;
-        // every pair of an exact group accumulates into the same INT32 tile
-        for (int q = p.gstart[g]; q < p.gstart[g + 1]; ++q) {
-          const bool first_pair = q == p.gstart[g];
-          for (int kb = 0; kb < p.nkb; ++kb) {
-            mbar_wait(smem_u32(&full[stage]), phase);
-            tc_fence_after();
-            const uint64_t soff = (uint64_t)((stage * TILE_BYTES) >> 4);
-#pragma unroll
-            for (int kk = 0; kk < BK / 32; ++kk) {
-              tc_mma_i8_elect(dtmem, adesc0 + soff + 2 * kk, bdesc0 + soff + 2 * kk, IDESC,
-                              (first_pair && (kb | kk) == 0) ? 0u : 1u);
-            }
-            if (stage % SGROUP == SGROUP - 1) tc_commit_elect(smem_u32(&empty[stage / SGROUP]));
-            __syncwarp();
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
-          }
-        }
-        tc_commit_elect(smem_u32(&tfull[buf]));
-        __syncwarp();
-      }
-    }
-  } else if (warp >= EPI_WARP0) {
-    // --------------------------------------------------------------- epilogue
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
-    const int ew = warp - EPI_WARP0;  // 0..7
-    const int quad = warp & 3;        // TMEM lane quadrant this warp may access
-    const int half = ew >> 2;         // column half (0: cols 0-63, 1: 64-127)
-    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-    double gmax = 0.0;
-    uint32_t it = 0;
-    const bool debug = p.debug_out != nullptr;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      int mt, nt;
-      tile_coords(p, t, mt, nt);
-      double acc[64];
-#pragma unroll
-      for (int i = 0; i < 64; ++i) acc[i] = 0.0;
-      const int row = mt * BM + quad * 32 + lane;
-      const int col0 = nt * BN + half * 64;
-      for (int q = 0; q < p.ngroups; ++q, ++it) {
-        const uint32_t buf = it % NUM_ACC, aph = (it / NUM_ACC) & 1;
-        mbar_wait(smem_u32(&tfull[buf]), aph);
-        tc_fence_after();
-        const double s = pow2(-(int)p.gshift[q]);
-        const uint32_t taddr = tmem_base + lane_base + buf * BN + half * 64;
-#pragma unroll
-        for (int c = 0; c < 64; c += 16) {
-          uint32_t v[16];
-          tmem_ld16(taddr + c, v);
-          tmem_wait_ld();
-          if (debug) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int col = col0 + c + i;
-              if (row < p.m && col < p.n) p.debug_out[(int64_t)col * p.ldo + row] = (int32_t)v[i];
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) acc[c + i] = fma(i32_to_f64(v[i]), s, acc[c + i]);
-          }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
-      }
-      if (debug) continue;
-      // final scale, alpha/beta epilogue, column-major store (coalesced per column)
-      if (row < p.m) {
-        const int er = p.expA[row];
-        const bool use_c = p.c_is_input && p.beta != 0.0;
-        // chunks of 16 columns: issue all loads of a chunk before any store
-#pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 16) {
-          int eb[16];
-          double cv[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int col = col0 + c0 + i;
-            const bool ok = col < p.n;
-            eb[i] = ok ? __ldg(p.expB + col) : 0;
-            cv[i] = (ok && use_c) ? p.c[(int64_t)col * p.ldc + row] : 0.0;
-          }
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int col = col0 + c0 + i;
-            if (col < p.n) {
-              const double ab = ldexp_exact(acc[c0 + i], er + eb[i]);
-              double out = __dmul_rn(p.alpha, ab);
-              if (use_c) out = __dadd_rn(out, __dmul_rn(p.beta, cv[i]));
-              p.c[(int64_t)col * p.ldc + row] = out;
-              gmax = fmax(gmax, fabs(out));
-            }
-          }
-        }
-      }
-    }
-    if (p.growth != nullptr) {
-      gmax = warp_max(gmax);
-      if (lane == 0 && gmax > 0.0) atomic_max_abs(p.growth, gmax);
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(TMEM_COLS)
-                 : "memory");
-  }
-}
-
-
 // =====================================================================
 // CTA-pair variant (cta_group::2): the pair computes a 256 x 128 tile; each
 // CTA stages its own 128 rows of A and one half (64 rows) of B, the leader
@@ -433,7 +175,7 @@ constexpr int FP_CHUNK = 8;  // final-pass columns with loads in flight at once
 // warps 8 and 9 — the top ids of SMSPs 0 and 1 — and are never starved by the
 // epilogue warps 0-7 that share those SMSPs.
 constexpr int P_PRODUCER = 8, P_MMA = 9, P_ALLOC = 10;
-constexpr int P_EPI_ARRIVALS = 2 * (NUM_THREADS / 32 - EPI_WARP0);
+constexpr int P_EPI_ARRIVALS = 2 * EPI_WARPS;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -823,11 +565,6 @@ void build_groups(Params& p, const int32_t* shift, int npairs, int64_t inner) {
   p.ngroups = g;
 }
 
-bool use_pair_kernel() {
-  static const bool single = getenv("OZ_GEMM_1CTA") != nullptr;  // A/B switch for tuning
-  return !single;
-}
-
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStream_t st,
                 int max_ctas = 0) {
   static bool attr_set = false;
@@ -859,26 +596,6 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStr
     emu_gemm_pair_kernel<true><<<grid, NUM_THREADS, P_SMEM_BYTES, st>>>(ta, tb, p);
   else
     emu_gemm_pair_kernel<false><<<grid, NUM_THREADS, P_SMEM_BYTES, st>>>(ta, tb, p);
-  OZ_CHECK_LAUNCH();
-  return OZ_OK;
-}
-
-int launch(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    OZ_CHECK_CUDA(cudaFuncSetAttribute(emu_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)SMEM_BYTES));
-    attr_set = true;
-  }
-  p.num_m_tiles = (int)ceil_div(p.m, BM);
-  p.num_n_tiles = (int)ceil_div(p.n, BN);
-  p.num_tiles = p.num_m_tiles * p.num_n_tiles;
-  p.nkb = (int)ceil_div(p.inner, BK);
-  p.group_m = GROUP_M;
-  int grid = sm_count();
-  if (const char* g = getenv("OZ_GEMM_GRID")) grid = atoi(g) > 0 ? atoi(g) : grid;  // tuning knob
-  if (grid > p.num_tiles) grid = p.num_tiles;
-  emu_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ta, tb, p);
   OZ_CHECK_LAUNCH();
   return OZ_OK;
 }
@@ -924,11 +641,9 @@ int gemm_emu_launch(int64_t m, int64_t n, int64_t inner, const int8_t* a_slices,
   p.beta = beta;
   p.growth = growth;
   CUtensorMap ta, tb;
-  const bool pair = use_pair_kernel();
   OZ_TRY(make_slice_map(&ta, a_slices, inner, m, a_ld, a_sstride, a_nslices, BM));
-  OZ_TRY(make_slice_map(&tb, b_slices, inner, n, b_ld, b_sstride, b_nslices,
-                        pair ? P_BN / 2 : BN));
-  return pair ? launch_pair(ta, tb, p, st, max_ctas) : launch(ta, tb, p, st);
+  OZ_TRY(make_slice_map(&tb, b_slices, inner, n, b_ld, b_sstride, b_nslices, P_BN / 2));
+  return launch_pair(ta, tb, p, st, max_ctas);
 }
 
 }  // namespace oz
@@ -971,11 +686,9 @@ extern "C" int oz_gemm_pair_i32(int64_t m, int64_t n, int64_t inner, const int8_
   p.ldo = ldo;
   p.alpha = 1.0;
   CUtensorMap ta, tb;
-  const bool pair = use_pair_kernel();
   OZ_TRY(make_slice_map(&ta, a_slice, inner, m, a_ld, round_up(m * a_ld, 16), 1, BM));
-  OZ_TRY(make_slice_map(&tb, b_slice, inner, n, b_ld, round_up(n * b_ld, 16), 1,
-                        pair ? P_BN / 2 : BN));
-  return pair ? launch_pair(ta, tb, p, as_stream(stream)) : launch(ta, tb, p, as_stream(stream));
+  OZ_TRY(make_slice_map(&tb, b_slice, inner, n, b_ld, round_up(n * b_ld, 16), 1, P_BN / 2));
+  return launch_pair(ta, tb, p, as_stream(stream));
 }
 
 // Host-only: expose the exact-level grouping plan (for tests / introspection).
