@@ -77,7 +77,11 @@ size_t oz_split_aux_bytes(void);
  * Bit-exact with the reference.  `aux` is device scratch of
  * oz_split_aux_bytes() bytes; after the call aux[0] (int32) is nonzero iff a
  * NaN/Inf was seen (the Python layer raises NonFiniteEntryError).
- * slice_bits must be <= 7 (int8 slices).
+ * slice_bits 1..7: int8 slices, plane s = slice s.  slice_bits 8..10 (the
+ * reference's int16 slices, split.py:144): 2 * num_slices int8 planes,
+ * plane 2s = floor(slice / 128), plane 2s+1 = slice mod 128 (slice =
+ * 128 * hi + lo); oz_gemm_emu takes the same planes with the same slice_bits
+ * and recombines every slice product exactly.
  */
 int oz_split(const double* src, int64_t rows, int64_t cols,
              int64_t row_stride, int64_t col_stride,
@@ -101,15 +105,15 @@ int oz_gemm_emu(int64_t m, int64_t n, int64_t inner,
                 const int8_t* b_slices, int64_t b_ld, int64_t b_sstride, int b_nslices,
                 const int32_t* b_exps,
                 int npairs, const int32_t* pair_a, const int32_t* pair_b,
-                const int32_t* pair_shift,
+                const int32_t* pair_shift, int slice_bits,
                 double alpha, double beta, double* c, int64_t ldc, int c_is_input,
                 unsigned long long* growth_max, void* stream);
 
 /* Host-only: the exact-level grouping plan oz_gemm_emu uses (see
  * csrc/gemm_emu.cu build_groups).  Returns the group count; gstart[0..G] are
  * pair offsets, gshift[0..G) the (i+j)*q of each group. */
-int oz_plan_groups(int npairs, const int32_t* pair_shift, int64_t inner, int32_t* gstart,
-                   int32_t* gshift);
+int oz_plan_groups(int npairs, const int32_t* pair_shift, int64_t inner, int slice_bits,
+                   int32_t* gstart, int32_t* gshift);
 
 /* One slice-pair product as raw INT32 (debug/parity: test_gemm.py:218-240). */
 int oz_gemm_pair_i32(int64_t m, int64_t n, int64_t inner,
@@ -133,7 +137,7 @@ int oz_dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k, double alp
  * interchanges; `stats` (device double[4]) receives {observed max, max|A|, -, -}
  * for the growth factor; `info` (device int32) = first zero-pivot column + 1 or 0.
  */
-size_t oz_lu_workspace_bytes(int64_t n, int64_t nb, int num_slices);
+size_t oz_lu_workspace_bytes(int64_t n, int64_t nb, int num_slices, int slice_bits);
 int oz_lu_factor(double* a, int64_t n, int64_t lda, int64_t nb,
                  int backend, int num_slices, int slice_bits,
                  int npairs, const int32_t* pair_a, const int32_t* pair_b,
@@ -182,7 +186,8 @@ int oz_copy2d(const double* src, int64_t rows, int64_t cols, int64_t src_rs, int
 /*
  * Step-level LU (the loop of solve.py:94-140 owned by the caller; used by the
  * distributed 1 x Q block-cyclic HPL driver).  All take the LU workspace
- * (oz_lu_workspace_bytes(ws_n, ws_nb, ws_slices) bytes) and its shape.
+ * (oz_lu_workspace_bytes(ws_n, ws_nb, num_slices, slice_bits) bytes) and its
+ * shape; ws_slices counts int8 planes (num_slices, doubled for slice_bits > 7).
  *
  * oz_lu_ws_init:  zero the workspace's barriers/tags (once per factorization).
  * oz_lu_panel:    factor the m x jb panel at `a` (its diagonal corner, rows

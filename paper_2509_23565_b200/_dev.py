@@ -49,7 +49,8 @@ def strides2d(x):
 
 
 class SplitResult:
-    """Device slice stack: slices [k, nvec, ld] int8 (K-major), exps int32[nvec]."""
+    """Device slice stack: slices [planes, nvec, ld] int8 (K-major; planes = k,
+    or 2k (hi, lo) planes for q > 7), exps int32[nvec]."""
 
     __slots__ = ("slices", "exps", "ld", "nvec", "inner", "k")
 
@@ -64,7 +65,8 @@ def split_device(a, k: int, q: int, orientation: int, mode: int) -> SplitResult:
     rows, cols = int(a.shape[0]), int(a.shape[1])
     nvec, inner = (rows, cols) if orientation == 0 else (cols, rows)
     ld = max(16, -(-inner // 16) * 16)
-    slices = t.empty((k, nvec, ld), dtype=t.int8, device=a.device)
+    planes = 2 * k if q > 7 else k   # q > 7: (hi, lo) int8 planes per int16 slice
+    slices = t.empty((planes, nvec, ld), dtype=t.int8, device=a.device)
     exps = t.empty((nvec,), dtype=t.int32, device=a.device)
     aux = t.empty((4,), dtype=t.int32, device=a.device)
     rs, cs = strides2d(a)

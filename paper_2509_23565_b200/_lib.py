@@ -35,11 +35,11 @@ _SIGNATURES = {
     "oz_split": [_vp, _i64, _i64, _i64, _i64, _int, _int, _int, _int, _vp, _i64, _i64, _vp, _vp,
                  _vp],
     "oz_gemm_emu": [_i64, _i64, _i64, _vp, _i64, _i64, _int, _vp, _vp, _i64, _i64, _int, _vp,
-                    _int, _vp, _vp, _vp, _dbl, _dbl, _vp, _i64, _int, _vp, _vp],
-    "oz_plan_groups": [_int, _vp, _i64, _vp, _vp],
+                    _int, _vp, _vp, _vp, _int, _dbl, _dbl, _vp, _i64, _int, _vp, _vp],
+    "oz_plan_groups": [_int, _vp, _i64, _int, _vp, _vp],
     "oz_gemm_pair_i32": [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp],
     "oz_dgemm": [_int, _int, _i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64, _vp],
-    "oz_lu_workspace_bytes": [_i64, _i64, _int],
+    "oz_lu_workspace_bytes": [_i64, _i64, _int, _int],
     "oz_lu_factor": [_vp, _i64, _i64, _i64, _int, _int, _int, _int, _vp, _vp, _vp, _vp, _vp,
                      _vp, _vp, C.c_size_t, _vp],
     "oz_ipiv_to_perm": [_vp, _i64, _vp],

@@ -62,6 +62,7 @@ struct Params {
   int ngroups;
   int group_m;  // raster band height in tiles
   int experiment;  // tuning only (OZ_GEMM_EXPERIMENT): 1 = skip FP64 math, 2 = also skip final pass
+  int wide;        // slice_bits > 7: (hi, lo) int8 planes per slice
   uint8_t pa[MAX_PAIRS];
   uint8_t pb[MAX_PAIRS];
   uint16_t gshift[MAX_PAIRS];      // (i+j)*q of the group's pairs
@@ -93,6 +94,15 @@ __device__ __forceinline__ void tc_fence_before() {
 }
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
   asm volatile(
@@ -253,7 +263,12 @@ __device__ __forceinline__ void pair_tile_coords(const Params& p, int t, int& mt
   tile_coords(p, t, mt, nt);  // same grouped raster, on pair tiles (num_m_tiles in 256 rows)
 }
 
-template <bool kDebug>
+// kWide (slice_bits 8..10): each slice is a (hi, lo) pair of int8 planes
+// (split.cu) and a slice-pair product is 16384*P(hi,hi) + 128*(P(hi,lo) +
+// P(lo,hi)) + P(lo,lo).  The three INT32 parts of a group land in TMEM slots
+// 0, 1, 2 and the epilogue recombines them exactly (integers < 2^53) before
+// the reference-order FP64 accumulation; one group is in flight at a time.
+template <bool kDebug, bool kWide>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     emu_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                          const __grid_constant__ CUtensorMap tmB, const __grid_constant__ Params p) {
@@ -316,7 +331,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const int arow = mt * P_BM + (int)rank * 128;
       const int brow = nt * P_BN + (int)rank * (P_BN / 2);
       for (int q = 0; q < p.npairs; ++q) {
-        const int sa = p.pa[q], sb = p.pb[q];
+       for (int sub = 0; sub < (kWide ? 4 : 1); ++sub) {
+        // kWide sub-products: (hi,hi), (hi,lo), (lo,hi), (lo,lo) planes
+        const int sa = kWide ? 2 * p.pa[q] + (sub >> 1) : p.pa[q];
+        const int sb = kWide ? 2 * p.pb[q] + (sub & 1) : p.pb[q];
         for (int kb = 0; kb < p.nkb; ++kb) {
           if (stage % P_SGROUP == 0) mbar_wait(smem_u32(&empty[stage / P_SGROUP]), phase ^ 1);
           if (elect_one()) {
@@ -334,6 +352,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             phase ^= 1;
           }
         }
+       }
       }
     }
   } else if (warp == P_MMA) {
@@ -348,19 +367,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       uint32_t it = 0;
       for (int t = cid; t < p.num_tiles; t += ncl) {
         for (int g = 0; g < p.ngroups; ++g, ++it) {
-          const uint32_t buf = it % NUM_ACC, aph = (it / NUM_ACC) & 1;
+          const uint32_t ring = kWide ? 1 : NUM_ACC;  // kWide: one slot triple
+          const uint32_t buf = it % ring, aph = (it / ring) & 1;
           mbar_wait(smem_u32(&tempty[buf]), aph ^ 1);
           tc_fence_after();
-          const uint32_t dtmem = tmem_base + buf * P_BN;
           for (int q = p.gstart[g]; q < p.gstart[g + 1]; ++q) {
             const bool first_pair = q == p.gstart[g];
+           for (int sub = 0; sub < (kWide ? 4 : 1); ++sub) {
+            // kWide: (hi,hi) -> slot 0, (hi,lo) and (lo,hi) -> slot 1, (lo,lo) -> slot 2
+            const uint32_t slot = kWide ? (sub == 0 ? 0u : sub == 3 ? 2u : 1u) : buf;
+            const bool opens = first_pair && (!kWide || sub != 2);
+            const uint32_t dtmem = tmem_base + slot * P_BN;
             for (int kb = 0; kb < p.nkb; ++kb) {
               mbar_wait(smem_u32(&full[stage]), phase);
               tc_fence_after();
               static_assert(BK / 32 == 4, "stage issue assumes 4 MMAs per stage");
               tc_mma_i8_pair_stage(dtmem, a_lo0 + (uint32_t)stage * (P_A_BYTES >> 4),
                                    b_lo0 + (uint32_t)stage * (P_B_BYTES >> 4), desc_hi, P_IDESC,
-                                   (first_pair && kb == 0) ? 0u : 1u);
+                                   (opens && kb == 0) ? 0u : 1u);
               if (stage % P_SGROUP == P_SGROUP - 1)
                 tc_commit_pair(smem_u32(&empty[stage / P_SGROUP]));
               __syncwarp();
@@ -369,6 +393,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 phase ^= 1;
               }
             }
+           }
           }
           tc_commit_pair(smem_u32(&tfull[buf]));
           __syncwarp();
@@ -395,6 +420,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const int row = mt * P_BM + (int)rank * 128 + quad * 32 + lane;
       const int col0 = nt * P_BN + half * 64;
       for (int q = 0; q < p.ngroups; ++q, ++it) {
+        if constexpr (kWide) {
+          // slot triple: exact 16384*hh + 128*mid + ll per element, then one
+          // reference-order FMA; 16 columns at a time keeps registers in budget
+          const uint32_t aph = it & 1;
+          mbar_wait(smem_u32(&tfull[0]), aph);
+          tc_fence_after();
+          const uint32_t tb = tmem_base + lane_base + half * 64;
+          const double s = pow2(-(int)p.gshift[q]);
+#pragma unroll
+          for (int c = 0; c < 64; c += 16) {
+            uint32_t hh[16], mid[16], ll[16];
+            tmem_ld16(tb + c, hh);
+            tmem_ld16(tb + P_BN + c, mid);
+            tmem_ld16(tb + 2 * P_BN + c, ll);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const double t = __dadd_rn(fma(i32_to_f64(hh[i]), 16384.0,
+                                             __dmul_rn(i32_to_f64(mid[i]), 128.0)),
+                                         i32_to_f64(ll[i]));
+              acc[c + i] = fma(t, s, acc[c + i]);
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote(tempty_leader);
+          continue;
+        }
         const uint32_t buf = it % NUM_ACC, aph = (it / NUM_ACC) & 1;
         mbar_wait(smem_u32(&tfull[buf]), aph);
         tc_fence_after();
@@ -529,8 +582,12 @@ int make_slice_map(CUtensorMap* map, const int8_t* base, int64_t inner, int64_t 
 // (b) the running magnitude bound, in units of the level's LSB 2^-shift, stays
 // below 2^53.  From the first level that fails, every pair is its own group
 // and is accumulated in the reference order with one rounding per pair.
-void build_groups(Params& p, const int32_t* shift, int npairs, int64_t inner) {
-  const double term = (double)inner * 127.0 * 127.0;  // max |P| of one pair
+void build_groups(Params& p, const int32_t* shift, int npairs, int64_t inner, int q) {
+  // max |P| of one pair: K * (2^q - 1)^2 (q > 7: int16 slices), and the INT32
+  // sub-accumulators hold at most K * 127^2 per pair (int8 operands)
+  const double smax = q > 7 ? (double)((1 << q) - 1) : 127.0;
+  const double term = (double)inner * smax * smax;
+  const double term32 = (double)inner * 127.0 * 127.0;
   double bound = 0.0;                                  // sum of max |P_p| * 2^-shift_p
   bool exact = true;
   int g = 0, i = 0;
@@ -541,7 +598,7 @@ void build_groups(Params& p, const int32_t* shift, int npairs, int64_t inner) {
     if (exact) {
       const double lvl = term * (j - i);
       const double nb = bound + ldexp(lvl, -shift[i]);
-      if (lvl < 2147483648.0 && ldexp(nb, shift[i]) < 9007199254740992.0) {
+      if (term32 * (j - i) < 2147483648.0 && ldexp(nb, shift[i]) < 9007199254740992.0) {
         bound = nb;
         grouped = true;
       } else {
@@ -569,10 +626,13 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStr
                 int max_ctas = 0) {
   static bool attr_set = false;
   if (!attr_set) {
-    OZ_CHECK_CUDA(cudaFuncSetAttribute(emu_gemm_pair_kernel<false>,
+    OZ_CHECK_CUDA(cudaFuncSetAttribute(emu_gemm_pair_kernel<false, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)P_SMEM_BYTES));
-    OZ_CHECK_CUDA(cudaFuncSetAttribute(emu_gemm_pair_kernel<true>,
+    OZ_CHECK_CUDA(cudaFuncSetAttribute(emu_gemm_pair_kernel<false, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)P_SMEM_BYTES));
+    OZ_CHECK_CUDA(cudaFuncSetAttribute(emu_gemm_pair_kernel<true, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)P_SMEM_BYTES));
     attr_set = true;
@@ -593,9 +653,11 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStr
   if (grid < 2) grid = 2;
   if (grid > 2 * p.num_tiles) grid = 2 * p.num_tiles;
   if (p.debug_out != nullptr)
-    emu_gemm_pair_kernel<true><<<grid, NUM_THREADS, P_SMEM_BYTES, st>>>(ta, tb, p);
+    emu_gemm_pair_kernel<true, false><<<grid, NUM_THREADS, P_SMEM_BYTES, st>>>(ta, tb, p);
+  else if (p.wide)
+    emu_gemm_pair_kernel<false, true><<<grid, NUM_THREADS, P_SMEM_BYTES, st>>>(ta, tb, p);
   else
-    emu_gemm_pair_kernel<false><<<grid, NUM_THREADS, P_SMEM_BYTES, st>>>(ta, tb, p);
+    emu_gemm_pair_kernel<false, false><<<grid, NUM_THREADS, P_SMEM_BYTES, st>>>(ta, tb, p);
   OZ_CHECK_LAUNCH();
   return OZ_OK;
 }
@@ -606,10 +668,12 @@ int gemm_emu_launch(int64_t m, int64_t n, int64_t inner, const int8_t* a_slices,
                     int64_t a_sstride, int a_nslices, const int32_t* a_exps,
                     const int8_t* b_slices, int64_t b_ld, int64_t b_sstride, int b_nslices,
                     const int32_t* b_exps, int npairs, const int32_t* pair_a,
-                    const int32_t* pair_b, const int32_t* pair_shift, double alpha, double beta,
-                    double* c, int64_t ldc, int c_is_input, unsigned long long* growth,
-                    cudaStream_t st, int max_ctas) {
+                    const int32_t* pair_b, const int32_t* pair_shift, int slice_bits,
+                    double alpha, double beta, double* c, int64_t ldc, int c_is_input,
+                    unsigned long long* growth, cudaStream_t st, int max_ctas) {
   using namespace emu;
+  OZ_REQUIRE(slice_bits >= 1 && slice_bits <= 10, OZ_INVALID_PARAMS, "slice_bits outside 1..10");
+  const bool wide = slice_bits > 7;  // slices are (hi, lo) int8 plane pairs
   OZ_REQUIRE(m >= 1 && n >= 1 && inner >= 1, OZ_INVALID_PARAMS, "empty GEMM");
   OZ_REQUIRE(m < (1ll << 31) && n < (1ll << 31), OZ_INVALID_PARAMS, "dimension too large");
   OZ_REQUIRE(inner * 127ll * 127ll < (1ll << 31), OZ_ACC_OVERFLOW,
@@ -631,7 +695,8 @@ int gemm_emu_launch(int64_t m, int64_t n, int64_t inner, const int8_t* a_slices,
     p.pa[i] = (uint8_t)pair_a[i];
     p.pb[i] = (uint8_t)pair_b[i];
   }
-  build_groups(p, pair_shift, npairs, inner);
+  build_groups(p, pair_shift, npairs, inner, slice_bits);
+  p.wide = wide ? 1 : 0;
   p.expA = a_exps;
   p.expB = b_exps;
   p.c = c;
@@ -641,8 +706,10 @@ int gemm_emu_launch(int64_t m, int64_t n, int64_t inner, const int8_t* a_slices,
   p.beta = beta;
   p.growth = growth;
   CUtensorMap ta, tb;
-  OZ_TRY(make_slice_map(&ta, a_slices, inner, m, a_ld, a_sstride, a_nslices, BM));
-  OZ_TRY(make_slice_map(&tb, b_slices, inner, n, b_ld, b_sstride, b_nslices, P_BN / 2));
+  OZ_TRY(make_slice_map(&ta, a_slices, inner, m, a_ld, a_sstride, wide ? 2 * a_nslices : a_nslices,
+                        BM));
+  OZ_TRY(make_slice_map(&tb, b_slices, inner, n, b_ld, b_sstride, wide ? 2 * b_nslices : b_nslices,
+                        P_BN / 2));
   return launch_pair(ta, tb, p, st, max_ctas);
 }
 
@@ -652,15 +719,15 @@ extern "C" int oz_gemm_emu(int64_t m, int64_t n, int64_t inner, const int8_t* a_
                            int64_t a_ld, int64_t a_sstride, int a_nslices, const int32_t* a_exps,
                            const int8_t* b_slices, int64_t b_ld, int64_t b_sstride, int b_nslices,
                            const int32_t* b_exps, int npairs, const int32_t* pair_a,
-                           const int32_t* pair_b, const int32_t* pair_shift, double alpha,
-                           double beta, double* c, int64_t ldc, int c_is_input,
+                           const int32_t* pair_b, const int32_t* pair_shift, int slice_bits,
+                           double alpha, double beta, double* c, int64_t ldc, int c_is_input,
                            unsigned long long* growth_max, void* stream) {
   cudaStream_t st = oz::as_stream(stream);
   const int tag = oz::prof_start(st);
   const int s = oz::gemm_emu_launch(m, n, inner, a_slices, a_ld, a_sstride, a_nslices, a_exps,
                                     b_slices, b_ld, b_sstride, b_nslices, b_exps, npairs, pair_a,
-                                    pair_b, pair_shift, alpha, beta, c, ldc, c_is_input,
-                                    growth_max, st, 0);
+                                    pair_b, pair_shift, slice_bits, alpha, beta, c, ldc,
+                                    c_is_input, growth_max, st, 0);
   oz::prof_stop(tag, st, oz::PROF_EMU_GEMM, 2.0 * npairs * (double)m * n * inner);
   return s;
 }
@@ -694,12 +761,12 @@ extern "C" int oz_gemm_pair_i32(int64_t m, int64_t n, int64_t inner, const int8_
 // Host-only: expose the exact-level grouping plan (for tests / introspection).
 // gstart must hold npairs+1 entries; returns the number of groups.
 extern "C" int oz_plan_groups(int npairs, const int32_t* pair_shift, int64_t inner,
-                              int32_t* gstart, int32_t* gshift) {
+                              int slice_bits, int32_t* gstart, int32_t* gshift) {
   using namespace oz;
   using namespace oz::emu;
   OZ_REQUIRE(npairs >= 1 && npairs <= MAX_PAIRS, OZ_INVALID_PARAMS, "npairs out of range");
   Params p{};
-  build_groups(p, pair_shift, npairs, inner);
+  build_groups(p, pair_shift, npairs, inner, slice_bits);
   for (int g = 0; g <= p.ngroups; ++g) gstart[g] = p.gstart[g];
   for (int g = 0; g < p.ngroups; ++g) gshift[g] = p.gshift[g];
   return p.ngroups;

@@ -40,9 +40,9 @@ int gemm_emu_launch(int64_t m, int64_t n, int64_t inner, const int8_t* a_slices,
                     int64_t a_sstride, int a_nslices, const int32_t* a_exps,
                     const int8_t* b_slices, int64_t b_ld, int64_t b_sstride, int b_nslices,
                     const int32_t* b_exps, int npairs, const int32_t* pair_a,
-                    const int32_t* pair_b, const int32_t* pair_shift, double alpha, double beta,
-                    double* c, int64_t ldc, int c_is_input, unsigned long long* growth,
-                    cudaStream_t st, int max_ctas);
+                    const int32_t* pair_b, const int32_t* pair_shift, int slice_bits,
+                    double alpha, double beta, double* c, int64_t ldc, int c_is_input,
+                    unsigned long long* growth, cudaStream_t st, int max_ctas);
 
 namespace {
 
@@ -1029,8 +1029,8 @@ int schur_cols(const Schur& s, int64_t c0, int64_t c1, const LuWs& ws, cudaStrea
   const int tag = prof_start(st);
   OZ_TRY(gemm_emu_launch(s.m, nc, s.jb, ws.slA, ws.ldK, s.m * ws.ldK, s.k, ws.expA,
                          ws.slB + c0 * ws.ldK, ws.ldK, s.ncols * ws.ldK, s.k, ws.expB + c0,
-                         s.npairs, s.pa, s.pb, s.ps, -1.0, 1.0, c, s.lda22, 1, s.growth, st,
-                         max_ctas));
+                         s.npairs, s.pa, s.pb, s.ps, s.q, -1.0, 1.0, c, s.lda22, 1, s.growth,
+                         st, max_ctas));
   prof_stop(tag, st, PROF_EMU_GEMM, 2.0 * s.npairs * s.m * nc * s.jb);
   return OZ_OK;
 }
@@ -1126,7 +1126,8 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
   OZ_REQUIRE(lda >= n, OZ_INVALID_PARAMS, "lda < n");
   OZ_REQUIRE(backend >= 0 && backend <= 2, OZ_INVALID_PARAMS, "bad backend %d", backend);
   LuWs ws;
-  const size_t need = lu_ws_layout(n, nb, backend != 0 ? k : 0, (uint8_t*)workspace, &ws);
+  const int planes = backend != 0 ? (q > 7 ? 2 * k : k) : 0;  // int8 planes per slice stack
+  const size_t need = lu_ws_layout(n, nb, planes, (uint8_t*)workspace, &ws);
   OZ_REQUIRE(ws_bytes >= need, OZ_INVALID_PARAMS, "workspace too small (%zu < %zu)", ws_bytes,
              need);
   OZ_CHECK_CUDA(cudaMemsetAsync(ws.bar, 0, sizeof(GridBar), st));
@@ -1264,8 +1265,8 @@ int gemv_rows(const double* a, int64_t n, int64_t rs, int64_t cs, const double* 
 }  // namespace oz
 
 // ======================================================================= C ABI
-extern "C" size_t oz_lu_workspace_bytes(int64_t n, int64_t nb, int num_slices) {
-  return oz::lu_ws_layout(n, nb, num_slices, nullptr, nullptr);
+extern "C" size_t oz_lu_workspace_bytes(int64_t n, int64_t nb, int num_slices, int slice_bits) {
+  return oz::lu_ws_layout(n, nb, slice_bits > 7 ? 2 * num_slices : num_slices, nullptr, nullptr);
 }
 
 extern "C" int oz_lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend,
@@ -1416,7 +1417,8 @@ extern "C" int oz_schur_update(int backend, int64_t m, int64_t ncols, int64_t jb
   OZ_REQUIRE(backend == 0 || (m <= ws_n && ncols <= ws_n && jb <= ws_nb), OZ_INVALID_PARAMS,
              "schur update larger than the workspace");
   LuWs w;
-  OZ_TRY(ws_view(ws, ws_bytes, ws_n, ws_nb, backend != 0 ? num_slices : 0, &w));
+  OZ_TRY(ws_view(ws, ws_bytes, ws_n, ws_nb,
+                 backend != 0 ? (slice_bits > 7 ? 2 * num_slices : num_slices) : 0, &w));
   return schur_update(backend, m, ncols, jb, a21, lda21, u12, ldu, a22, lda22, num_slices,
                       slice_bits, npairs, pair_a, pair_b, pair_shift, growth_bits, w,
                       as_stream(stream));
@@ -1482,7 +1484,7 @@ extern "C" int oz_schur_split(int backend, int64_t m, int64_t ncols, int64_t jb,
   OZ_REQUIRE(m <= ws_n && ncols <= ws_n && jb <= ws_nb, OZ_INVALID_PARAMS,
              "schur update larger than the workspace");
   LuWs w;
-  OZ_TRY(ws_view(ws, ws_bytes, ws_n, ws_nb, num_slices, &w));
+  OZ_TRY(ws_view(ws, ws_bytes, ws_n, ws_nb, slice_bits > 7 ? 2 * num_slices : num_slices, &w));
   const Schur s{backend, m, ncols, jb, a21, lda21, u12, ldu, nullptr, 0, num_slices, slice_bits,
                 0, nullptr, nullptr, nullptr, nullptr};
   return schur_split(s, w, as_stream(stream));
@@ -1501,7 +1503,8 @@ extern "C" int oz_schur_cols(int backend, int64_t m, int64_t ncols, int64_t jb,
   OZ_REQUIRE(backend == 0 || (m <= ws_n && ncols <= ws_n && jb <= ws_nb), OZ_INVALID_PARAMS,
              "schur update larger than the workspace");
   LuWs w;
-  OZ_TRY(ws_view(ws, ws_bytes, ws_n, ws_nb, backend != 0 ? num_slices : 0, &w));
+  OZ_TRY(ws_view(ws, ws_bytes, ws_n, ws_nb,
+                 backend != 0 ? (slice_bits > 7 ? 2 * num_slices : num_slices) : 0, &w));
   const Schur s{backend, m, ncols, jb, a21, lda21, u12, ldu, a22, lda22, num_slices, slice_bits,
                 npairs, pair_a, pair_b, pair_shift, growth_bits};
   return schur_cols(s, c0, c1, w, as_stream(stream), max_ctas);

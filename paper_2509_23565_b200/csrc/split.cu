@@ -10,6 +10,10 @@
 // Layout: "vector" v carries the exponent (rows when ROW_SCALED, columns when
 // COL_SCALED), t is the inner (GEMM-K) index.  Element (v,t) of the source is
 // src[v*vs + t*ts].  Output slices are K-major int8: slices[s*sstride + v*ld + t].
+// For q = 8..10 (int16 slices, split.py:144) each slice is written as two int8
+// planes, plane 2s = floor(slice / 128) and plane 2s+1 = slice mod 128, so the
+// tensor cores multiply int8 planes and the GEMM recombines the slice product
+// exactly (gemm_emu.cu, kWide).
 //
 // Two kernels: (1) exponent pass = warp-shuffle max reduction per vector plus
 // NaN/Inf detection; (2) slice emission.  Each has a fast path for the
@@ -118,7 +122,7 @@ __device__ __forceinline__ int vector_exponent(const int32_t* exps, int64_t v, i
 // ---- slice emission, K contiguous: one warp per vector, 16 t per lane ------
 template <int KS>
 __global__ void slices_kcontig_kernel(const double* __restrict__ src, int64_t nvec, int64_t K,
-                                      int64_t vs, int mode, int ksl, int q,
+                                      int64_t vs, int mode, int ksl, int q, bool wide,
                                       int8_t* __restrict__ out, int64_t ld, int64_t sstride,
                                       int32_t* __restrict__ exps, const SplitAux* aux) {
   const int lane = threadIdx.x & 31;
@@ -147,27 +151,28 @@ __global__ void slices_kcontig_kernel(const double* __restrict__ src, int64_t nv
 #pragma unroll
       for (int i = 0; i < 16; ++i) x[i] = ldexp_exact(x[i], -e);
       for (int s = 0; s < ksl; ++s) {
-        uint32_t w[4];
+        uint32_t w[4], wl[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          uint32_t packed = 0;
+          uint32_t packed = 0, packed_lo = 0;
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
             double y = __dmul_rn(x[4 * i + b], radix);
             double tr = trunc(y);
             x[4 * i + b] = __dsub_rn(y, tr);
-            packed |= (uint32_t)(uint8_t)(int8_t)(int)tr << (8 * b);
+            const int ti = (int)tr;
+            // q > 7: slice = 128 * hi + lo, hi = floor(slice / 128), lo in [0, 127]
+            packed |= (uint32_t)(uint8_t)(int8_t)(wide ? (ti >> 7) : ti) << (8 * b);
+            packed_lo |= (uint32_t)(uint8_t)(ti & 127) << (8 * b);
           }
           w[i] = packed;
+          wl[i] = packed_lo;
         }
-        int8_t* dst = out + s * sstride + v * ld + t0;
-        if (t0 + 16 <= ld) {
-          *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
-        } else {  // ld is a multiple of 16, so this branch is never taken
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (t0 + i < ld) dst[i] = (int8_t)(w[i >> 2] >> (8 * (i & 3)));
-        }
+        // ld is a multiple of 16, so every 16-byte store is in bounds
+        int8_t* dst = out + (wide ? 2 * s : s) * sstride + v * ld + t0;
+        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+        if (wide)
+          *reinterpret_cast<uint4*>(dst + sstride) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
       }
     }
   }
@@ -175,7 +180,7 @@ __global__ void slices_kcontig_kernel(const double* __restrict__ src, int64_t nv
 
 // ---- slice emission, general strides: 32 vectors x 64 t tile via smem ------
 __global__ void slices_tiled_kernel(const double* __restrict__ src, int64_t nvec, int64_t K,
-                                    int64_t vs, int64_t ts, int mode, int ksl, int q,
+                                    int64_t vs, int64_t ts, int mode, int ksl, int q, bool wide,
                                     int8_t* __restrict__ out, int64_t ld, int64_t sstride,
                                     int32_t* __restrict__ exps, const SplitAux* aux) {
   __shared__ double tile[64][33];
@@ -212,20 +217,25 @@ __global__ void slices_tiled_kernel(const double* __restrict__ src, int64_t nvec
 #pragma unroll
   for (int i = 0; i < 8; ++i) x[i] = ldexp_exact(tile[tc + i][vl], -e);
   for (int s = 0; s < ksl; ++s) {
-    uint32_t w[2];
+    uint32_t w[2], wl[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      uint32_t packed = 0;
+      uint32_t packed = 0, packed_lo = 0;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         double y = __dmul_rn(x[4 * i + b], radix);
         double tr = trunc(y);
         x[4 * i + b] = __dsub_rn(y, tr);
-        packed |= (uint32_t)(uint8_t)(int8_t)(int)tr << (8 * b);
+        const int ti = (int)tr;
+        packed |= (uint32_t)(uint8_t)(int8_t)(wide ? (ti >> 7) : ti) << (8 * b);
+        packed_lo |= (uint32_t)(uint8_t)(ti & 127) << (8 * b);
       }
       w[i] = packed;
+      wl[i] = packed_lo;
     }
-    *reinterpret_cast<uint2*>(out + s * sstride + v * ld + tt) = make_uint2(w[0], w[1]);
+    int8_t* dst = out + (wide ? 2 * s : s) * sstride + v * ld + tt;
+    *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+    if (wide) *reinterpret_cast<uint2*>(dst + sstride) = make_uint2(wl[0], wl[1]);
   }
 }
 
@@ -236,8 +246,8 @@ int split_launch(const double* src, int64_t rows, int64_t cols, int64_t row_stri
                  int64_t slice_ld, int64_t slice_stride, int32_t* exps, void* aux_v,
                  cudaStream_t st) {
   OZ_REQUIRE(k >= 1, OZ_INVALID_PARAMS, "num_slices must be >= 1");
-  OZ_REQUIRE(q >= 1 && q <= 7, OZ_UNSUPPORTED,
-             "slice_bits=%d: only int8 slices (q <= 7) run on the tensor cores", q);
+  OZ_REQUIRE(q >= 1 && q <= 10, OZ_INVALID_PARAMS, "slice_bits=%d outside 1..10", q);
+  const bool wide = q > 7;  // int16 slices, emitted as (hi, lo) int8 planes
   OZ_REQUIRE(rows >= 1 && cols >= 1, OZ_INVALID_PARAMS, "empty matrices are not supported");
   OZ_REQUIRE(orientation == OZ_ROW_SCALED || orientation == OZ_COL_SCALED, OZ_INVALID_PARAMS,
              "bad orientation");
@@ -260,14 +270,14 @@ int split_launch(const double* src, int64_t rows, int64_t cols, int64_t row_stri
     exps_kcontig_kernel<<<(unsigned)blocks, threads, 0, st>>>(src, nvec, K, vs, mode, exps, aux);
     OZ_CHECK_LAUNCH();
     slices_kcontig_kernel<16><<<(unsigned)blocks, threads, 0, st>>>(
-        src, nvec, K, vs, mode, k, q, slices, slice_ld, slice_stride, exps, aux);
+        src, nvec, K, vs, mode, k, q, wide, slices, slice_ld, slice_stride, exps, aux);
     OZ_CHECK_LAUNCH();
   } else {
     exps_tiled_kernel<<<(unsigned)ceil_div(nvec, 32), 256, 0, st>>>(src, nvec, K, vs, ts, mode,
                                                                      exps, aux);
     OZ_CHECK_LAUNCH();
     dim3 grid((unsigned)ceil_div(nvec, 32), (unsigned)ceil_div(slice_ld, 64));
-    slices_tiled_kernel<<<grid, 256, 0, st>>>(src, nvec, K, vs, ts, mode, k, q, slices, slice_ld,
+    slices_tiled_kernel<<<grid, 256, 0, st>>>(src, nvec, K, vs, ts, mode, k, q, wide, slices, slice_ld,
                                               slice_stride, exps, aux);
     OZ_CHECK_LAUNCH();
   }

@@ -151,9 +151,6 @@ class DeviceOps:
         from .solve import _backend_code
         self.code = _backend_code(backend)
         if self.emulated:
-            if backend.slice_bits > 7:
-                from .errors import DeviceError
-                raise DeviceError("slice_bits > 7 (int16 slices) is not supported on the GPU path")
             self.k, self.qbits = backend.splits, backend.slice_bits
             self.pa, self.pb, self.ps = pair_table(backend)
         else:
@@ -170,7 +167,8 @@ class DeviceOps:
         self.ipiv = t.empty((n,), dtype=t.int32, device=dev)
         self.info = t.zeros((1,), dtype=t.int32, device=dev)
         self.bits = t.zeros((2,), dtype=t.int64, device=dev)   # [seen, max|A|] as IEEE bits
-        self.wsb = int(_lib.query("oz_lu_workspace_bytes", n, nb, self.k))
+        self.wsb = int(_lib.query("oz_lu_workspace_bytes", n, nb, self.k, self.qbits))
+        self.planes = 2 * self.k if self.qbits > 7 else self.k   # workspace int8 planes
         self.ws = t.empty((self.wsb,), dtype=t.uint8, device=dev)
         self.tsb = int(_lib.query("oz_lu_solve_workspace_bytes", nb))
         self.tws = t.zeros((self.tsb // 4 + 1,), dtype=t.int32, device=dev)
@@ -208,7 +206,7 @@ class DeviceOps:
 
     # -- factorization steps
     def begin(self) -> None:
-        _lib.call("oz_lu_ws_init", self.ws.data_ptr(), self.wsb, self.n, self.nb, self.k,
+        _lib.call("oz_lu_ws_init", self.ws.data_ptr(), self.wsb, self.n, self.nb, self.planes,
                   self._st())
         self.info.zero_()
         self.bits.zero_()
@@ -219,7 +217,7 @@ class DeviceOps:
     def panel(self, lc: int, j: int, jb: int, slot: int = 0) -> None:
         _lib.call("oz_lu_panel", self._a(lc, j), self.n, self.n - j, jb, j,
                   self.ipiv_buf[slot].data_ptr(), self.info.data_ptr(), self.bits.data_ptr(),
-                  self.ws.data_ptr(), self.wsb, self.n, self.nb, self.k, self._st())
+                  self.ws.data_ptr(), self.wsb, self.n, self.nb, self.planes, self._st())
         # triu of the panel's diagonal block: finalized U rows (solve.py:135-137)
         _lib.call("oz_max_abs_bits", self._a(lc, j), jb, jb, 1, self.n, 1,
                   self.bits.data_ptr(), self._st())
@@ -238,7 +236,7 @@ class DeviceOps:
         (c0a, c1a), (c0b, c1b) = ranges
         _lib.call("oz_laswp", self.slab.data_ptr(), self.n, c0a, c1a, c0b, c1b, j,
                   self.ipiv_buf[slot].data_ptr(), jb, self.ws.data_ptr(), self.wsb, self.n,
-                  self.nb, self.k, self._st())
+                  self.nb, self.planes, self._st())
 
     def trsm_split(self, j: int, jb: int, lstart: int, nt: int, slot: int = 0) -> None:
         """U12 <- L11^-1 A12 on local columns lstart..lstart+nt, then split

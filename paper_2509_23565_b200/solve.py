@@ -177,16 +177,13 @@ def factor_device(a_cm, nb: int, backend: GemmBackend):
     emulated = backend.kind is BackendKind.EMULATED_INT8
     k = backend.splits if emulated else 0
     if emulated:
-        if backend.slice_bits > 7:
-            from .errors import DeviceError
-            raise DeviceError("slice_bits > 7 (int16 slices) is not supported on the GPU path")
         if nb << (2 * backend.slice_bits) >= 1 << 53:
             from .errors import AccumulatorOverflowError
             raise AccumulatorOverflowError("lu_block too large for exact accumulation")
         pa, pb, sh = pair_table(backend)
     else:
         pa = pb = sh = np.zeros(1, dtype=np.int32)
-    ws_bytes = int(_lib.query("oz_lu_workspace_bytes", n, nb, k))
+    ws_bytes = int(_lib.query("oz_lu_workspace_bytes", n, nb, k, backend.slice_bits))
     ws = t.empty((ws_bytes,), dtype=t.uint8, device="cuda")
     ipiv = t.empty((n,), dtype=t.int32, device="cuda")
     stats = t.zeros((4,), dtype=t.float64, device="cuda")

@@ -34,7 +34,10 @@ def test_host_entry_points():
     lib = _lib.load()
     assert lib.oz_version() >= 100
     assert _lib.query("oz_split_aux_bytes") == 16
-    assert _lib.query("oz_lu_workspace_bytes", 4096, 512, 7) > 7 * 4096 * 512
+    assert _lib.query("oz_lu_workspace_bytes", 4096, 512, 7, 7) > 2 * 7 * 4096 * 512
+    # slice_bits > 7: two int8 planes per slice
+    assert (_lib.query("oz_lu_workspace_bytes", 4096, 512, 7, 10)
+            > _lib.query("oz_lu_workspace_bytes", 4096, 512, 14, 7) - 4096)
     ipiv = np.array([2, 2, 3, 3], dtype=np.int32)
     perm = np.empty(4, dtype=np.int64)
     _lib.call("oz_ipiv_to_perm", ipiv.ctypes.data, 4, perm.ctypes.data)
@@ -51,7 +54,7 @@ def _plan(k, inner, q=7):
     _, _, sh = pair_table(GemmBackend.int8(k, q))
     gs = np.zeros(len(sh) + 1, dtype=np.int32)
     gsh = np.zeros(len(sh), dtype=np.int32)
-    ng = _lib.query("oz_plan_groups", len(sh), sh.ctypes.data, inner, gs.ctypes.data,
+    ng = _lib.query("oz_plan_groups", len(sh), sh.ctypes.data, inner, q, gs.ctypes.data,
                     gsh.ctypes.data)
     return ng, gs[:ng + 1], gsh[:ng], sh
 
@@ -85,6 +88,14 @@ def test_grouping_plan_is_exact_and_ordered():
     assert ng7 == 18          # levels 2..6 grouped, levels 7 and 8 per pair
     ng3, _, _, _ = _plan(3, 16384)
     assert ng3 == 3
+    # int16 slices (q = 10): the 53-bit bound uses |slice| <= 1023
+    for k in (3, 5):
+        ng, gs, gsh, sh = _plan(k, 256, q=10)
+        bound = 0.0
+        for g in range(ng):
+            if gs[g + 1] - gs[g] > 1:
+                bound += 256 * 1023.0**2 * (gs[g + 1] - gs[g]) * 2.0 ** -gsh[g]
+                assert bound * 2.0 ** gsh[g] < 2**53
 
 
 def test_pair_tables_match_enumeration():

@@ -136,3 +136,43 @@ def test_gemm_native_close():
     out = oz.gemm(oz.GemmBackend.native(), -1.0, a, b, 1.0, c)
     scale = np.abs(a) @ np.abs(b) + np.abs(c)
     assert (np.abs(out - (c - a @ b)) <= 4 * 2.0**-52 * scale).all()
+
+
+def test_int16_slices_bit_exact():
+    """slice_bits 8..10: the device split (int16 slices as hi/lo int8 planes)
+    and the wide GEMM (exact recombination of the four plane products) are
+    bit-identical to the reference (wide.npz) and to the oracle."""
+    import paper_2509_23565_b200 as oz
+    from oracle import ozaki_oracle as orc
+    g = load_golden("wide")
+    for i in range(int(g["split_count"][0])):
+        k, q, orient = (int(v) for v in g[f"s{i}_meta"])
+        st = oz.split_matrix(g["split_a"], k, q,
+                             oz.Orientation.COL_SCALED if orient else oz.Orientation.ROW_SCALED)
+        assert np.array_equal(np.stack(st.slices), g[f"s{i}_slices"]), i
+        assert np.array_equal(st.exponents, g[f"s{i}_exps"]), i
+    for i in range(int(g["gemm_count"][0])):
+        k, q = (int(v) for v in g[f"g{i}_meta"])
+        out = oz.gemm(oz.GemmBackend.int8(k, q), -1.0, g["gemm_a"], g["gemm_b"], 1.0, g["gemm_c"])
+        assert np.array_equal(out, g[f"g{i}_out"]), (k, q)
+    rng = np.random.default_rng(5)
+    a = rng.random((300, 700)) - 0.5
+    b = rng.random((700, 260)) - 0.5
+    for q, k in ((8, 4), (10, 3), (10, 6)):
+        got = oz.gemm(oz.GemmBackend.int8(k, q), 1.0, a, b, 0.0)
+        assert np.array_equal(got, orc.gemm(1.0, a, b, 0.0, k=k, q=q)), (k, q)
+
+
+def test_int16_slice_lu():
+    import paper_2509_23565_b200 as oz
+    g = load_golden("wide")
+    f = oz.lu_factor(g["lu_a"], 16, oz.GemmBackend.int8(3, 10))
+    assert np.array_equal(f.pivots, g["lu_perm"])
+    assert np.abs(f.lu - g["lu_lu"]).max() <= 2.0**-40
+    from oracle import ozaki_oracle as orc
+    m = oz.hpl_uniform(512, 99)
+    for k in (4, 6):      # 40 vs 60 mantissa bits: same verdict as the reference algorithm
+        _, rep = oz.solve_system(m, m @ np.ones(512), 128, oz.GemmBackend.int8(k, 10))
+        lu, perm, _ = orc.lu_factor(m, 128, k, q=10)
+        ref = orc.residual(m, orc.lu_solve(lu, perm, m @ np.ones(512)), m @ np.ones(512))[0]
+        assert rep.passed == (ref < 16.0) and 0.5 <= rep.scaled_residual / ref <= 2.0, (k, ref)
