@@ -30,7 +30,9 @@ matrix is dealt to the N ranks in 1 x N block-cyclic column blocks, the panel
 owner factors and NCCL-broadcasts each panel and its pivots, every rank
 applies the interchanges and updates its own trailing columns.  Weak scaling
 in memory: n = 32768 * sqrt(N) (rounded to nb) keeps the per-GPU slab fixed;
-value = (2/3) n^3 / max-over-ranks step time for the whole job.
+value = (2/3) n^3 / max-over-ranks step time for the whole job.  The N > 1
+line also carries the D3 GEMM k-sweep row-sharded over the ranks and a
+distributed HPL k-sweep (k = 3..9 + native, with residuals).
 (BENCH_DIST_BACKEND=gloo runs the same path with several ranks on one GPU,
 for testing only.)
 """
@@ -386,6 +388,7 @@ def run_distributed(args, rank, world):
     torch.cuda.empty_cache()
     ks = [int(v) for v in args.sweep_k.split(",") if v.strip()]
     gsweep = gemm_sweep(args.gemm_n, ks, peak, comm=comm) if ks else None
+    lsweep = dist_lu_sweep(args, comm, ks) if ks else None
     if rank != 0:
         return
     gemm_ms, gemm_ops = prof[0], prof[2]
@@ -423,7 +426,42 @@ def run_distributed(args, rank, world):
         "scaled_residual": rep.scaled_residual, "passed": rep.passed, "growth": growth,
         "native_fp64": native, "breakdown_rank0": breakdown,
         "gemm_k_sweep": gsweep,
+        "lu_k_sweep": lsweep,
     }), flush=True)
+
+
+def dist_lu_sweep(args, comm, ks):
+    """The distributed HPL at a moderate order (args.sweep_lu_n * sqrt(N),
+    rounded to nb) for k = 3..9 plus native FP64, one timed run each with its
+    scaled residual (configs[3]/[4] verdicts vs k across the N GPUs)."""
+    import math
+
+    import torch
+
+    import paper_2509_23565_b200 as oz
+    from paper_2509_23565_b200 import hpl
+    nb = args.nb
+    n = int(round(args.sweep_lu_n * math.sqrt(comm.size) / nb)) * nb
+    rows = []
+    for k in list(ks) + [0]:
+        bk = oz.GemmBackend.int8(k) if k else oz.GemmBackend.native()
+        prob = hpl.HplProblem(n, nb, bk, comm=comm)
+        prob.step()                                   # warm
+        torch.cuda.synchronize()
+        comm.barrier()
+        e0, e1 = _events()
+        e0.record()
+        x = prob.step()
+        e1.record()
+        torch.cuda.synchronize()
+        t = comm.allreduce_values([e0.elapsed_time(e1) / 1e3], "max")[0]
+        r = prob.verify(x).scaled_residual
+        rows.append({"k": k if k else "fp64", "ms": t * 1e3, "tflops_fp64_equiv":
+                     flops(n) / t / 1e12, "scaled_residual": r, "passed": r < 16.0})
+        del prob
+        torch.cuda.empty_cache()
+    return {"workload": f"distributed HPL U(-1/2,1/2) n={n} nb={nb}, 1x{comm.size} "
+                        f"block-cyclic, factor+solve", "runs": rows}
 
 
 # ---------------------------------------------------------------- GPU arm
