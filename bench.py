@@ -71,7 +71,19 @@ def parse():
     p.add_argument("--sweep-lu-n", type=int, default=16384, help="LU k-sweep size")
     p.add_argument("--dist-n", type=int, default=0,
                    help="N>1: global order (default n*sqrt(N) rounded to nb: fixed HBM per GPU)")
+    p.add_argument("--grid", default="",
+                   help="N>1: process grid PxQ (default 1xN: panel local to one GPU; P>1 runs "
+                        "hpl2d.py with a distributed panel and cross-rank row swaps)")
     return p.parse_args()
+
+
+def parse_grid(text, world):
+    if not text:
+        return 1, world
+    P, Q = (int(v) for v in text.lower().split("x"))
+    if P * Q != world:
+        raise SystemExit(f"--grid {text} does not match {world} ranks")
+    return P, Q
 
 
 def flops(n):
@@ -321,7 +333,9 @@ def run_distributed(args, rank, world):
     n = args.dist_n or int(round(args.n * math.sqrt(world) / nb)) * nb
     dev = torch.cuda.current_device()
     comm = hpl.Comm()
-    prob = hpl.HplProblem(n, nb, oz.GemmBackend.int8(k), comm=comm)
+    P, Q = parse_grid(args.grid, world)
+    gname = f"{P}x{Q}"
+    prob = hpl.HplProblem(n, nb, oz.GemmBackend.int8(k), comm=comm, grid=(P, Q))
     for _ in range(args.warmup):
         prob.step()
     torch.cuda.synchronize()
@@ -363,12 +377,12 @@ def run_distributed(args, rank, world):
                "h2d_bytes_per_step": int(host_slab.numel() * 8) * world,
                "d2h_bytes_per_step": int(xh.numel() * 8) * world, "ms_per_step": te * 1e3,
                "api": "paper_2509_23565_b200.hpl.HplProblem (slab H2D from pinned host, "
-                      "factor_block_cyclic, solve_block_cyclic, x D2H)"}
+                      "factor, solve, x D2H)"}
     del host_slab
 
     native = None
     if not args.skip_native:
-        nprob = hpl.HplProblem(n, nb, oz.GemmBackend.native(), comm=comm)
+        nprob = hpl.HplProblem(n, nb, oz.GemmBackend.native(), comm=comm, grid=(P, Q))
         nprob.step()
         torch.cuda.synchronize()
         comm.barrier()
@@ -388,7 +402,7 @@ def run_distributed(args, rank, world):
     torch.cuda.empty_cache()
     ks = [int(v) for v in args.sweep_k.split(",") if v.strip()]
     gsweep = gemm_sweep(args.gemm_n, ks, peak, comm=comm) if ks else None
-    lsweep = dist_lu_sweep(args, comm, ks) if ks else None
+    lsweep = dist_lu_sweep(args, comm, ks, (P, Q)) if ks else None
     if rank != 0:
         return
     gemm_ms, gemm_ops = prof[0], prof[2]
@@ -408,9 +422,9 @@ def run_distributed(args, rank, world):
         "data": "synthetic (hpl_uniform(n, 99) generated on device per rank, bit-identical "
                 "to numpy)",
         "config": {"workload": f"configs[3]/[4] shape: distributed HPL LU+solve U(-1/2,1/2) "
-                               f"n={n}, k={k}, 1x{world} block-cyclic, NCCL panel broadcast",
-                   "n": n, "nb": nb, "k": k, "grid": f"1x{world}",
-                   "parallelism": f"block-cyclic 1x{world}",
+                               f"n={n}, k={k}, {gname} block-cyclic, NCCL panel broadcast",
+                   "n": n, "nb": nb, "k": k, "grid": gname,
+                   "parallelism": f"block-cyclic {gname}",
                    "l2": "inputs >> 126 MB L2; no flush needed",
                    "flop_convention": "2/3 n^3 (harness.py:383)",
                    "weak_scaling": "n = n1*sqrt(N): per-GPU slab fixed"},
@@ -430,7 +444,7 @@ def run_distributed(args, rank, world):
     }), flush=True)
 
 
-def dist_lu_sweep(args, comm, ks):
+def dist_lu_sweep(args, comm, ks, grid):
     """The distributed HPL at a moderate order (args.sweep_lu_n * sqrt(N),
     rounded to nb) for k = 3..9 plus native FP64, one timed run each with its
     scaled residual (configs[3]/[4] verdicts vs k across the N GPUs)."""
@@ -445,7 +459,7 @@ def dist_lu_sweep(args, comm, ks):
     rows = []
     for k in list(ks) + [0]:
         bk = oz.GemmBackend.int8(k) if k else oz.GemmBackend.native()
-        prob = hpl.HplProblem(n, nb, bk, comm=comm)
+        prob = hpl.HplProblem(n, nb, bk, comm=comm, grid=grid)
         prob.step()                                   # warm
         torch.cuda.synchronize()
         comm.barrier()
@@ -460,7 +474,7 @@ def dist_lu_sweep(args, comm, ks):
                      flops(n) / t / 1e12, "scaled_residual": r, "passed": r < 16.0})
         del prob
         torch.cuda.empty_cache()
-    return {"workload": f"distributed HPL U(-1/2,1/2) n={n} nb={nb}, 1x{comm.size} "
+    return {"workload": f"distributed HPL U(-1/2,1/2) n={n} nb={nb}, {grid[0]}x{grid[1]} "
                         f"block-cyclic, factor+solve", "runs": rows}
 
 

@@ -185,7 +185,7 @@ int oz_copy2d(const double* src, int64_t rows, int64_t cols, int64_t src_rs, int
 
 /*
  * Step-level LU (the loop of solve.py:94-140 owned by the caller; used by the
- * distributed 1 x Q block-cyclic HPL driver).  All take the LU workspace
+ * distributed block-cyclic HPL drivers, hpl.py and hpl2d.py).  All take the LU workspace
  * (oz_lu_workspace_bytes(ws_n, ws_nb, num_slices, slice_bits) bytes) and its
  * shape; ws_slices counts int8 planes (num_slices, doubled for slice_bits > 7).
  *
@@ -260,6 +260,50 @@ int oz_generate_cyclic(int kind, int64_t n, int64_t depth, int64_t block, double
                        uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                        int64_t nb, int64_t Q, int64_t q, int64_t ncols, double* out,
                        int64_t ldo, void* stream);
+
+/* The same on a P x Q block-cyclic grid: local row lr of process row p is
+ * global row ((lr/nb)*P + p)*nb + lr%nb; mloc local rows, ldo >= mloc. */
+int oz_generate_block_cyclic(int kind, int64_t n, int64_t depth, int64_t block, double alpha,
+                             uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                             uint64_t inc_lo, int64_t nb, int64_t P, int64_t p, int64_t mloc,
+                             int64_t Q, int64_t q, int64_t ncols, double* out, int64_t ldo,
+                             void* stream);
+
+/*
+ * P x Q (P > 1) HPL steps (dpanel.cu).  The panel's rows are spread over the
+ * P ranks of a process column, so each panel column's pivot search is a
+ * candidate exchange: oz_dpanel_candidate writes this rank's record
+ * (3 + 2*jb doubles: max |a[lr0.., t]|, its global row, whether this rank
+ * owns global row g = j + t, that row and row g's panel entries), the caller
+ * all-gathers the P records along the process column (NCCL), and
+ * oz_dpanel_apply picks the same winner on every rank (largest |v|, then
+ * smallest global row = np.argmax order), swaps rows g and the pivot row in
+ * the panel columns, sets ipiv[t] (global row) and *info on a zero pivot,
+ * divides the column below g by the pivot and applies the outer-product
+ * update with separately rounded product and difference (solve.py:75-90).
+ * a is the panel's first column on this rank (local rows, leading dim lda);
+ * lr0 = first local row with global index >= g.
+ *
+ * oz_gather_rows / oz_scatter_rows: copy local rows rows[0..nrows) of
+ * columns [c0a,c1a) U [c0b,c1b) to / from rows buf_rows[0..nrows) (null:
+ * 0..nrows) of buf (column-major, leading dim ldb), for the row
+ * interchanges that cross process rows.
+ * oz_scatter_vec: dst[global(lr0 + i)] = src[i], i < count (row map of p).
+ */
+int oz_dpanel_candidate(const double* a, int64_t lda, int64_t lr0, int64_t mloc, int t, int jb,
+                        int owns_g, int64_t nb, int64_t P, int64_t p, double* rec, void* stream);
+int oz_dpanel_apply(double* a, int64_t lda, int64_t lr0, int64_t mloc, int t, int jb, int64_t g,
+                    int owns_g, int64_t nb, int64_t P, int64_t p, const double* recs,
+                    int32_t* ipiv, int32_t* info, unsigned long long* growth_bits,
+                    void* stream);
+int oz_gather_rows(const double* a, int64_t lda, const int32_t* rows, int64_t nrows, int64_t c0a,
+                   int64_t c1a, int64_t c0b, int64_t c1b, double* buf, const int32_t* buf_rows,
+                   int64_t ldb, void* stream);
+int oz_scatter_rows(double* a, int64_t lda, const int32_t* rows, int64_t nrows, int64_t c0a,
+                    int64_t c1a, int64_t c0b, int64_t c1b, const double* buf,
+                    const int32_t* buf_rows, int64_t ldb, void* stream);
+int oz_scatter_vec(const double* src, int64_t lr0, int64_t count, int64_t nb, int64_t P,
+                   int64_t p, double* dst, void* stream);
 
 #ifdef __cplusplus
 }

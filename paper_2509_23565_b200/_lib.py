@@ -68,6 +68,14 @@ _SIGNATURES = {
     "oz_gemv_partial": [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp],
     "oz_generate_cyclic": [_int, _i64, _i64, _i64, _dbl, _u64, _u64, _u64, _u64, _i64, _i64,
                            _i64, _i64, _vp, _i64, _vp],
+    "oz_generate_block_cyclic": [_int, _i64, _i64, _i64, _dbl, _u64, _u64, _u64, _u64, _i64,
+                                 _i64, _i64, _i64, _i64, _i64, _i64, _vp, _i64, _vp],
+    "oz_dpanel_candidate": [_vp, _i64, _i64, _i64, _int, _int, _int, _i64, _i64, _i64, _vp, _vp],
+    "oz_dpanel_apply": [_vp, _i64, _i64, _i64, _int, _int, _i64, _int, _i64, _i64, _i64, _vp,
+                        _vp, _vp, _vp, _vp],
+    "oz_gather_rows": [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp],
+    "oz_scatter_rows": [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp],
+    "oz_scatter_vec": [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp],
 }
 _RESTYPES = {
     "oz_launch_count": C.c_longlong,

@@ -125,11 +125,13 @@ __global__ void gen_interleaved_kernel(int kind, int64_t n, int64_t d, int64_t b
 __global__ void gen_cyclic_kernel(int kind, int64_t n, int64_t d, int64_t blk, double alpha,
                                   unsigned long long st_hi, unsigned long long st_lo,
                                   unsigned long long inc_hi, unsigned long long inc_lo,
-                                  int64_t nb, int64_t Q, int64_t q, int64_t ncols,
+                                  int64_t nb, int64_t P, int64_t p, int64_t mloc,
+                                  int64_t Q, int64_t q, int64_t ncols,
                                   double* __restrict__ out, int64_t ldo) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t lc0 = (int64_t)blockIdx.y * RUN;
-  if (i >= n) return;
+  if (li >= mloc) return;
+  const int64_t i = ((li / nb) * P + p) * nb + li % nb;
   const int64_t lc1 = min(ncols, lc0 + RUN);
   const u128 inc = ((u128)inc_hi << 64) | inc_lo;
   const u128 s0 = ((u128)st_hi << 64) | st_lo;
@@ -138,35 +140,45 @@ __global__ void gen_cyclic_kernel(int kind, int64_t n, int64_t d, int64_t blk, d
   for (int64_t lc = lc0; lc < lc1; ++lc) {
     const int64_t j = ((lc / nb) * Q + q) * nb + lc % nb;
     if (kind == OZ_GEN_PARAWILK) {
-      out[i + lc * ldo] = pattern(i, j, d, blk, alpha);
+      out[li + lc * ldo] = pattern(i, j, d, blk, alpha);
       continue;
     }
     if (lc == lc0 || lc % nb == 0) s = pcg_advance(s0, inc, (unsigned long long)(i * n + j));
     s = s * m + inc;
-    out[i + lc * ldo] = element(kind, i, j, pcg_double(s), d, blk, alpha);
+    out[li + lc * ldo] = element(kind, i, j, pcg_double(s), d, blk, alpha);
   }
 }
 
 }  // namespace
 }  // namespace oz
 
+extern "C" int oz_generate_block_cyclic(int kind, int64_t n, int64_t depth, int64_t block,
+                                        double alpha, uint64_t state_hi, uint64_t state_lo,
+                                        uint64_t inc_hi, uint64_t inc_lo, int64_t nb, int64_t P,
+                                        int64_t p, int64_t mloc, int64_t Q, int64_t q,
+                                        int64_t ncols, double* out, int64_t ldo, void* stream) {
+  using namespace oz;
+  OZ_REQUIRE(kind >= 0 && kind <= 2, OZ_INVALID_PARAMS, "bad generator kind %d", kind);
+  OZ_REQUIRE(n >= 1 && nb >= 1 && P >= 1 && p >= 0 && p < P && Q >= 1 && q >= 0 && q < Q &&
+                 mloc >= 0 && ldo >= mloc,
+             OZ_INVALID_PARAMS, "bad block-cyclic generator shape");
+  if (ncols <= 0 || mloc <= 0) return OZ_OK;
+  const int64_t d = depth > n - 1 ? n - 1 : depth;
+  dim3 grid((unsigned)ceil_div(mloc, 128), (unsigned)ceil_div(ncols, RUN));
+  gen_cyclic_kernel<<<grid, 128, 0, as_stream(stream)>>>(kind, n, d, block, alpha, state_hi,
+                                                        state_lo, inc_hi, inc_lo, nb, P, p, mloc,
+                                                        Q, q, ncols, out, ldo);
+  OZ_CHECK_LAUNCH();
+  return OZ_OK;
+}
+
 extern "C" int oz_generate_cyclic(int kind, int64_t n, int64_t depth, int64_t block,
                                   double alpha, uint64_t state_hi, uint64_t state_lo,
                                   uint64_t inc_hi, uint64_t inc_lo, int64_t nb, int64_t Q,
                                   int64_t q, int64_t ncols, double* out, int64_t ldo,
                                   void* stream) {
-  using namespace oz;
-  OZ_REQUIRE(kind >= 0 && kind <= 2, OZ_INVALID_PARAMS, "bad generator kind %d", kind);
-  OZ_REQUIRE(n >= 1 && nb >= 1 && Q >= 1 && q >= 0 && q < Q && ldo >= n, OZ_INVALID_PARAMS,
-             "bad block-cyclic generator shape");
-  if (ncols <= 0) return OZ_OK;
-  const int64_t d = depth > n - 1 ? n - 1 : depth;
-  dim3 grid((unsigned)ceil_div(n, 128), (unsigned)ceil_div(ncols, RUN));
-  gen_cyclic_kernel<<<grid, 128, 0, as_stream(stream)>>>(kind, n, d, block, alpha, state_hi,
-                                                        state_lo, inc_hi, inc_lo, nb, Q, q, ncols,
-                                                        out, ldo);
-  OZ_CHECK_LAUNCH();
-  return OZ_OK;
+  return oz_generate_block_cyclic(kind, n, depth, block, alpha, state_hi, state_lo, inc_hi,
+                                  inc_lo, nb, 1, 0, n, Q, q, ncols, out, ldo, stream);
 }
 
 extern "C" int oz_generate(int kind, int64_t n, int64_t depth, int64_t block, double alpha,

@@ -105,6 +105,23 @@ class Comm:
             return None
         return self.dist.broadcast(t, self._grank(src), group=self.group, async_op=True)
 
+    def allgather(self, t):
+        """-> (size, *t.shape) tensor of every rank's t, on t's device."""
+        import torch
+        if self.size == 1:
+            return t.reshape((1,) + tuple(t.shape))
+        if self.stage and t.is_cuda:
+            parts = [torch.empty_like(t, device="cpu") for _ in range(self.size)]
+            self.dist.all_gather(parts, t.cpu(), group=self.group)
+            return torch.stack(parts).to(t.device)
+        if not t.is_cuda:
+            parts = [torch.empty_like(t) for _ in range(self.size)]
+            self.dist.all_gather(parts, t, group=self.group)
+            return torch.stack(parts)
+        out = torch.empty((self.size,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        self.dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
+        return out
+
     def allreduce(self, t, op: str) -> None:
         if self.size == 1:
             return
@@ -446,23 +463,40 @@ def _residual(ops, comm, n, nb, x, b):
 class HplProblem:
     """One distributed HPL problem kept resident: the generated matrix (a
     pristine copy of every rank's slab), the replicated b = A @ 1, and the
-    buffers of the factorization.  ``step()`` = restore + factor + solve."""
+    buffers of the factorization.  ``step()`` = restore + factor + solve.
+    grid = (P, Q) with P * Q = world size; P = 1 (default) runs the 1 x Q
+    driver of this module, P > 1 the 2-D driver of hpl2d.py."""
 
     def __init__(self, n: int, nb: int, backend: GemmBackend | None = None, *,
                  matrix: str = "uniform", seed: int = 99, depth: int = 4, block: int = 15,
-                 alpha: float = 0.5, comm: Comm | None = None, ops: DeviceOps | None = None):
+                 alpha: float = 0.5, comm: Comm | None = None, ops=None,
+                 grid: tuple[int, int] | None = None):
         from .matgen import GEN_PARAWILK_RANDOMIZED, GEN_UNIFORM
         self.backend = backend or GemmBackend.native()
         self.comm = comm or Comm()
         if not 1 <= nb <= min(n, 1024):
             raise InvalidParamsError(f"nb must be in 1..{min(n, 1024)}, got {nb}")
-        self.n, self.nb = n, nb
-        self.ops = ops or DeviceOps(n, nb, self.comm.size, self.comm.rank, self.backend)
+        P, Q = grid if grid is not None else (1, self.comm.size)
+        if P < 1 or Q < 1 or P * Q != self.comm.size:
+            raise InvalidParamsError(f"grid {P}x{Q} does not match {self.comm.size} ranks")
+        self.n, self.nb, self.P, self.Q = n, nb, P, Q
+        self.grid = None
+        if P > 1:
+            from .hpl2d import DeviceOps2D, Grid
+            self.grid = Grid(P, Q, self.comm)
+            self.ops = ops or DeviceOps2D(n, nb, P, Q, self.grid.p, self.grid.q, self.backend)
+        else:
+            self.ops = ops or DeviceOps(n, nb, self.comm.size, self.comm.rank, self.backend)
         self.gen = (GEN_UNIFORM if matrix == "uniform" else GEN_PARAWILK_RANDOMIZED, seed, depth,
                     block, alpha)
         self.ops.generate(*self.gen)
-        self.b = _replicated_rhs(self.ops, self.comm)
-        self.a0 = self.ops.slab.clone() if isinstance(self.ops, DeviceOps) else None
+        if self.grid is not None:
+            from .hpl2d import rhs_2d
+            self.b = rhs_2d(self.ops, self.grid)
+        else:
+            self.b = _replicated_rhs(self.ops, self.comm)
+        self.a0 = self.ops.slab.clone() if hasattr(self.ops, "slab") and \
+            hasattr(self.ops.slab, "clone") else None
         self.growth = None
 
     def restore(self) -> None:
@@ -471,11 +505,24 @@ class HplProblem:
         else:
             self.ops.generate(*self.gen)
 
-    def factor_solve(self):
+    def factor(self):
+        if self.grid is not None:
+            from .hpl2d import factor_2d
+            ipiv, self.growth = factor_2d(self.ops, self.grid, self.n, self.nb)
+        else:
+            ipiv, self.growth = factor_block_cyclic(self.ops, self.comm, self.n, self.nb)
+        return ipiv
+
+    def solve(self, ipiv):
         from .solve import ipiv_to_perm
-        ipiv, self.growth = factor_block_cyclic(self.ops, self.comm, self.n, self.nb)
-        return solve_block_cyclic(self.ops, self.comm, self.n, self.nb, ipiv_to_perm(ipiv),
-                                  self.b.cpu().numpy())
+        perm, bh = ipiv_to_perm(ipiv), self.b.cpu().numpy()
+        if self.grid is not None:
+            from .hpl2d import solve_2d
+            return solve_2d(self.ops, self.grid, self.n, self.nb, perm, bh)
+        return solve_block_cyclic(self.ops, self.comm, self.n, self.nb, perm, bh)
+
+    def factor_solve(self):
+        return self.solve(self.factor())
 
     def step(self):
         self.restore()
@@ -483,34 +530,38 @@ class HplProblem:
 
     def verify(self, x):
         self.restore()
+        if self.grid is not None:
+            from .hpl2d import residual_2d
+            return residual_2d(self.ops, self.grid, self.n, self.nb, x, self.b)
         return _residual(self.ops, self.comm, self.n, self.nb, x, self.b)
 
 
 def hpl_run(n: int, nb: int, backend: GemmBackend | None = None, *, matrix: str = "uniform",
             seed: int = 99, depth: int = 4, block: int = 15, alpha: float = 0.5,
-            comm: Comm | None = None, ops: DeviceOps | None = None) -> HplReport:
+            comm: Comm | None = None, ops=None, grid: tuple[int, int] | None = None) -> HplReport:
     """Generate the matrix distributed (hpl_uniform or randomized ParaWilk,
-    matgen.py:149-171), b = A @ 1, factor, solve and verify.  Times factor and
-    solve with device events, max over ranks."""
+    matgen.py:149-171), b = A @ 1, factor, solve and verify on a P x Q grid
+    (default 1 x world).  Times factor and solve with device events, max over
+    ranks."""
     import torch
     prob = HplProblem(n, nb, backend, matrix=matrix, seed=seed, depth=depth, block=block,
-                      alpha=alpha, comm=comm, ops=ops)
+                      alpha=alpha, comm=comm, ops=ops, grid=grid)
     comm, backend = prob.comm, prob.backend
     prob.restore()
     comm.barrier()
     torch.cuda.synchronize()
     e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
     e0.record()
-    from .solve import ipiv_to_perm
-    ipiv, growth = factor_block_cyclic(prob.ops, comm, n, nb)
+    ipiv = prob.factor()
+    growth = prob.growth
     e1.record()
-    x = solve_block_cyclic(prob.ops, comm, n, nb, ipiv_to_perm(ipiv), prob.b.cpu().numpy())
+    x = prob.solve(ipiv)
     e2.record()
     torch.cuda.synchronize()
     tf, ts = comm.allreduce_values([e0.elapsed_time(e1) / 1e3, e1.elapsed_time(e2) / 1e3],
                                    "max")
     rep = prob.verify(x)
-    return HplReport(n=n, nb=nb, grid=f"1x{comm.size}", backend=backend.describe(),
+    return HplReport(n=n, nb=nb, grid=f"{prob.P}x{prob.Q}", backend=backend.describe(),
                      scaled_residual=rep.scaled_residual, raw_residual_inf=rep.raw_residual_inf,
                      norm_a_inf=rep.norm_a_inf, norm_x_inf=rep.norm_x_inf,
                      norm_b_inf=rep.norm_b_inf, growth=growth, seconds_factor=tf,

@@ -129,3 +129,165 @@ class NumpyOps:
 
     def zero_diag(self):
         return self.flag
+
+
+class NumpyOps2D:
+    """The same stand-in for hpl2d.DeviceOps2D (P x Q grid): local rows x
+    local columns of the oracle's matrix; every operation restates the
+    oracle on those blocks (dpanel.cu's column step = solve.py:75-90)."""
+
+    def __init__(self, a_full: np.ndarray, nb: int, P: int, Q: int, p: int, q: int,
+                 k: int | None):
+        from paper_2509_23565_b200.hpl2d import global_rows
+        self.n = a_full.shape[0]
+        self.nb, self.P, self.Q, self.p, self.q, self.k = nb, P, Q, p, q, k
+        self.full = a_full
+        self.grows = global_rows(self.n, nb, P, p)
+        self.gcols = global_rows(self.n, nb, Q, q)
+        self.mloc, self.ncl = len(self.grows), len(self.gcols)
+        self.slab = np.asfortranarray(a_full[np.ix_(self.grows, self.gcols)])
+        self.pbuf = torch.zeros(max(self.mloc, 1) * nb, dtype=torch.float64)
+        self.ubuf = torch.zeros(nb * max(self.ncl, 1), dtype=torch.float64)
+        self.ipiv_buf = torch.zeros(nb, dtype=torch.int32)
+        self.ipiv = np.zeros(self.n, dtype=np.int32)
+        self.flag = 0
+
+    def generate(self, *args, **kw):
+        self.slab = np.asfortranarray(self.full[np.ix_(self.grows, self.gcols)])
+
+    def vector(self, host=None, n=None):
+        if host is None:
+            return torch.zeros(n, dtype=torch.float64)
+        return torch.from_numpy(np.array(host, dtype=np.float64))
+
+    def row_partials(self, x_local=None):
+        x = np.ones(self.ncl) if x_local is None else x_local.numpy()
+        ax, asum = np.zeros(self.n), np.zeros(self.n)
+        ax[self.grows] = self.slab @ x if self.ncl else 0.0
+        asum[self.grows] = np.abs(self.slab).sum(axis=1)
+        return torch.from_numpy(ax), torch.from_numpy(asum)
+
+    def begin(self):
+        self.info = 0
+        self.seen = 0.0
+        self.top = float(np.abs(self.slab).max()) if self.slab.size else 0.0
+
+    def dpanel_candidate(self, lc, lr0, t, jb, owns_g):
+        rec = np.zeros(3 + 2 * jb)
+        col = self.slab[lr0:, lc + t]
+        if col.size == 0:
+            rec[0] = rec[1] = -1.0
+        else:
+            i = int(np.argmax(np.abs(col)))
+            rec[0], rec[1] = abs(col[i]), self.grows[lr0 + i]
+            rec[3:3 + jb] = self.slab[lr0 + i, lc:lc + jb]
+        rec[2] = 1.0 if owns_g else 0.0
+        if owns_g:
+            rec[3 + jb:] = self.slab[lr0, lc:lc + jb]
+        return torch.from_numpy(rec)
+
+    def dpanel_apply(self, lc, lr0, t, jb, g, owns_g, recs):
+        r = recs.numpy()
+        w = 0
+        for i in range(1, r.shape[0]):
+            if r[i, 0] > r[w, 0] or (r[i, 0] == r[w, 0] >= 0 and r[i, 1] < r[w, 1]):
+                w = i
+        rw = r[w]
+        rg = r[int(np.nonzero(r[:, 2])[0][0])]
+        piv = int(rw[1])
+        self.ipiv_buf[t] = piv
+        if rw[3 + t] == 0.0 and not self.info:
+            self.info = g + 1
+        a = self.slab
+        if piv != g:
+            if owns_g:
+                a[lr0, lc:lc + jb] = rw[3:3 + jb]
+            if (piv // self.nb) % self.P == self.p:
+                lrp = ((piv // self.nb) // self.P) * self.nb + piv % self.nb
+                a[lrp, lc:lc + jb] = rg[3 + jb:]
+        r0 = lr0 + (1 if owns_g else 0)
+        pv = rw[3 + t]
+        if pv != 0.0 and r0 < self.mloc:
+            a[r0:, lc + t] /= pv
+            if t + 1 < jb:
+                a[r0:, lc + t + 1:lc + jb] -= np.outer(a[r0:, lc + t], rw[3 + t + 1:3 + jb])
+                self.seen = max(self.seen, float(np.abs(a[r0:, lc + t + 1:lc + jb]).max()))
+
+    def panel_finish(self, lc, lr_j, jb, diag):
+        if diag:
+            self.seen = max(self.seen, float(np.abs(np.triu(
+                self.slab[lr_j:lr_j + jb, lc:lc + jb])).max()))
+        m = self.mloc - lr_j
+        if m > 0:
+            self.pbuf[:m * jb] = torch.from_numpy(
+                self.slab[lr_j:, lc:lc + jb].ravel(order="F").copy())
+
+    def panel_buffers(self, lr_j, jb):
+        return self.pbuf[:(self.mloc - lr_j) * jb], self.ipiv_buf[:jb]
+
+    def record_pivots(self, j, jb):
+        self.ipiv[j:j + jb] = self.ipiv_buf[:jb].numpy()
+        return self.ipiv[j:j + jb].copy()
+
+    @staticmethod
+    def _cols(ranges):
+        return np.r_[ranges[0][0]:ranges[0][1], ranges[1][0]:ranges[1][1]].astype(np.int64)
+
+    def gather_rows(self, lrows, ranges):
+        blk = self.slab[np.ix_(np.asarray(lrows), self._cols(ranges))]
+        return torch.from_numpy(blk.ravel(order="F").copy())
+
+    def rows_buffer(self, nrows, ranges):
+        return torch.zeros(nrows * len(self._cols(ranges)), dtype=torch.float64)
+
+    def scatter_rows(self, lrows, ranges, buf, brows, ldb):
+        if len(lrows) == 0:
+            return
+        cols = self._cols(ranges)
+        b = buf.numpy().reshape((len(cols), ldb)).T
+        self.slab[np.ix_(np.asarray(lrows), cols)] = b[np.asarray(brows), :]
+
+    def _pan(self, lr_j, jb):
+        m = self.mloc - lr_j
+        return self.pbuf[:m * jb].numpy().reshape((jb, m)).T
+
+    def trsm(self, lr_j, jb, lstart, nt):
+        pan = self._pan(lr_j, jb)
+        u12 = solve_triangular(pan[:jb, :jb], self.slab[lr_j:lr_j + jb, lstart:lstart + nt],
+                               lower=True, unit_diagonal=True, check_finite=False)
+        self.slab[lr_j:lr_j + jb, lstart:lstart + nt] = u12
+        self.seen = max(self.seen, float(np.abs(u12).max()))
+        self.ubuf[:jb * nt] = torch.from_numpy(u12.ravel(order="F").copy())
+
+    def ubuf_view(self, jb, nt):
+        return self.ubuf[:jb * nt]
+
+    def schur(self, lr_j, jb, skip, lstart, nt):
+        mr = self.mloc - lr_j - skip
+        if mr <= 0 or nt <= 0:
+            return
+        l21 = self._pan(lr_j, jb)[skip:, :]
+        u12 = self.ubuf[:jb * nt].numpy().reshape((nt, jb)).T
+        cols = slice(lstart, lstart + nt)
+        rows = slice(lr_j + skip, self.mloc)
+        self.slab[rows, cols] = orc.gemm(-1.0, l21, u12, 1.0, self.slab[rows, cols], k=self.k)
+        self.seen = max(self.seen, float(np.abs(self.slab[rows, cols]).max()))
+
+    def finish(self):
+        return self.ipiv.copy(), self.info, self.seen, self.top
+
+    def trsv(self, lr, lc, jb, upper, x, j):
+        blk = self.slab[lr:lr + jb, lc:lc + jb]
+        if upper and np.any(np.diag(blk) == 0.0):
+            self.flag = 1
+            return
+        xs = x[j:j + jb].numpy()
+        xs[:] = solve_triangular(blk, xs, lower=not upper, unit_diagonal=not upper,
+                                 check_finite=False)
+
+    def gemv_rows(self, lr0, lr1, lc, jb, x, j, out):
+        if lr1 > lr0:
+            out.numpy()[self.grows[lr0:lr1]] = self.slab[lr0:lr1, lc:lc + jb] @ x.numpy()[j:j + jb]
+
+    def zero_diag(self):
+        return self.flag
