@@ -98,13 +98,16 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 // candidate record: [0] |v| (double), [1] pos (low 32) | tag (high 32), [2] physical
 // row, [4..4+w) row values.  Data first, tag last (release store).
 
+constexpr int STAGE_G = 16;  // grids up to this size read every record in one round trip
+
 struct PanelShared {
   double red_a[PANEL_WARPS];
   int red_p[PANEL_WARPS];
   int red_r[PANEL_WARPS];
   int occ[PANEL_W];
   int prow[PANEL_W];
-  double urow[PANEL_W];
+  double urow[2][PANEL_W];  // pivot rows of steps t (buf) and t-1 (buf ^ 1)
+  double stage[STAGE_G][CAND_STRIDE];
   int best;
 };
 
@@ -159,8 +162,11 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
   }
 
   long long _tp = clock64();
+  const bool staged = gridDim.x <= STAGE_G;
   for (int t = 0; t < w; ++t) {
     const int buf = t & 1;
+    double* urow = sh.urow[buf];
+    const double* uprev = sh.urow[buf ^ 1];
     // ---- block argmax of the thread candidates (np.argmax order)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -195,11 +201,20 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
         }
       }
       br = __shfl_sync(0xffffffffu, br, 0);
-      // ---- publish the CTA's candidate record, then arrive on the step counter
+      // ---- publish the CTA's candidate record, then arrive on the step counter.
+      // Step t-1's update of columns > t is deferred (below), so the
+      // candidate row's values there are formed here with the same
+      // product-then-subtract the deferred update will store.
       double* rec = p.cand + ((size_t)buf * gridDim.x + blockIdx.x) * CAND_STRIDE;
       long long* irec = reinterpret_cast<long long*>(rec);
-      if (br >= 0)
-        for (int c = t + lane; c < w; c += 32) rec[4 + c] = sm[c * R + br];
+      if (br >= 0) {
+        const double lp = t > 0 ? sm[(t - 1) * R + br] : 0.0;
+        for (int c = t + lane; c < w; c += 32) {
+          double v = sm[c * R + br];
+          if (t > 0 && c > t) v = __dsub_rn(v, __dmul_rn(lp, uprev[c]));
+          rec[4 + c] = v;
+        }
+      }
       if (lane == 0) {
         rec[0] = br >= 0 ? fabs(sm[t * R + br]) : -1.0;
         irec[1] = br >= 0 ? pos[br] : 0x7fffffff;
@@ -210,35 +225,79 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
       __syncwarp();
       if (lane == 0) red_release_add(&p.bar->count, 1u);
       if (p.dbg && lane == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 0, (unsigned long long)(_n - _tp)); _tp = _n; }
-      // ---- wait for all CTAs (counter reaches G*(t+1)), reduce all records
-      if (lane == 0) {
-        const unsigned target = gridDim.x * (unsigned)(t + 1);
-        while (ld_acquire_u32(&p.bar->count) < target) {
+    }
+    __syncthreads();  // the publish above read row br before the deferred update below
+    // ---- while the other CTAs arrive: step t-1's update of columns t+1..w-1
+    //      (column t was updated before the argmax).  pos[] is unchanged
+    //      since that step, so the same rows are updated.
+    if (t > 0) {
+      for (int r = tid; r < nloc; r += PANEL_THREADS) {
+        if (pos[r] < 0) continue;
+        const double l = sm[(t - 1) * R + r];
+#pragma unroll 4
+        for (int c = t + 1; c < w; ++c) {
+          const double x = __dsub_rn(sm[c * R + r], __dmul_rn(l, uprev[c]));
+          sm[c * R + r] = x;
+          gmax = fmax(gmax, fabs(x));
         }
       }
-      __syncwarp();
-      if (p.dbg && lane == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 1, (unsigned long long)(_n - _tp)); _tp = _n; }
-      constexpr int PER = 5;  // up to 160 CTAs
-      double av[PER];
-      long long pk[PER];
-#pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        const int g = lane + 32 * i;
-        const double* cr_ = p.cand + ((size_t)buf * gridDim.x + g) * CAND_STRIDE;
-        av[i] = g < (int)gridDim.x ? __ldcg(cr_) : -2.0;
-        pk[i] = g < (int)gridDim.x ? __ldcg(reinterpret_cast<const long long*>(cr_) + 1)
-                                   : 0x7fffffffll;
+    }
+    // ---- wait for all CTAs (counter reaches G*(t+1))
+    if (tid == 0) {
+      const unsigned target = gridDim.x * (unsigned)(t + 1);
+      while (ld_acquire_u32(&p.bar->count) < target) {
       }
-      ba = -2.0;
-      bp = 0x7fffffff;
-      int bg = 0;
+    }
+    __syncthreads();
+    if (p.dbg && tid == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 1, (unsigned long long)(_n - _tp)); _tp = _n; }
+    const double* recs = p.cand + (size_t)buf * gridDim.x * CAND_STRIDE;
+    if (staged) {
+      // small grids: the whole record array in one round trip, all threads
+      constexpr int LOADS = (STAGE_G * CAND_STRIDE + PANEL_THREADS - 1) / PANEL_THREADS;
+      const int total = (int)gridDim.x * CAND_STRIDE;
+      double v[LOADS];
 #pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        if (lane + 32 * i >= (int)gridDim.x) continue;
-        if (better(av[i], (int)pk[i], ba, bp)) {
-          ba = av[i];
-          bp = (int)pk[i];
-          bg = lane + 32 * i;
+      for (int i = 0; i < LOADS; ++i) {
+        const int e = tid + i * PANEL_THREADS;
+        v[i] = e < total ? __ldcg(recs + e) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < LOADS; ++i) {
+        const int e = tid + i * PANEL_THREADS;
+        if (e < total) (&sh.stage[0][0])[e] = v[i];
+      }
+      __syncthreads();
+    }
+    if (wid == 0) {
+      double ba = -2.0;
+      int bp = 0x7fffffff;
+      int bg = 0;
+      if (staged) {
+        if (lane < (int)gridDim.x) {
+          ba = sh.stage[lane][0];
+          bp = (int)reinterpret_cast<const long long*>(sh.stage[lane])[1];
+          bg = lane;
+        }
+      } else {
+        constexpr int PER = 5;  // up to 160 CTAs
+        double av[PER];
+        long long pk[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+          const int g = lane + 32 * i;
+          const double* cr_ = recs + (size_t)g * CAND_STRIDE;
+          av[i] = g < (int)gridDim.x ? __ldcg(cr_) : -2.0;
+          pk[i] = g < (int)gridDim.x ? __ldcg(reinterpret_cast<const long long*>(cr_) + 1)
+                                     : 0x7fffffffll;
+        }
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+          if (lane + 32 * i >= (int)gridDim.x) continue;
+          if (better(av[i], (int)pk[i], ba, bp)) {
+            ba = av[i];
+            bp = (int)pk[i];
+            bg = lane + 32 * i;
+          }
         }
       }
 #pragma unroll
@@ -254,16 +313,18 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
       }
       if (p.dbg && lane == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 2, (unsigned long long)(_n - _tp)); _tp = _n; }
       // ---- winner's row (the new U row) and interchange bookkeeping
-      const double* win = p.cand + ((size_t)buf * gridDim.x + bg) * CAND_STRIDE;
-      for (int c = t + lane; c < w; c += 32) sh.urow[c] = __ldcg(win + 4 + c);
+      const double* win = staged ? sh.stage[bg] : recs + (size_t)bg * CAND_STRIDE;
+      for (int c = t + lane; c < w; c += 32) urow[c] = staged ? win[4 + c] : __ldcg(win + 4 + c);
       if (lane == 0) {
-        const int ppos = (int)__ldcg(reinterpret_cast<const long long*>(win) + 1);
-        const int64_t prow = __ldcg(reinterpret_cast<const long long*>(win) + 2);
+        const int ppos = staged ? (int)reinterpret_cast<const long long*>(win)[1]
+                                : (int)__ldcg(reinterpret_cast<const long long*>(win) + 1);
+        const int64_t prow = staged ? reinterpret_cast<const long long*>(win)[2]
+                                    : __ldcg(reinterpret_cast<const long long*>(win) + 2);
+        const double pv = staged ? win[4 + t] : __ldcg(win + 4 + t);
         const int rt = sh.occ[t];  // relative physical row currently at position t
-        const double piv = __ldcg(win + 4 + t);
         if (blockIdx.x == 0) {
           p.ipiv[p.r0 + t] = (int32_t)(p.base + p.r0 + ppos);
-          if (piv == 0.0)
+          if (pv == 0.0)
             atomicCAS(reinterpret_cast<int*>(p.info), 0, (int)(p.base + p.r0 + t + 1));
           sh.prow[t] = (int)prow;
         }
@@ -278,10 +339,10 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
       if (p.dbg && lane == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 3, (unsigned long long)(_n - _tp)); _tp = _n; }
     }
     __syncthreads();
-    // ---- column scaling by DIVISION (solve.py:84) and rank-1 update (:86) as
-    //      product-then-subtract (np.outer then -=); the next column's
-    //      candidate is tracked on the fly
-    const double piv = sh.urow[t];
+    // ---- column scaling by DIVISION (solve.py:84) and the rank-1 update
+    //      (:86, np.outer then -=) of column t+1 only, tracking the next
+    //      column's candidate; columns t+2.. follow after the next publish
+    const double piv = urow[t];
     ca = -1.0;
     cp = 0x7fffffff;
     cr = -1;
@@ -290,9 +351,9 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
       if (pr < 0) continue;
       const double l = sm[t * R + r] / piv;
       sm[t * R + r] = l;
-      int c = t + 1;
+      const int c = t + 1;
       if (c < w) {
-        const double x = __dsub_rn(sm[c * R + r], __dmul_rn(l, sh.urow[c]));
+        const double x = __dsub_rn(sm[c * R + r], __dmul_rn(l, urow[c]));
         sm[c * R + r] = x;
         const double ax = fabs(x);
         gmax = fmax(gmax, ax);
@@ -301,12 +362,6 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
           cp = pr;
           cr = r;
         }
-      }
-#pragma unroll 4
-      for (c = t + 2; c < w; ++c) {
-        const double x = __dsub_rn(sm[c * R + r], __dmul_rn(l, sh.urow[c]));
-        sm[c * R + r] = x;
-        gmax = fmax(gmax, fabs(x));
       }
     }
     if (p.dbg && tid == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 5, (unsigned long long)(_n - _tp)); _tp = _n; }
