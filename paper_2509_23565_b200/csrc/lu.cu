@@ -583,6 +583,95 @@ __global__ void __launch_bounds__(TRSM_COLS) trsm_unit_lower_kernel(
 }
 constexpr size_t TRSM_SMEM = sizeof(double) * (TRSM_W * TRSM_W + TRSM_W * TRSM_COLS);
 
+// Whole-panel forward substitution in one launch: B[0:jb, c] <- L^{-1} B[0:jb, c]
+// for NC columns per CTA, L unit lower jb x jb (jb <= 1024).  The CTA keeps its
+// jb x NC block of B in shared memory and walks the 64-row diagonal blocks:
+// a warp solves each column of the diagonal block (lanes = rows, x_k broadcast
+// by shuffle), then all threads update the rows below, each row's NC values in
+// registers and every L element read once per CTA.  Per element the order is
+// the sequential forward substitution, b_r = fma(-l_rk, x_k, b_r) for k = 0, 1,
+// ..., so the result does not depend on how the columns are partitioned.
+constexpr int TRSMF_THREADS = 256;
+constexpr int TRSMF_MAXJB = 1024;
+template <int NC>
+__global__ void __launch_bounds__(TRSMF_THREADS) trsm_fused_kernel(
+    const double* __restrict__ L, int64_t ldl, int jb, double* __restrict__ B, int64_t ldb,
+    int64_t ncols) {
+  extern __shared__ double dsm[];
+  double* sB = dsm;                          // [jb][NC]
+  double* sD = dsm + (size_t)jb * NC;        // [64][65] diagonal block, row-major
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * NC;
+  const int nc = (int)(ncols - c0 < NC ? ncols - c0 : NC);
+  // loads batched (unrolled) so each thread keeps several L2/HBM requests in flight
+#pragma unroll 8
+  for (int i = tid; i < jb * NC; i += TRSMF_THREADS) {
+    const int c = i / jb, r = i - c * jb;
+    sB[r * NC + c] = c < nc ? B[(c0 + c) * ldb + r] : 0.0;
+  }
+  for (int r0 = 0; r0 < jb; r0 += TRSM_W) {
+    const int w = jb - r0 < TRSM_W ? jb - r0 : TRSM_W;
+    constexpr int DL = TRSM_W * TRSM_W / TRSMF_THREADS;
+    double dv[DL];
+#pragma unroll
+    for (int u = 0; u < DL; ++u) {
+      const int i = tid + u * TRSMF_THREADS;
+      const int c = i / TRSM_W, r = i - c * TRSM_W;
+      dv[u] = (r < w && c < w && r > c) ? L[(r0 + c) * ldl + r0 + r] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < DL; ++u) {
+      const int i = tid + u * TRSMF_THREADS;
+      const int c = i / TRSM_W, r = i - c * TRSM_W;
+      sD[r * (TRSM_W + 1) + c] = dv[u];
+    }
+    __syncthreads();
+    for (int c = wid; c < NC; c += TRSMF_THREADS / 32) {
+      double v0 = lane < w ? sB[(r0 + lane) * NC + c] : 0.0;
+      double v1 = lane + 32 < w ? sB[(r0 + lane + 32) * NC + c] : 0.0;
+      for (int k = 0; k < w; ++k) {
+        const double xk = __shfl_sync(0xffffffffu, k < 32 ? v0 : v1, k & 31);
+        if (lane > k) v0 = fma(-sD[lane * (TRSM_W + 1) + k], xk, v0);
+        if (lane + 32 > k) v1 = fma(-sD[(lane + 32) * (TRSM_W + 1) + k], xk, v1);
+      }
+      if (lane < w) sB[(r0 + lane) * NC + c] = v0;
+      if (lane + 32 < w) sB[(r0 + lane + 32) * NC + c] = v1;
+    }
+    __syncthreads();
+    for (int r = r0 + w + tid; r < jb; r += TRSMF_THREADS) {
+      double b[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) b[c] = sB[r * NC + c];
+      const double* lr = L + (int64_t)r0 * ldl + r;
+      // 16 L loads in flight per thread before their FMAs (L2 latency)
+      for (int k0 = 0; k0 < w; k0 += 16) {
+        double l[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) l[u] = k0 + u < w ? __ldg(lr + (int64_t)(k0 + u) * ldl) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          if (k0 + u < w) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) b[c] = fma(-l[u], sB[(r0 + k0 + u) * NC + c], b[c]);
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) sB[r * NC + c] = b[c];
+    }
+    __syncthreads();
+  }
+#pragma unroll 8
+  for (int i = tid; i < jb * NC; i += TRSMF_THREADS) {
+    const int c = i / jb, r = i - c * jb;
+    if (c < nc) B[(c0 + c) * ldb + r] = sB[r * NC + c];
+  }
+}
+template <int NC>
+constexpr size_t trsmf_smem(int jb) {
+  return sizeof(double) * ((size_t)jb * NC + TRSM_W * (TRSM_W + 1));
+}
+
 // --------------------------------------------------------------- reductions
 __global__ void max_abs_kernel(const double* __restrict__ a, int64_t m, int64_t n, int64_t rs,
                                int64_t cs, int upper_only, int64_t diag_off,
@@ -841,9 +930,36 @@ int apply_list(double* a, int64_t lda, const LuWs& ws, int64_t c0a, int64_t c1a,
 }
 
 // U12 <- L11^{-1} A12 for L11 (jb x jb, unit lower) at a[j,j], A12 = rows j..j+jb, ncols
+template <int NC>
+int trsm_fused(const double* L, int64_t lda, int64_t jb, double* b, int64_t ldb, int64_t ncols,
+               cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    OZ_CHECK_CUDA(cudaFuncSetAttribute(trsm_fused_kernel<NC>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)trsmf_smem<NC>(TRSMF_MAXJB)));
+    attr = true;
+  }
+  trsm_fused_kernel<NC><<<(unsigned)ceil_div(ncols, NC), TRSMF_THREADS, trsmf_smem<NC>((int)jb),
+                          st>>>(L, lda, (int)jb, b, ldb, ncols);
+  OZ_CHECK_LAUNCH();
+  return OZ_OK;
+}
+
 int trsm_blocked(double* a, int64_t lda, int64_t j, int64_t jb, double* b, int64_t ldb,
                  int64_t ncols, cudaStream_t st) {
   if (ncols <= 0) return OZ_OK;
+  static const bool legacy = getenv("OZ_TRSM_LEGACY") != nullptr;
+  // few right-hand sides (the look-ahead's next panel, the recursion inside a
+  // panel): one launch, latency-bound (~0.3 ms at jb = 1024 vs ~0.5 ms for the
+  // 2*jb/64 launches below); wide updates: diagonal blocks + cuBLAS DGEMM,
+  // FP64-throughput-bound (15 vs 5 TFLOP/s at 30720 columns)
+  if (!legacy && jb <= TRSMF_MAXJB && ncols <= 2048) {
+    const int tag = prof_start(st);
+    const int s = trsm_fused<8>(a + j * lda + j, lda, jb, b, ldb, ncols, st);
+    prof_stop(tag, st, PROF_TRSM, (double)jb * jb * ncols);
+    return s;
+  }
   static bool attr = false;
   if (!attr) {
     OZ_CHECK_CUDA(cudaFuncSetAttribute(trsm_unit_lower_kernel,
