@@ -305,6 +305,10 @@ int oz_scatter_rows(double* a, int64_t lda, const int32_t* rows, int64_t nrows, 
 int oz_scatter_vec(const double* src, int64_t lr0, int64_t count, int64_t nb, int64_t P,
                    int64_t p, double* dst, void* stream);
 
+/* Tuning only: with OZ_GEMM_STARTS=1 in the environment every emulated-GEMM
+ * launch logs its CTAs' start/end times; this prints the spreads to stderr. */
+int oz_gemm_starts_dump(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -95,14 +95,18 @@ static cublasHandle_t cublas_handle(cudaStream_t st) {
   return h;
 }
 
+// sm_target > 0: cuBLAS sizes its grid for that many SMs (the look-ahead's
+// side-stream panel must leave the concurrent GEMM's SMs alone).
 int dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha, const double* a,
           int64_t lda, const double* b, int64_t ldb, double beta, double* c, int64_t ldc,
-          cudaStream_t st) {
+          cudaStream_t st, int sm_target) {
   if (m == 0 || n == 0) return OZ_OK;
   cublasHandle_t h = cublas_handle(st);
   OZ_REQUIRE(h != nullptr, OZ_CUDA_ERROR, "cublasCreate failed");
   OZ_REQUIRE(cublasSetStream(h, st) == CUBLAS_STATUS_SUCCESS, OZ_CUDA_ERROR,
              "cublasSetStream failed");
+  OZ_REQUIRE(cublasSetSmCountTarget(h, sm_target > 0 ? sm_target : 0) == CUBLAS_STATUS_SUCCESS,
+             OZ_CUDA_ERROR, "cublasSetSmCountTarget failed");
   cublasStatus_t s = cublasDgemm(h, transa ? CUBLAS_OP_T : CUBLAS_OP_N,
                                  transb ? CUBLAS_OP_T : CUBLAS_OP_N, (int)m, (int)n, (int)k,
                                  &alpha, a, (int)lda, b, (int)ldb, &beta, c, (int)ldc);
@@ -154,7 +158,7 @@ extern "C" int oz_dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k,
                         const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
                         double* c, int64_t ldc, void* stream) {
   return oz::dgemm(transa, transb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc,
-                   oz::as_stream(stream));
+                   oz::as_stream(stream), 0);
 }
 
 // LAPACK-style interchanges -> permutation vector: pivots[i] is the original

@@ -29,6 +29,7 @@
 #include <cudaTypedefs.h>
 
 #include <stdlib.h>
+#include <vector>
 
 #include "common.cuh"
 
@@ -63,6 +64,7 @@ struct Params {
   int group_m;  // raster band height in tiles
   int experiment;  // tuning only (OZ_GEMM_EXPERIMENT): 1 = skip FP64 math, 2 = also skip final pass
   int wide;        // slice_bits > 7: (hi, lo) int8 planes per slice
+  unsigned long long* starts;  // tuning only (OZ_GEMM_STARTS): per-CTA start/end globaltimer
   uint8_t pa[MAX_PAIRS];
   uint8_t pb[MAX_PAIRS];
   uint16_t gshift[MAX_PAIRS];      // (i+j)*q of the group's pairs
@@ -317,6 +319,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  if (p.starts != nullptr && threadIdx.x == 0) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    p.starts[blockIdx.x] = t0;
+  }
 
   if (warp >= P_PRODUCER) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
@@ -533,6 +540,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   cluster_sync_all();
+  if (p.starts != nullptr && threadIdx.x == 0) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    p.starts[gridDim.x + blockIdx.x] = t1;
+  }
   if (warp == P_ALLOC) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -622,6 +634,21 @@ void build_groups(Params& p, const int32_t* shift, int npairs, int64_t inner, in
   p.ngroups = g;
 }
 
+struct StartLog {
+  static constexpr int LAUNCHES = 256;
+  unsigned long long* buf = nullptr;
+  int used = 0;
+  int grid[LAUNCHES], m[LAUNCHES], n[LAUNCHES];
+};
+StartLog& start_log() {
+  static StartLog lg;
+  if (!lg.buf) {
+    cudaMalloc(&lg.buf, sizeof(unsigned long long) * StartLog::LAUNCHES * 2 * 512);
+    cudaMemset(lg.buf, 0, sizeof(unsigned long long) * StartLog::LAUNCHES * 2 * 512);
+  }
+  return lg;
+}
+
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStream_t st,
                 int max_ctas = 0) {
   static bool attr_set = false;
@@ -652,6 +679,17 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStr
   if (max_ctas > 0 && grid > (max_ctas & ~1)) grid = max_ctas & ~1;
   if (grid < 2) grid = 2;
   if (grid > 2 * p.num_tiles) grid = 2 * p.num_tiles;
+  p.starts = nullptr;
+  if (getenv("OZ_GEMM_STARTS")) {  // tuning: CTA start/end spread of every launch
+    StartLog& lg = start_log();
+    if (lg.used < StartLog::LAUNCHES) {
+      p.starts = lg.buf + (size_t)lg.used * 2 * 512;
+      lg.grid[lg.used] = grid;
+      lg.m[lg.used] = p.m;
+      lg.n[lg.used] = p.n;
+      ++lg.used;
+    }
+  }
   if (p.debug_out != nullptr)
     emu_gemm_pair_kernel<true, false><<<grid, NUM_THREADS, P_SMEM_BYTES, st>>>(ta, tb, p);
   else if (p.wide)
@@ -770,4 +808,30 @@ extern "C" int oz_plan_groups(int npairs, const int32_t* pair_shift, int64_t inn
   for (int g = 0; g <= p.ngroups; ++g) gstart[g] = p.gstart[g];
   for (int g = 0; g < p.ngroups; ++g) gshift[g] = p.gshift[g];
   return p.ngroups;
+}
+
+// Tuning only (OZ_GEMM_STARTS=1): per launch, the spread of CTA start times
+// and of CTA end times (globaltimer, us), to spot late-starting CTAs.
+extern "C" int oz_gemm_starts_dump(void) {
+  using namespace oz::emu;
+  StartLog& lg = start_log();
+  cudaDeviceSynchronize();
+  std::vector<unsigned long long> h((size_t)lg.used * 2 * 512);
+  cudaMemcpy(h.data(), lg.buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  for (int i = 0; i < lg.used; ++i) {
+    const unsigned long long* s0 = h.data() + (size_t)i * 2 * 512;
+    const int g = lg.grid[i];
+    unsigned long long smin = ~0ull, smax = 0, emin = ~0ull, emax = 0;
+    for (int b = 0; b < g; ++b) {
+      smin = s0[b] < smin ? s0[b] : smin;
+      smax = s0[b] > smax ? s0[b] : smax;
+      emin = s0[g + b] < emin ? s0[g + b] : emin;
+      emax = s0[g + b] > emax ? s0[g + b] : emax;
+    }
+    fprintf(stderr, "gemm %3d m=%6d n=%6d grid=%3d  start spread %8.1f us  end spread %8.1f us  "
+            "duration %8.1f us\n", i, lg.m[i], lg.n[i], g, (smax - smin) / 1e3, (emax - emin) / 1e3,
+            (emax - smin) / 1e3);
+  }
+  lg.used = 0;
+  return 0;
 }

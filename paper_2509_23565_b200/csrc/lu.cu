@@ -31,7 +31,7 @@ namespace oz {
 
 int dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha, const double* a,
           int64_t lda, const double* b, int64_t ldb, double beta, double* c, int64_t ldc,
-          cudaStream_t st);
+          cudaStream_t st, int sm_target = 0);
 int split_launch(const double* src, int64_t rows, int64_t cols, int64_t row_stride,
                  int64_t col_stride, int orientation, int mode, int k, int q, int8_t* slices,
                  int64_t slice_ld, int64_t slice_stride, int32_t* exps, void* aux_v,
@@ -601,7 +601,9 @@ __global__ void __launch_bounds__(TRSMF_THREADS) trsm_fused_kernel(
   double* sB = dsm;                          // [jb][NC]
   double* sD = dsm + (size_t)jb * NC;        // [64][65] diagonal block, row-major
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t c0 = (int64_t)blockIdx.x * NC;
+  // grid-stride over column groups: a capped grid (look-ahead side stream)
+  // walks every group
+  for (int64_t c0 = (int64_t)blockIdx.x * NC; c0 < ncols; c0 += (int64_t)gridDim.x * NC) {
   const int nc = (int)(ncols - c0 < NC ? ncols - c0 : NC);
   // loads batched (unrolled) so each thread keeps several L2/HBM requests in flight
 #pragma unroll 8
@@ -665,6 +667,8 @@ __global__ void __launch_bounds__(TRSMF_THREADS) trsm_fused_kernel(
   for (int i = tid; i < jb * NC; i += TRSMF_THREADS) {
     const int c = i / jb, r = i - c * jb;
     if (c < nc) B[(c0 + c) * ldb + r] = sB[r * NC + c];
+  }
+  __syncthreads();
   }
 }
 template <int NC>
@@ -913,7 +917,7 @@ int max_abs(const double* a, int64_t m, int64_t n, int64_t rs, int64_t cs, int u
 }
 
 int apply_list(double* a, int64_t lda, const LuWs& ws, int64_t c0a, int64_t c1a, int64_t c0b,
-               int64_t c1b, cudaStream_t st) {
+               int64_t c1b, cudaStream_t st, int max_ctas = 0) {
   const int64_t ncols = (c1a - c0a) + (c1b - c0b);
   if (ncols <= 0) return OZ_OK;
   struct Stop {
@@ -923,6 +927,7 @@ int apply_list(double* a, int64_t lda, const LuWs& ws, int64_t c0a, int64_t c1a,
   } stop{prof_start(st), st};
   int64_t blocks = ceil_div(ncols, 8);
   if (blocks > sm_count() * 16) blocks = sm_count() * 16;
+  if (max_ctas > 0 && blocks > max_ctas) blocks = max_ctas;
   laswp_gather_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, lda, ws.swap_dst, ws.swap_src,
                                                         ws.swap_cnt, c0a, c1a, c0b, c1b);
   OZ_CHECK_LAUNCH();
@@ -932,7 +937,7 @@ int apply_list(double* a, int64_t lda, const LuWs& ws, int64_t c0a, int64_t c1a,
 // U12 <- L11^{-1} A12 for L11 (jb x jb, unit lower) at a[j,j], A12 = rows j..j+jb, ncols
 template <int NC>
 int trsm_fused(const double* L, int64_t lda, int64_t jb, double* b, int64_t ldb, int64_t ncols,
-               cudaStream_t st) {
+               cudaStream_t st, int max_ctas) {
   static bool attr = false;
   if (!attr) {
     OZ_CHECK_CUDA(cudaFuncSetAttribute(trsm_fused_kernel<NC>,
@@ -940,14 +945,40 @@ int trsm_fused(const double* L, int64_t lda, int64_t jb, double* b, int64_t ldb,
                                        (int)trsmf_smem<NC>(TRSMF_MAXJB)));
     attr = true;
   }
-  trsm_fused_kernel<NC><<<(unsigned)ceil_div(ncols, NC), TRSMF_THREADS, trsmf_smem<NC>((int)jb),
-                          st>>>(L, lda, (int)jb, b, ldb, ncols);
+  int64_t grid = ceil_div(ncols, NC);
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  trsm_fused_kernel<NC><<<(unsigned)grid, TRSMF_THREADS, trsmf_smem<NC>((int)jb), st>>>(
+      L, lda, (int)jb, b, ldb, ncols);
   OZ_CHECK_LAUNCH();
   return OZ_OK;
 }
 
+// Wide right-hand sides: recursive halving, X1 = L11^-1 B1, B2 -= L21 X1
+// (one DGEMM of depth jb/2, jb/4, ... instead of jb/64 DGEMMs of depth 64),
+// X2 = L22^-1 B2; 64-row diagonal blocks by trsm_unit_lower_kernel.
+int trsm_rec(double* a, int64_t lda, int64_t j, int64_t jb, double* b, int64_t ldb,
+             int64_t ncols, cudaStream_t st, int max_ctas) {
+  if (jb <= TRSM_W) {
+    const int tag = prof_start(st);
+    trsm_unit_lower_kernel<<<(unsigned)ceil_div(ncols, TRSM_COLS), TRSM_COLS, TRSM_SMEM, st>>>(
+        a + j * lda + j, lda, (int)jb, b, ldb, ncols);
+    OZ_CHECK_LAUNCH();
+    prof_stop(tag, st, PROF_TRSM, (double)jb * jb * ncols);
+    return OZ_OK;
+  }
+  const int64_t h = ((jb / 2 + TRSM_W - 1) / TRSM_W) * TRSM_W;
+  OZ_TRY(trsm_rec(a, lda, j, h, b, ldb, ncols, st, max_ctas));
+  const int tag = prof_start(st);
+  OZ_TRY(dgemm(0, 0, jb - h, ncols, h, -1.0, a + j * lda + (j + h), lda, b, ldb, 1.0, b + h, ldb,
+               st, max_ctas));
+  prof_stop(tag, st, PROF_DGEMM_TRSM, 2.0 * (jb - h) * ncols * h);
+  return trsm_rec(a, lda, j + h, jb - h, b + h, ldb, ncols, st, max_ctas);
+}
+
+// max_ctas > 0 caps every grid of the call (look-ahead side stream: the
+// panel must not take SMs the concurrent persistent GEMM was sized for)
 int trsm_blocked(double* a, int64_t lda, int64_t j, int64_t jb, double* b, int64_t ldb,
-                 int64_t ncols, cudaStream_t st) {
+                 int64_t ncols, cudaStream_t st, int max_ctas = 0) {
   if (ncols <= 0) return OZ_OK;
   static const bool legacy = getenv("OZ_TRSM_LEGACY") != nullptr;
   // few right-hand sides (the look-ahead's next panel, the recursion inside a
@@ -956,7 +987,7 @@ int trsm_blocked(double* a, int64_t lda, int64_t j, int64_t jb, double* b, int64
   // FP64-throughput-bound (15 vs 5 TFLOP/s at 30720 columns)
   if (!legacy && jb <= TRSMF_MAXJB && ncols <= 2048) {
     const int tag = prof_start(st);
-    const int s = trsm_fused<8>(a + j * lda + j, lda, jb, b, ldb, ncols, st);
+    const int s = trsm_fused<8>(a + j * lda + j, lda, jb, b, ldb, ncols, st, max_ctas);
     prof_stop(tag, st, PROF_TRSM, (double)jb * jb * ncols);
     return s;
   }
@@ -967,23 +998,7 @@ int trsm_blocked(double* a, int64_t lda, int64_t j, int64_t jb, double* b, int64
                                        (int)TRSM_SMEM));
     attr = true;
   }
-  for (int64_t i = 0; i < jb; i += TRSM_W) {
-    const int w = (int)(jb - i < TRSM_W ? jb - i : TRSM_W);
-    const double* L = a + (j + i) * lda + (j + i);
-    int tag = prof_start(st);
-    trsm_unit_lower_kernel<<<(unsigned)ceil_div(ncols, TRSM_COLS), TRSM_COLS, TRSM_SMEM, st>>>(
-        L, lda, w, b + i, ldb, ncols);
-    OZ_CHECK_LAUNCH();
-    prof_stop(tag, st, PROF_TRSM, (double)w * w * ncols);
-    const int64_t below = jb - i - w;
-    if (below > 0) {
-      tag = prof_start(st);
-      OZ_TRY(dgemm(0, 0, below, ncols, w, -1.0, a + (j + i) * lda + (j + i + w), lda, b + i, ldb,
-                   1.0, b + i + w, ldb, st));
-      prof_stop(tag, st, PROF_DGEMM_TRSM, 2.0 * below * ncols * w);
-    }
-  }
-  return OZ_OK;
+  return trsm_rec(a, lda, j, jb, b, ldb, ncols, st, max_ctas);
 }
 
 int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t base,
@@ -1106,19 +1121,20 @@ int panel_rec(double* a, int64_t lda, int64_t m, int64_t jb, int64_t c0, int64_t
               int64_t base, int32_t* ipiv, int32_t* info, unsigned long long* growth,
               const LuWs& ws, cudaStream_t st, int ctas) {
   const int64_t w = c1 - c0;
+  const int cap = ctas < sm_count() ? ctas : 0;  // side-stream panel: keep to its SMs
   if (w <= wmax) {
     OZ_TRY(panel_window(a, lda, c0, m - c0, (int)w, base, ipiv, info, growth, ws, st, ctas));
-    return apply_list(a, lda, ws, 0, c0, c1, jb, st);
+    return apply_list(a, lda, ws, 0, c0, c1, jb, st, cap);
   }
   int64_t mid = c0 + ((w / 2 + wmax - 1) / wmax) * wmax;
   if (mid >= c1) mid = c0 + wmax;
   OZ_TRY(panel_rec(a, lda, m, jb, c0, mid, wmax, base, ipiv, info, growth, ws, st, ctas));
   const int64_t kk = mid - c0, right = c1 - mid;
-  OZ_TRY(trsm_blocked(a, lda, c0, kk, a + mid * lda + c0, lda, right, st));
+  OZ_TRY(trsm_blocked(a, lda, c0, kk, a + mid * lda + c0, lda, right, st, cap));
   if (m - mid > 0) {
     const int tag = prof_start(st);
     OZ_TRY(dgemm(0, 0, m - mid, right, kk, -1.0, a + c0 * lda + mid, lda, a + mid * lda + c0,
-                 lda, 1.0, a + mid * lda + mid, lda, st));
+                 lda, 1.0, a + mid * lda + mid, lda, st, cap));
     prof_stop(tag, st, PROF_DGEMM_PANEL, 2.0 * (m - mid) * right * kk);
   }
   return panel_rec(a, lda, m, jb, mid, c1, wmax, base, ipiv, info, growth, ws, st, ctas);
@@ -1255,6 +1271,15 @@ int lookahead_split(int setting, int64_t m, int64_t nb, int npairs, int sms) {
 struct LuTrace {
   bool on = false;
   std::vector<cudaEvent_t> ev;
+  std::vector<int> split;  // look-ahead SMs per step
+  std::vector<cudaEvent_t> sub;  // per look-ahead step: after laswp / trsm / split of the rest
+  void mark_sub(cudaStream_t st) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    sub.push_back(e);
+  }
   void mark(cudaStream_t st) {
     if (!on) return;
     cudaEvent_t e;
@@ -1275,7 +1300,11 @@ int side_stream(SideStream** out) {
   if ((int)per_dev.size() <= dev) per_dev.resize(dev + 1);
   SideStream& s = per_dev[dev];
   if (!s.st) {
-    OZ_CHECK_CUDA(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
+    int lo = 0, hi = 0;
+    OZ_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    const char* pr = getenv("OZ_SIDE_PRIO");  // tuning: 1 = highest priority for the panel
+    OZ_CHECK_CUDA(cudaStreamCreateWithPriority(&s.st, cudaStreamNonBlocking,
+                                               pr && atoi(pr) ? hi : lo));
     OZ_CHECK_CUDA(cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming));
     OZ_CHECK_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
   }
@@ -1348,6 +1377,7 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
       if (la) {
         const int la_sms = lookahead_split(la_setting, rest, jb, backend != 0 ? npairs : 0,
                                            sm_count());
+        if (tr.on) tr.split.push_back(la_sms);
         OZ_CHECK_CUDA(cudaEventRecord(side->ready, st));
         OZ_CHECK_CUDA(cudaStreamWaitEvent(side->st, side->ready, 0));
         OZ_TRY(panel_factor(p2, lda, rest, jb2, j + jb, ipiv + j + jb, info, ws.bits, ws,
@@ -1355,8 +1385,11 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
         OZ_CHECK_CUDA(cudaEventRecord(side->done, side->st));
         tr.mark(side->st);  // 5 side stream: panel done
         OZ_TRY(laswp_ipiv(a, lda, 0, j, j + jb + jb2, n, j, ipiv + j, (int)jb, ws, st));
+        tr.mark_sub(st);
         OZ_TRY(trsm_blocked(a, lda, j, jb, a12 + jb2 * lda, lda, rest - jb2, st));
+        tr.mark_sub(st);
         OZ_TRY(schur_split_part(sc, false, jb2, rest, ws, st));
+        tr.mark_sub(st);
         OZ_TRY(schur_cols(sc, jb2, rest, ws, st, sm_count() - la_sms));
         tr.mark(st);  // 6 after the rest of the step
         OZ_CHECK_CUDA(cudaStreamWaitEvent(st, side->done, 0));
@@ -1373,16 +1406,24 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
   if (tr.on) {
     cudaStreamSynchronize(st);
     // 7 marks per full step: start, laswp, trsm, split, gemm_a, side_done, gemm_b
-    fprintf(stderr, "step    m  laswp  trsm  split gemm_a  panel(side) gemm_b  total [ms]\n");
+    fprintf(stderr, "step    m  laswp  trsm  split gemm_a  panel(side) gemm_b  total [ms]  sms"
+                    "  (rest: laswp trsm split gemm)\n");
     for (size_t i = 0; i + 7 <= tr.ev.size(); i += 7) {
       float t[7];
       for (int q2 = 1; q2 < 7; ++q2) cudaEventElapsedTime(&t[q2], tr.ev[i], tr.ev[i + q2]);
       const float total = i + 7 < tr.ev.size() ? [&] { float x; cudaEventElapsedTime(&x, tr.ev[i], tr.ev[i + 7]); return x; }() : t[6];
-      fprintf(stderr, "%4zu %6lld %6.2f %5.2f %6.2f %6.2f %11.2f %6.2f %6.2f\n", i / 7,
-              (long long)(n - (int64_t)(i / 7) * nb - nb), t[1], t[2] - t[1], t[3] - t[2],
-              t[4] - t[3], t[5] - t[4], t[6] - t[4], total);
+      const size_t si = i / 7;
+      float r3[3] = {0, 0, 0};
+      if (3 * si + 2 < tr.sub.size())
+        for (int q3 = 0; q3 < 3; ++q3) cudaEventElapsedTime(&r3[q3], tr.ev[i + 4], tr.sub[3 * si + q3]);
+      fprintf(stderr, "%4zu %6lld %6.2f %5.2f %6.2f %6.2f %11.2f %6.2f %6.2f %4d  %5.2f %5.2f %5.2f %6.2f\n",
+              si, (long long)(n - (int64_t)si * nb - nb), t[1], t[2] - t[1], t[3] - t[2],
+              t[4] - t[3], t[5] - t[4], t[6] - t[4], total,
+              si < tr.split.size() ? tr.split[si] : 0, r3[0], r3[1] - r3[0], r3[2] - r3[1],
+              t[6] - t[4] - r3[2]);
     }
     for (auto e : tr.ev) cudaEventDestroy(e);
+    for (auto e : tr.sub) cudaEventDestroy(e);
   }
   if (unsigned long long* dbg = panel_dbg()) {
     // debug: per-phase cycles of the panel steps, summed over all CTAs

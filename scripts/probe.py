@@ -53,7 +53,7 @@ def lu_probe(n, nb, backends):
 
 if __name__ == "__main__":
     what = sys.argv[1]
-    if what in ("gemm1", "lu1", "kern", "e2e"):
+    if what in ("gemm1", "lu1", "kern", "e2e", "starts"):
         pass
     elif what == "gemm":
         gemm_probe(int(sys.argv[2]), [int(k) for k in sys.argv[3].split(",")])
@@ -80,10 +80,12 @@ if __name__ == "__main__" and sys.argv[1] == "gemm1":
 
 if __name__ == "__main__" and sys.argv[1] == "lu1":
     n, nb, k = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
-    a = generate_device(0, n, seed=99, layout="F")
     bk = oz.GemmBackend.int8(k) if k > 0 else oz.GemmBackend.native()
-    r = factor_device(a, nb, bk)
-    torch.cuda.synchronize()
+    for _ in range(int(os.environ.get("OZ_PROBE_REPS", "1"))):  # >1: trace a warm run
+        a = generate_device(0, n, seed=99, layout="F")
+        r = factor_device(a, nb, bk)
+        torch.cuda.synchronize()
+        del a
     print("lu1 done info", int(r[2].item()))
 
 
@@ -136,3 +138,13 @@ if __name__ == "__main__" and sys.argv[1] == "e2e":
         print(f"e2e n={n}: H2D alone {1e3*(t1-t0):.1f} ms ({8*n*n/(t1-t0)/1e9:.1f} GB/s), "
               f"solve_system {1e3*(t2-t1):.1f} ms (factor+solve {1e3*r.seconds:.1f} ms), "
               f"resid {r.scaled_residual:.3g}", flush=True)
+
+
+if __name__ == "__main__" and sys.argv[1] == "starts":
+    # OZ_GEMM_STARTS=1: CTA start/end spread of each emulated-GEMM launch in one LU
+    n, nb, k = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
+    a = generate_device(0, n, seed=99, layout="F")
+    r = factor_device(a, nb, oz.GemmBackend.int8(k))
+    torch.cuda.synchronize()
+    from paper_2509_23565_b200 import _lib
+    _lib.call("oz_gemm_starts_dump")
