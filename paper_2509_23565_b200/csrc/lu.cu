@@ -23,6 +23,7 @@
 // panel is updated with trsm + cuBLAS DGEMM; the Schur update is cuBLAS DGEMM
 // (native comparator) or the Ozaki-INT8 tcgen05 GEMM (gemm_emu.cu).
 #include <stdlib.h>
+#include <algorithm>
 #include <vector>
 
 #include "common.cuh"
@@ -108,6 +109,7 @@ struct PanelShared {
   int prow[PANEL_W];
   double urow[2][PANEL_W];  // pivot rows of steps t (buf) and t-1 (buf ^ 1)
   double stage[STAGE_G][CAND_STRIDE];
+  double crec[2][CAND_STRIDE];  // cluster variant: this CTA's published record (DSMEM)
   int best;
 };
 
@@ -125,7 +127,28 @@ size_t panel_smem_bytes(int w, int R) {
   return (size_t)w * R * sizeof(double) + (size_t)R * sizeof(int);
 }
 
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acquire() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ double ld_dsmem(const void* local, unsigned rank) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(local);
+  unsigned ra;
+  double v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
+  return v;
+}
+
 // One window of the panel: solve.py:75-90 for columns r0..r0+w-1 over rows r0..
+// kCluster = false: G co-resident CTAs (cooperative launch) exchange candidate
+// records through global memory and a release/acquire counter; kCluster =
+// true: the G CTAs form one thread-block cluster, each publishes its record in
+// its own shared memory and a cluster barrier (arrive.release / wait.acquire)
+// replaces the counter, so one column's exchange costs ~1 us instead of ~3.
+template <bool kCluster>
 __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArgs p) {
   extern __shared__ double sm[];  // slab [w][R] column-major, then pos[R]
   __shared__ PanelShared sh;
@@ -161,8 +184,12 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
     }
   }
 
+  if (kCluster) {  // every CTA of the cluster is running before any DSMEM access
+    cluster_arrive_release();
+    cluster_wait_acquire();
+  }
   long long _tp = clock64();
-  const bool staged = gridDim.x <= STAGE_G;
+  const bool staged = kCluster || gridDim.x <= STAGE_G;
   for (int t = 0; t < w; ++t) {
     const int buf = t & 1;
     double* urow = sh.urow[buf];
@@ -205,7 +232,8 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
       // Step t-1's update of columns > t is deferred (below), so the
       // candidate row's values there are formed here with the same
       // product-then-subtract the deferred update will store.
-      double* rec = p.cand + ((size_t)buf * gridDim.x + blockIdx.x) * CAND_STRIDE;
+      double* rec = kCluster ? sh.crec[buf]
+                             : p.cand + ((size_t)buf * gridDim.x + blockIdx.x) * CAND_STRIDE;
       long long* irec = reinterpret_cast<long long*>(rec);
       if (br >= 0) {
         const double lp = t > 0 ? sm[(t - 1) * R + br] : 0.0;
@@ -223,10 +251,11 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
       // the warp's record stores are ordered before lane 0's release-add by
       // the warp barrier (one release instead of a GPU-scope fence per lane)
       __syncwarp();
-      if (lane == 0) red_release_add(&p.bar->count, 1u);
+      if (!kCluster && lane == 0) red_release_add(&p.bar->count, 1u);
       if (p.dbg && lane == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 0, (unsigned long long)(_n - _tp)); _tp = _n; }
     }
     __syncthreads();  // the publish above read row br before the deferred update below
+    if (kCluster) cluster_arrive_release();  // publishes sh.crec[buf] to the cluster
     // ---- while the other CTAs arrive: step t-1's update of columns t+1..w-1
     //      (column t was updated before the argmax).  pos[] is unchanged
     //      since that step, so the same rows are updated.
@@ -242,13 +271,17 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
         }
       }
     }
-    // ---- wait for all CTAs (counter reaches G*(t+1))
-    if (tid == 0) {
-      const unsigned target = gridDim.x * (unsigned)(t + 1);
-      while (ld_acquire_u32(&p.bar->count) < target) {
+    // ---- wait for all CTAs (counter reaches G*(t+1) / the cluster barrier)
+    if (kCluster) {
+      cluster_wait_acquire();
+    } else {
+      if (tid == 0) {
+        const unsigned target = gridDim.x * (unsigned)(t + 1);
+        while (ld_acquire_u32(&p.bar->count) < target) {
+        }
       }
+      __syncthreads();
     }
-    __syncthreads();
     if (p.dbg && tid == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 1, (unsigned long long)(_n - _tp)); _tp = _n; }
     const double* recs = p.cand + (size_t)buf * gridDim.x * CAND_STRIDE;
     if (staged) {
@@ -259,7 +292,12 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
 #pragma unroll
       for (int i = 0; i < LOADS; ++i) {
         const int e = tid + i * PANEL_THREADS;
-        v[i] = e < total ? __ldcg(recs + e) : 0.0;
+        if (kCluster) {
+          const int g = e / CAND_STRIDE;
+          v[i] = e < total ? ld_dsmem(&sh.crec[buf][e - g * CAND_STRIDE], (unsigned)g) : 0.0;
+        } else {
+          v[i] = e < total ? __ldcg(recs + e) : 0.0;
+        }
       }
 #pragma unroll
       for (int i = 0; i < LOADS; ++i) {
@@ -385,6 +423,10 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
   if (p.growth) {
     gmax = warp_max(gmax);
     if (lane == 0 && gmax > 0.0) atomic_max_abs(p.growth, gmax);
+  }
+  if (kCluster) {  // no CTA leaves while others may still read its records
+    cluster_arrive_release();
+    cluster_wait_acquire();
   }
 }
 
@@ -1001,31 +1043,104 @@ int trsm_blocked(double* a, int64_t lda, int64_t j, int64_t jb, double* b, int64
   return trsm_rec(a, lda, j, jb, b, ldb, ncols, st, max_ctas);
 }
 
-int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t base,
-                 int32_t* ipiv, int32_t* info, unsigned long long* growth, const LuWs& ws,
-                 cudaStream_t st, int max_ctas) {
+// Cluster exchange for short panels: OZ_PANEL_CLUSTER = max cluster size
+// (default 16, 0 = off), OZ_PANEL_CLUSTER_M = max panel rows (default 8192).
+int panel_cluster_max() {
+  static const int v = [] {
+    const char* e = getenv("OZ_PANEL_CLUSTER");
+    return e ? atoi(e) : 16;
+  }();
+  return v;
+}
+int64_t panel_cluster_rows() {
+  static const int64_t v = [] {
+    const char* e = getenv("OZ_PANEL_CLUSTER_M");
+    return e ? (int64_t)atoll(e) : (int64_t)8192;
+  }();
+  return v;
+}
+int panel_smem_cap() {
   static int max_smem = 0;
   if (!max_smem) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    OZ_CHECK_CUDA(cudaFuncSetAttribute(panel_window_kernel,
+  }
+  return max_smem - (int)sizeof(PanelShared) - 1024;
+}
+// can a cluster of G panel CTAs (smem bytes each) be resident at all?
+bool cluster_fits(int G, size_t smem) {
+  static std::vector<std::pair<long long, bool>> memo;
+  const long long key = (long long)G << 32 | (long long)smem;
+  for (auto& kv : memo)
+    if (kv.first == key) return kv.second;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(PANEL_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = G;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  const bool ok = cudaOccupancyMaxActiveClusters(&n, (void*)panel_window_kernel<true>, &cfg) ==
+                      cudaSuccess && n > 0;
+  cudaGetLastError();
+  memo.push_back({key, ok});
+  return ok;
+}
+
+int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t base,
+                 int32_t* ipiv, int32_t* info, unsigned long long* growth, const LuWs& ws,
+                 cudaStream_t st, int max_ctas) {
+  static bool attr = false;
+  if (!attr) {
+    OZ_CHECK_CUDA(cudaFuncSetAttribute(panel_window_kernel<false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       max_smem - (int)sizeof(PanelShared) - 1024));
+                                       panel_smem_cap()));
+    OZ_CHECK_CUDA(cudaFuncSetAttribute(panel_window_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       panel_smem_cap()));
+    OZ_CHECK_CUDA(cudaFuncSetAttribute(panel_window_kernel<true>,
+                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr = true;
   }
   const int sms = max_ctas > 0 && max_ctas < sm_count() ? max_ctas : sm_count();
-  const size_t cap = (size_t)max_smem - sizeof(PanelShared) - 1024;
-  int G = (int)ceil_div(m, 256);
-  if (G > sms) G = sms;
-  if (G < 1) G = 1;
-  int R = (int)ceil_div(m, G);
-  while (panel_smem_bytes(w, R) > cap) {
-    OZ_REQUIRE(G < sms, OZ_UNSUPPORTED, "panel of %lld rows x %d cols does not fit on chip",
-               (long long)m, w);
-    ++G;
-    R = (int)ceil_div(m, G);
+  const size_t cap = (size_t)panel_smem_cap();
+  // cluster variant: as few CTAs as the slab allows, at most the cluster size
+  const int cmax = panel_cluster_max();
+  bool cluster = false;
+  int G = 0, R = 0;
+  if (cmax >= 2 && m <= panel_cluster_rows()) {
+    const int64_t rmax = (int64_t)((cap - 0) / ((size_t)w * sizeof(double) + sizeof(int)));
+    int g = (int)std::max<int64_t>(ceil_div(m, rmax), std::min<int64_t>(ceil_div(m, 256), cmax));
+    if (g < 2) g = 2;
+    if (g <= cmax && g <= sms) {
+      const int rr = (int)ceil_div(m, g);
+      g = (int)ceil_div(m, rr);
+      if (g >= 2 && panel_smem_bytes(w, rr) <= cap && cluster_fits(g, panel_smem_bytes(w, rr))) {
+        cluster = true;
+        G = g;
+        R = rr;
+      }
+    }
   }
-  G = (int)ceil_div(m, R);
+  if (!cluster) {
+    G = (int)ceil_div(m, 256);
+    if (G > sms) G = sms;
+    if (G < 1) G = 1;
+    R = (int)ceil_div(m, G);
+    while (panel_smem_bytes(w, R) > cap) {
+      OZ_REQUIRE(G < sms, OZ_UNSUPPORTED, "panel of %lld rows x %d cols does not fit on chip",
+                 (long long)m, w);
+      ++G;
+      R = (int)ceil_div(m, G);
+    }
+    G = (int)ceil_div(m, R);
+  }
   PanelArgs pa;
   pa.a = a;
   pa.lda = lda;
@@ -1048,13 +1163,29 @@ int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t b
   pa.list_cnt = ws.swap_cnt;
   pa.dbg = panel_dbg();
   OZ_CHECK_CUDA(cudaMemsetAsync(ws.swap_cnt, 0, sizeof(int32_t), st));
-  OZ_CHECK_CUDA(cudaMemsetAsync(ws.bar, 0, sizeof(GridBar), st));
-  void* args[] = {&pa};
   const int tag = prof_start(st);
   count_launch();
-  OZ_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)panel_window_kernel, dim3(G),
-                                            dim3(PANEL_THREADS), args, panel_smem_bytes(w, R),
-                                            st));
+  if (cluster) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(PANEL_THREADS);
+    cfg.dynamicSmemBytes = panel_smem_bytes(w, R);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    OZ_CHECK_CUDA(cudaLaunchKernelEx(&cfg, panel_window_kernel<true>, pa));
+  } else {
+    OZ_CHECK_CUDA(cudaMemsetAsync(ws.bar, 0, sizeof(GridBar), st));
+    void* args[] = {&pa};
+    OZ_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)panel_window_kernel<false>, dim3(G),
+                                              dim3(PANEL_THREADS), args,
+                                              panel_smem_bytes(w, R), st));
+  }
   prof_stop(tag, st, PROF_PANEL, (double)m * w);
   return OZ_OK;
 }
@@ -1098,11 +1229,13 @@ int laswp_ipiv(double* a, int64_t lda, int64_t c0a, int64_t c1a, int64_t c0b, in
 // Widest window (<= PANEL_W) whose m-row slab fits in the shared memory of
 // max_ctas CTAs: tall panels (distributed runs, m ~ 1e5) use narrower windows.
 int panel_width_for(int64_t m, int max_ctas) {
-  int dev = 0, smem = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const int64_t cap = (int64_t)smem - (int64_t)sizeof(PanelShared) - 1024;
-  const int64_t rows = ceil_div(m, max_ctas);
+  const int64_t cap = panel_smem_cap();
+  // short panels go to the cluster variant (<= panel_cluster_max() CTAs):
+  // the window must fit m / cmax rows per CTA
+  const int cmax = panel_cluster_max();
+  const int64_t ctas = cmax >= 2 && m <= panel_cluster_rows() ? std::min(cmax, max_ctas)
+                                                             : max_ctas;
+  const int64_t rows = ceil_div(m, ctas);
   int64_t w = (cap / rows - (int64_t)sizeof(int)) / (int64_t)sizeof(double);
   if (w > PANEL_W) w = PANEL_W;
   if (w >= 16) w &= ~7;  // keep the window a multiple of 8 columns
