@@ -68,6 +68,25 @@ __device__ __forceinline__ bool better(double a1, int p1, double a2, int p2) {
   return a1 > a2 || (a1 == a2 && p1 < p2);
 }
 
+// Warp-wide argmax in better() order with integer reductions instead of a
+// 5-round shuffle tree: the order-preserving bits of |v| (NaN canonical,
+// "no candidate" (a < 0) as 0 with position INT_MAX), then the smallest
+// position among the maxima.  Every lane returns the winner (a, p, r).
+__device__ __forceinline__ void warp_argmax(double& a, int& p, int& r) {
+  const unsigned long long b =
+      a < 0.0 ? 0ull
+              : (isnan(a) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(a));
+  const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  const bool top = hi == mhi && lo == mlo;
+  const int mp = __reduce_min_sync(0xffffffffu, top ? p : 0x7fffffff);
+  const int src = __ffs(__ballot_sync(0xffffffffu, top && p == mp)) - 1;
+  a = __shfl_sync(0xffffffffu, a, src);
+  r = __shfl_sync(0xffffffffu, r, src);
+  p = mp;
+}
+
 struct PanelArgs {
   double* a;
   int64_t lda;
@@ -195,17 +214,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
     double* urow = sh.urow[buf];
     const double* uprev = sh.urow[buf ^ 1];
     // ---- block argmax of the thread candidates (np.argmax order)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double oa = __shfl_xor_sync(0xffffffffu, ca, o);
-      const int op = __shfl_xor_sync(0xffffffffu, cp, o);
-      const int orr = __shfl_xor_sync(0xffffffffu, cr, o);
-      if (better(oa, op, ca, cp)) {
-        ca = oa;
-        cp = op;
-        cr = orr;
-      }
-    }
+    warp_argmax(ca, cp, cr);
     if (lane == 0) {
       sh.red_a[wid] = ca;
       sh.red_p[wid] = cp;
@@ -216,18 +225,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
       double ba = lane < PANEL_WARPS ? sh.red_a[lane] : -2.0;
       int bp = lane < PANEL_WARPS ? sh.red_p[lane] : 0x7fffffff;
       int br = lane < PANEL_WARPS ? sh.red_r[lane] : -1;
-#pragma unroll
-      for (int o = 4; o > 0; o >>= 1) {
-        const double oa = __shfl_xor_sync(0xffffffffu, ba, o);
-        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-        const int orr = __shfl_xor_sync(0xffffffffu, br, o);
-        if (better(oa, op, ba, bp)) {
-          ba = oa;
-          bp = op;
-          br = orr;
-        }
-      }
-      br = __shfl_sync(0xffffffffu, br, 0);
+      warp_argmax(ba, bp, br);
       // ---- publish the CTA's candidate record, then arrive on the step counter.
       // Step t-1's update of columns > t is deferred (below), so the
       // candidate row's values there are formed here with the same
@@ -338,17 +336,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
           }
         }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double oa = __shfl_xor_sync(0xffffffffu, ba, o);
-        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-        const int og = __shfl_xor_sync(0xffffffffu, bg, o);
-        if (better(oa, op, ba, bp)) {
-          ba = oa;
-          bp = op;
-          bg = og;
-        }
-      }
+      warp_argmax(ba, bp, bg);
       if (p.dbg && lane == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 2, (unsigned long long)(_n - _tp)); _tp = _n; }
       // ---- winner's row (the new U row) and interchange bookkeeping
       const double* win = staged ? sh.stage[bg] : recs + (size_t)bg * CAND_STRIDE;
