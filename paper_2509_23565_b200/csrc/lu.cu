@@ -261,14 +261,33 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
       for (int r = tid; r < nloc; r += PANEL_THREADS) {
         if (pos[r] < 0) continue;
         const double l = sm[(t - 1) * R + r];
-#pragma unroll 4
-        for (int c = t + 1; c < w; ++c) {
+        int c = t + 1;
+        // batches of 8: all loads issued before the dependent math and the
+        // stores (the compiler cannot reorder shared loads past shared
+        // stores it cannot disambiguate), max over a shallow tree
+        for (; c + 8 <= w; c += 8) {
+          double x[8], u[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            x[i] = sm[(c + i) * R + r];
+            u[i] = uprev[c + i];
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) x[i] = __dsub_rn(x[i], __dmul_rn(l, u[i]));
+#pragma unroll
+          for (int i = 0; i < 8; ++i) sm[(c + i) * R + r] = x[i];
+          const double m01 = fmax(fabs(x[0]), fabs(x[1])), m23 = fmax(fabs(x[2]), fabs(x[3]));
+          const double m45 = fmax(fabs(x[4]), fabs(x[5])), m67 = fmax(fabs(x[6]), fabs(x[7]));
+          gmax = fmax(gmax, fmax(fmax(m01, m23), fmax(m45, m67)));
+        }
+        for (; c < w; ++c) {
           const double x = __dsub_rn(sm[c * R + r], __dmul_rn(l, uprev[c]));
           sm[c * R + r] = x;
           gmax = fmax(gmax, fabs(x));
         }
       }
     }
+    if (p.dbg && tid == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 4, (unsigned long long)(_n - _tp)); _tp = _n; }
     // ---- wait for all CTAs (counter reaches G*(t+1) / the cluster barrier)
     if (kCluster) {
       cluster_wait_acquire();
@@ -1104,7 +1123,12 @@ int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t b
   int G = 0, R = 0;
   if (cmax >= 2 && m <= panel_cluster_rows()) {
     const int64_t rmax = (int64_t)((cap - 0) / ((size_t)w * sizeof(double) + sizeof(int)));
-    int g = (int)std::max<int64_t>(ceil_div(m, rmax), std::min<int64_t>(ceil_div(m, 256), cmax));
+    static const int64_t rows_target = [] {  // tuning: rows per CTA the cluster aims for
+      const char* e = getenv("OZ_PANEL_CLUSTER_ROWS");
+      return e ? (int64_t)atoll(e) : (int64_t)128;  // measured: 128 beats 256, = 64
+    }();
+    int g = (int)std::max<int64_t>(ceil_div(m, rmax),
+                                   std::min<int64_t>(ceil_div(m, rows_target), cmax));
     if (g < 2) g = 2;
     if (g <= cmax && g <= sms) {
       const int rr = (int)ceil_div(m, g);
@@ -1551,8 +1575,8 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
     cudaStreamSynchronize(st);
     unsigned long long h[8] = {0};
     cudaMemcpy(h, dbg, sizeof(h), cudaMemcpyDeviceToHost);
-    fprintf(stderr, "panel phases (Mcycles summed over CTAs): publish %.1f barrier %.1f reduce %.1f urow %.1f book %.1f update %.1f\n",
-            h[0] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6, h[4] / 1e6, h[5] / 1e6);
+    fprintf(stderr, "panel phases (Mcycles summed over CTAs): publish %.1f deferred-update %.1f wait %.1f reduce %.1f urow %.1f update %.1f\n",
+            h[0] / 1e6, h[4] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6, h[5] / 1e6);
     cudaMemset(dbg, 0, sizeof(h));
   }
   finalize_stats_kernel<<<1, 1, 0, st>>>(ws.bits, stats);
