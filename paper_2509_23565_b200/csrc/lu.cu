@@ -642,6 +642,8 @@ constexpr size_t TRSM_SMEM = sizeof(double) * (TRSM_W * TRSM_W + TRSM_W * TRSM_C
 // ..., so the result does not depend on how the columns are partitioned.
 constexpr int TRSMF_THREADS = 256;
 constexpr int TRSMF_MAXJB = 1024;
+constexpr int TRSMF_RPT = (TRSMF_MAXJB - 64 + TRSMF_THREADS - 1) / TRSMF_THREADS;  // rows/thread
+constexpr int TRSMF_KB = 16;  // L columns per load batch
 template <int NC>
 __global__ void __launch_bounds__(TRSMF_THREADS) trsm_fused_kernel(
     const double* __restrict__ L, int64_t ldl, int jb, double* __restrict__ B, int64_t ldb,
@@ -689,26 +691,43 @@ __global__ void __launch_bounds__(TRSMF_THREADS) trsm_fused_kernel(
       if (lane + 32 < w) sB[(r0 + lane + 32) * NC + c] = v1;
     }
     __syncthreads();
-    for (int r = r0 + w + tid; r < jb; r += TRSMF_THREADS) {
-      double b[NC];
+    // rows below the block: each thread owns up to TRSMF_RPT rows and issues
+    // the L loads of all of them per batch of TRSMF_KB columns (one L2 round
+    // trip per batch instead of one per row and batch)
+    {
+      double b[TRSMF_RPT][NC];
+      int rr[TRSMF_RPT];
 #pragma unroll
-      for (int c = 0; c < NC; ++c) b[c] = sB[r * NC + c];
-      const double* lr = L + (int64_t)r0 * ldl + r;
-      // 16 L loads in flight per thread before their FMAs (L2 latency)
-      for (int k0 = 0; k0 < w; k0 += 16) {
-        double l[16];
+      for (int q = 0; q < TRSMF_RPT; ++q) {
+        rr[q] = r0 + w + tid + q * TRSMF_THREADS;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) l[u] = k0 + u < w ? __ldg(lr + (int64_t)(k0 + u) * ldl) : 0.0;
+        for (int c = 0; c < NC; ++c) b[q][c] = rr[q] < jb ? sB[rr[q] * NC + c] : 0.0;
+      }
+      for (int k0 = 0; k0 < w; k0 += TRSMF_KB) {
+        double l[TRSMF_RPT][TRSMF_KB];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
+        for (int q = 0; q < TRSMF_RPT; ++q)
+#pragma unroll
+          for (int u = 0; u < TRSMF_KB; ++u)
+            l[q][u] = (rr[q] < jb && k0 + u < w) ? __ldg(L + (int64_t)(r0 + k0 + u) * ldl + rr[q])
+                                                 : 0.0;
+#pragma unroll
+        for (int u = 0; u < TRSMF_KB; ++u) {
           if (k0 + u < w) {
 #pragma unroll
-            for (int c = 0; c < NC; ++c) b[c] = fma(-l[u], sB[(r0 + k0 + u) * NC + c], b[c]);
+            for (int c = 0; c < NC; ++c) {
+              const double x = sB[(r0 + k0 + u) * NC + c];
+#pragma unroll
+              for (int q = 0; q < TRSMF_RPT; ++q) b[q][c] = fma(-l[q][u], x, b[q][c]);
+            }
           }
         }
       }
 #pragma unroll
-      for (int c = 0; c < NC; ++c) sB[r * NC + c] = b[c];
+      for (int q = 0; q < TRSMF_RPT; ++q)
+        if (rr[q] < jb)
+#pragma unroll
+          for (int c = 0; c < NC; ++c) sB[rr[q] * NC + c] = b[q][c];
     }
     __syncthreads();
   }
