@@ -56,8 +56,8 @@ constexpr int SWAP_MAX = 2048;            // max entries of a composed swap list
 
 // ------------------------------------------------------------------ grid barrier
 struct GridBar {
-  unsigned count;
-  unsigned gen;
+  unsigned count;  // arrivals; reset before every window launch
+  unsigned pad;
 };
 
 // np.argmax(|col|) order: larger magnitude wins, ties -> smaller logical position;
@@ -100,7 +100,6 @@ struct PanelArgs {
   int32_t* info;
   GridBar* bar;
   double* cand;  // [2][gridDim][CAND_STRIDE]
-  unsigned epoch;  // unique per window launch: candidate tags are epoch*64 + step + 1
   int32_t* list_dst;  // gather list of this window's interchanges (rows outside
   int32_t* list_src;  // the window columns): new_row[dst] = old_row[src]
   int32_t* list_cnt;
@@ -1185,10 +1184,6 @@ int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t b
   pa.info = info;
   pa.bar = ws.bar;
   pa.cand = ws.cand;
-  static unsigned epoch = 0;
-  epoch = (epoch + 1) & 0x3ffffff;
-  if (epoch == 0) epoch = 1;
-  pa.epoch = epoch;
   pa.list_dst = ws.swap_dst;
   pa.list_src = ws.swap_src;
   pa.list_cnt = ws.swap_cnt;
