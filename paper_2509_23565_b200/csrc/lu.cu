@@ -585,6 +585,45 @@ __global__ void __launch_bounds__(LSWP_WARPS * 32) laswp_list_kernel(
   }
 }
 
+// Register variant: each warp holds one column's <= 2*COMPOSE_MAX source
+// values in registers (64 per lane, all loads in flight at once), then writes
+// the destinations.  No staging buffer, so 8 warps per CTA and one column's
+// whole gather is a single memory round trip.
+constexpr int LSWR_WARPS = 8;
+constexpr int LSWR_PER_LANE = LSWP_MAX / 32;
+__global__ void __launch_bounds__(LSWR_WARPS * 32, 1) laswp_list_reg_kernel(
+    double* __restrict__ a, int64_t lda, const int32_t* __restrict__ dst,
+    const int32_t* __restrict__ src, const int32_t* __restrict__ count, int64_t c0a, int64_t c1a,
+    int64_t c0b, int64_t c1b) {
+  __shared__ int32_t sd[LSWP_MAX];
+  __shared__ int32_t ss[LSWP_MAX];
+  const int cnt = *count;
+  if (cnt == 0) return;
+  for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+    sd[e] = dst[e];
+    ss[e] = src[e];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t na = c1a - c0a, nbb = c1b - c0b;
+  for (int64_t ci = (int64_t)blockIdx.x * LSWR_WARPS + wid; ci < na + nbb;
+       ci += (int64_t)gridDim.x * LSWR_WARPS) {
+    const int64_t col = ci < na ? c0a + ci : c0b + (ci - na);
+    double* colp = a + col * lda;
+    double v[LSWR_PER_LANE];
+#pragma unroll
+    for (int u = 0; u < LSWR_PER_LANE; ++u) {
+      const int e = lane + 32 * u;
+      v[u] = e < cnt ? colp[ss[e]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < LSWR_PER_LANE; ++u) {
+      const int e = lane + 32 * u;
+      if (e < cnt) colp[sd[e]] = v[u];
+    }
+  }
+}
+
 // ---------------------------------------------------------------- small trsm
 // B[0:w, c] <- L^{-1} B[0:w, c], L the unit-lower w x w block (w <= TRSM_W).
 // One thread per right-hand-side column, the column held in registers, L in
@@ -1238,10 +1277,18 @@ int laswp_ipiv(double* a, int64_t lda, int64_t c0a, int64_t c1a, int64_t c0b, in
   } stop{prof_start(st), st};
   compose_ipiv_kernel<<<1, 256, 0, st>>>(ipiv, npiv, k1, ws.cdst, ws.csrc, ws.ccnt);
   OZ_CHECK_LAUNCH();
-  int64_t blocks = ceil_div(ncols, LSWP_WARPS);
-  if (blocks > sm_count() * 2) blocks = sm_count() * 2;
-  laswp_list_kernel<<<(unsigned)blocks, LSWP_WARPS * 32, LSWP_SMEM, st>>>(
-      a, lda, ws.cdst, ws.csrc, ws.ccnt, c0a, c1a, c0b, c1b);
+  static const bool smem_variant = getenv("OZ_LASWP_SMEM") != nullptr;  // tuning
+  if (smem_variant) {
+    int64_t blocks = ceil_div(ncols, LSWP_WARPS);
+    if (blocks > sm_count() * 2) blocks = sm_count() * 2;
+    laswp_list_kernel<<<(unsigned)blocks, LSWP_WARPS * 32, LSWP_SMEM, st>>>(
+        a, lda, ws.cdst, ws.csrc, ws.ccnt, c0a, c1a, c0b, c1b);
+  } else {
+    int64_t blocks = ceil_div(ncols, LSWR_WARPS);
+    if (blocks > sm_count()) blocks = sm_count();
+    laswp_list_reg_kernel<<<(unsigned)blocks, LSWR_WARPS * 32, 0, st>>>(
+        a, lda, ws.cdst, ws.csrc, ws.ccnt, c0a, c1a, c0b, c1b);
+  }
   OZ_CHECK_LAUNCH();
   return OZ_OK;
 }
