@@ -436,7 +436,7 @@ def run_distributed(args, rank, world):
     gemm_ms, gemm_ops = prof[0], prof[2]
     achieved = gemm_ops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     kinds = ["emu_gemm", "panel", "schur_dgemm", "split", "laswp", "trsm", "solve", "other",
-             "swap_compose", "panel_dgemm", "trsm_dgemm", "-"]
+             "swap_compose", "panel_dgemm", "trsm_dgemm", "emu_gemm_sm_weighted"]
     breakdown = {kinds[i]: {"ms_per_step": prof[3 * i] / args.steps,
                             "launches_per_step": prof[3 * i + 1] / args.steps}
                  for i in range(12) if prof[3 * i + 1] > 0}
@@ -620,12 +620,15 @@ def run_ours(args, rank, world):
         return
     peaks, peak_kind = load_peaks()
     kinds = ["emu_gemm", "panel", "schur_dgemm", "split", "laswp", "trsm", "solve", "other",
-             "swap_compose", "panel_dgemm", "trsm_dgemm", "-"]
+             "swap_compose", "panel_dgemm", "trsm_dgemm", "emu_gemm_sm_weighted"]
     breakdown = {kinds[i]: {"ms_per_step": prof[3 * i] / args.steps,
                             "launches_per_step": prof[3 * i + 1] / args.steps}
                  for i in range(12) if prof[3 * i + 1] > 0}
     gemm_ms, gemm_launch, gemm_ops = prof[0], prof[1], prof[2]
     achieved = gemm_ops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    # the look-ahead runs most GEMM launches on 148 - S SMs (the panel has S):
+    # time-weighted share of the SMs the GEMM may use
+    sm_share = prof[33] / gemm_ms if gemm_ms > 0 and prof[33] > 0 else 1.0
     peak = 2.0 * float(peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"])
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
@@ -657,7 +660,9 @@ def run_ours(args, rank, world):
                                "recombine); achieved = INT8 ops (2*pairs*m*n*nb) / event time",
                      "peak_source": f"2 x bf16_tflops_sustained of {peak_kind} "
                                     f"MEASURED_PEAKS.json (dense int8 = 2x bf16 on sm_100)",
-                     "launches": gemm_launch / args.steps},
+                     "launches": gemm_launch / args.steps,
+                     "sm_share": sm_share,
+                     "frac_of_sms_used": (achieved / (peak * sm_share)) if achieved else None},
         "cpu_baseline": {"value": cpu_v, "unit": "TFLOP/s", "cores": cores, "kind": "port",
                          "sample": f"oracle LU factor+solve U(-1/2,1/2) n={args.cpu_n} "
                                    f"nb={min(nb, args.cpu_n)} k={k} on host cores "

@@ -31,6 +31,7 @@ struct ProfEntry {
   cudaEvent_t a = nullptr, b = nullptr;
   int kind = 0;
   double work = 0.0;
+  int sms = 0;  // SMs the launch may use (0: all)
   bool done = false;
 };
 static std::mutex g_prof_mu;
@@ -52,13 +53,14 @@ int prof_start(cudaStream_t st) {
   return tag;
 }
 
-void prof_stop(int tag, cudaStream_t st, int kind, double work) {
+void prof_stop(int tag, cudaStream_t st, int kind, double work, int sms) {
   if (tag < 0) return;
   std::lock_guard<std::mutex> lk(g_prof_mu);
   ProfEntry& e = g_prof[tag];
   cudaEventRecord(e.b, st);
   e.kind = kind;
   e.work = work;
+  e.sms = sms;
   e.done = true;
 }
 
@@ -145,6 +147,13 @@ extern "C" int oz_prof_summary(double* out) {
     out[3 * e.kind] += ms;
     out[3 * e.kind + 1] += 1.0;
     out[3 * e.kind + 2] += e.work;
+    if (e.kind == oz::PROF_EMU_GEMM) {  // SM-share-weighted time of the emulated GEMM
+      const int all = oz::sm_count();
+      const int used = e.sms > 0 && e.sms < all ? e.sms : all;
+      out[3 * oz::PROF_GEMM_SMS] += ms * (double)used / all;
+      out[3 * oz::PROF_GEMM_SMS + 1] += 1.0;
+      out[3 * oz::PROF_GEMM_SMS + 2] += e.work;
+    }
   }
   return OZ_OK;
 }

@@ -39,9 +39,11 @@ void count_launch();
 // oz_prof_enable(); used by bench.py for the roofline of the dominant kernel.
 enum ProfKind { PROF_EMU_GEMM = 0, PROF_PANEL = 1, PROF_DGEMM = 2, PROF_SPLIT = 3,
                 PROF_LASWP = 4, PROF_TRSM = 5, PROF_SOLVE = 6, PROF_OTHER = 7,
-                PROF_COMPOSE = 8, PROF_DGEMM_PANEL = 9, PROF_DGEMM_TRSM = 10, PROF_KINDS = 12 };
+                PROF_COMPOSE = 8, PROF_DGEMM_PANEL = 9, PROF_DGEMM_TRSM = 10,
+                PROF_GEMM_SMS = 11,  // emulated GEMM time x (SMs it may use / all SMs)
+                PROF_KINDS = 12 };
 int prof_start(cudaStream_t st);
-void prof_stop(int tag, cudaStream_t st, int kind, double work);
+void prof_stop(int tag, cudaStream_t st, int kind, double work, int sms = 0);
 
 #define OZ_REQUIRE(cond, code, ...)                                               \
   do {                                                                            \

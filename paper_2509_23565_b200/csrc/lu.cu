@@ -1424,7 +1424,7 @@ int schur_cols(const Schur& s, int64_t c0, int64_t c1, const LuWs& ws, cudaStrea
                          ws.slB + c0 * ws.ldK, ws.ldK, s.ncols * ws.ldK, s.k, ws.expB + c0,
                          s.npairs, s.pa, s.pb, s.ps, s.q, -1.0, 1.0, c, s.lda22, 1, s.growth,
                          st, max_ctas));
-  prof_stop(tag, st, PROF_EMU_GEMM, 2.0 * s.npairs * s.m * nc * s.jb);
+  prof_stop(tag, st, PROF_EMU_GEMM, 2.0 * s.npairs * s.m * nc * s.jb, max_ctas);
   return OZ_OK;
 }
 
