@@ -196,6 +196,8 @@ int oz_copy2d(const double* src, int64_t rows, int64_t cols, int64_t src_rs, int
  *                 (solve.py:66-91); interchanges applied to the panel columns
  *                 only.  ipiv[0..jb) <- global pivot rows; info <- first zero
  *                 pivot (global column + 1); growth_bits <- max |entry| seen.
+ *                 max_ctas > 0 keeps every kernel of the panel to that many
+ *                 CTAs (a look-ahead panel beside a trailing update).
  * oz_laswp:       apply ipiv[0..npiv) (rows k1.., global values) as
  *                 sequential interchanges to columns [c0a,c1a) U [c0b,c1b)
  *                 (solve.py:80-82 whole-row swaps; LAPACK dlaswp); npiv <= 1024.
@@ -210,7 +212,11 @@ int oz_lu_ws_init(void* workspace, size_t workspace_bytes, int64_t ws_n, int64_t
 int oz_lu_panel(double* a, int64_t lda, int64_t m, int64_t jb, int64_t base, int32_t* ipiv,
                 int32_t* info, unsigned long long* growth_bits, void* workspace,
                 size_t workspace_bytes, int64_t ws_n, int64_t ws_nb, int ws_slices,
-                void* stream);
+                int max_ctas, void* stream);
+/* SMs the look-ahead model gives a panel of m rows factored beside a trailing
+ * update of m x ncols (0: no look-ahead); npairs = 0 for the native backend.
+ * With ncols = m it is the single-GPU driver's split. */
+int oz_lookahead_sms(int64_t m, int64_t ncols, int64_t nb, int npairs);
 int oz_laswp(double* a, int64_t lda, int64_t c0a, int64_t c1a, int64_t c0b, int64_t c1b,
              int64_t k1, const int32_t* ipiv, int npiv, void* workspace,
              size_t workspace_bytes, int64_t ws_n, int64_t ws_nb, int ws_slices, void* stream);

@@ -53,7 +53,7 @@ _SIGNATURES = {
     # step-level LU (distributed driver, hpl.py)
     "oz_lu_ws_init": [_vp, C.c_size_t, _i64, _i64, _int, _vp],
     "oz_lu_panel": [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, C.c_size_t, _i64, _i64,
-                    _int, _vp],
+                    _int, _int, _vp],
     "oz_laswp": [_vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _int, _vp, C.c_size_t, _i64, _i64,
                  _int, _vp],
     "oz_trsm_lunit": [_vp, _i64, _i64, _vp, _i64, _i64, _vp],
@@ -77,9 +77,11 @@ _SIGNATURES = {
     "oz_scatter_rows": [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp],
     "oz_scatter_vec": [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp],
     "oz_gemm_starts_dump": [],
+    "oz_lookahead_sms": [_i64, _i64, _i64, _int],
 }
 _RESTYPES = {
     "oz_launch_count": C.c_longlong,
+    "oz_lookahead_sms": C.c_int,
     "oz_split_aux_bytes": C.c_size_t,
     "oz_lu_workspace_bytes": C.c_size_t,
     "oz_lu_solve_workspace_bytes": C.c_size_t,

@@ -1458,10 +1458,11 @@ int la_step() {  // tuning: granularity of the look-ahead SM search
   static const int v = getenv("OZ_LA_STEP") ? atoi(getenv("OZ_LA_STEP")) : 2;
   return v > 0 ? v : 2;  // measured: 2 vs 8 -> 497 vs 499-505 ms at n = 32768
 }
-int lookahead_split(int setting, int64_t m, int64_t nb, int npairs, int sms) {
+int lookahead_split(int setting, int64_t m, int64_t nb, int npairs, int sms, int64_t ncols = -1) {
   if (setting >= 0) return setting;
   if (npairs <= 0) return 40;  // native DGEMM Schur update: fixed split (measured best)
-  const double ops = 2.0 * npairs * (double)m * (double)m * (double)nb;
+  if (ncols < 0) ncols = m;    // single GPU: the whole trailing matrix
+  const double ops = 2.0 * npairs * (double)m * (double)ncols * (double)nb;
   const double rate = 2.3e15;  // emulated INT8 ops/s on the full chip
   int best = 16;
   double best_t = 1e30;
@@ -1796,17 +1797,26 @@ extern "C" int oz_lu_ws_init(void* ws, size_t ws_bytes, int64_t n, int64_t nb, i
   return OZ_OK;
 }
 
+// The look-ahead SM split for a panel of m rows beside a trailing update of
+// ncols columns (the single-GPU driver's model; 0 = no look-ahead).
+extern "C" int oz_lookahead_sms(int64_t m, int64_t ncols, int64_t nb, int npairs) {
+  const int setting = oz::lookahead_sms();
+  if (setting == 0) return 0;
+  return oz::lookahead_split(setting, m, nb, npairs, oz::sm_count(), ncols);
+}
+
 extern "C" int oz_lu_panel(double* a, int64_t lda, int64_t m, int64_t jb, int64_t base,
                            int32_t* ipiv, int32_t* info, unsigned long long* growth_bits,
                            void* ws, size_t ws_bytes, int64_t ws_n, int64_t ws_nb,
-                           int ws_slices, void* stream) {
+                           int ws_slices, int max_ctas, void* stream) {
   using namespace oz;
   OZ_REQUIRE(m >= jb && jb >= 1 && jb <= COMPOSE_MAX && lda >= m, OZ_INVALID_PARAMS,
              "bad panel shape m=%lld jb=%lld lda=%lld", (long long)m, (long long)jb,
              (long long)lda);
   LuWs w;
   OZ_TRY(ws_view(ws, ws_bytes, ws_n, ws_nb, ws_slices, &w));
-  return panel_factor(a, lda, m, jb, base, ipiv, info, growth_bits, w, as_stream(stream));
+  return panel_factor(a, lda, m, jb, base, ipiv, info, growth_bits, w, as_stream(stream),
+                      max_ctas > 0 ? max_ctas : 0);
 }
 
 extern "C" int oz_laswp(double* a, int64_t lda, int64_t c0a, int64_t c1a, int64_t c0b,

@@ -190,6 +190,23 @@ class DeviceOps:
         self.tsb = int(_lib.query("oz_lu_solve_workspace_bytes", nb))
         self.tws = t.zeros((self.tsb // 4 + 1,), dtype=t.int32, device=dev)
         self.flag = t.zeros((1,), dtype=t.int32, device=dev)
+        self.side = t.cuda.Stream()   # look-ahead panel (+ its broadcast) beside the update
+
+    def lookahead_sms(self, m: int, ncols: int) -> int:
+        """Look-ahead SMs for a panel of m rows beside this rank's update of
+        ncols trailing columns (the single-GPU driver's model)."""
+        return int(_lib.query("oz_lookahead_sms", m, ncols, self.nb,
+                              len(self.pa) if self.emulated else 0))
+
+    # -- streams
+    def side_stream(self):
+        """Context: run the enclosed calls on the side stream, after the work
+        already queued on the compute stream."""
+        self.side.wait_stream(self.t.cuda.current_stream())
+        return self.t.cuda.stream(self.side)
+
+    def join_side(self) -> None:
+        self.t.cuda.current_stream().wait_stream(self.side)
 
     # -- addressing
     def _a(self, lc: int, row: int) -> int:
@@ -231,10 +248,11 @@ class DeviceOps:
             _lib.call("oz_max_abs_bits", self.slab.data_ptr(), self.n, self.ncl, 1, self.n, 0,
                       self.bits.data_ptr() + 8, self._st())
 
-    def panel(self, lc: int, j: int, jb: int, slot: int = 0) -> None:
+    def panel(self, lc: int, j: int, jb: int, slot: int = 0, max_ctas: int = 0) -> None:
         _lib.call("oz_lu_panel", self._a(lc, j), self.n, self.n - j, jb, j,
                   self.ipiv_buf[slot].data_ptr(), self.info.data_ptr(), self.bits.data_ptr(),
-                  self.ws.data_ptr(), self.wsb, self.n, self.nb, self.planes, self._st())
+                  self.ws.data_ptr(), self.wsb, self.n, self.nb, self.planes, max_ctas,
+                  self._st())
         # triu of the panel's diagonal block: finalized U rows (solve.py:135-137)
         _lib.call("oz_max_abs_bits", self._a(lc, j), jb, jb, 1, self.n, 1,
                   self.bits.data_ptr(), self._st())
@@ -310,28 +328,33 @@ class DeviceOps:
 
 # ------------------------------------------------------------ the driver
 def factor_block_cyclic(ops, comm, n: int, nb: int, lookahead: bool = True,
-                        reserve_sms: int = 16):
+                        reserve_sms: int | None = None):
     """Blocked right-looking LU (solve.py:94-140) of the distributed matrix in
     ops' local slabs.  Returns (ipiv int32[n] global LAPACK-style, growth).
 
     Look-ahead (depth 1): the owner of panel b+1 updates that panel's columns
-    first, factors it into the other panel slot and starts its broadcast
-    (asynchronously on NCCL) before updating the rest of its columns on
-    sms - reserve_sms CTAs, so the other ranks find panel b+1 ready when they
-    finish step b.  The arithmetic is identical with or without it."""
+    first, then factors it on a side stream with S CTAs and starts its
+    broadcast from there (asynchronously on NCCL), while its compute stream
+    updates the rest of its columns on sms - S CTAs; the other ranks find
+    panel b+1 ready when they finish step b.  S (reserve_sms, default: the
+    look-ahead model for this rank's share of the update, oz_lookahead_sms)
+    also caps the panel's own kernels; on one rank it is the single-GPU
+    driver's split, so the factors equal the single-GPU LU's bit for bit.  The
+    last panel is factored after the update, as there."""
     Q, q = comm.size, comm.rank
     ncl = local_ncols(n, nb, Q, q)
     nblk = -(-n // nb)
     ops.begin()
     sends = {}                                   # slot -> in-flight early broadcast handles
     early = set()                                # panels already factored and sent
+    side_pending = False                         # side-stream panel not yet joined
 
-    def factor_and_send(b, lc, slot, async_ok):
+    def factor_and_send(b, lc, slot, async_ok, max_ctas=0):
         jj = b * nb
         jjb = min(nb, n - jj)
         for h in sends.pop(slot, ()):            # the slot's previous send must be done
             h.wait()
-        ops.panel(lc, jj, jjb, slot)
+        ops.panel(lc, jj, jjb, slot, max_ctas)
         if async_ok:
             pb, ip = ops.panel_buffers(jj, jjb, slot)
             sends[slot] = [h for h in (comm.bcast_async(pb, q), comm.bcast_async(ip, q)) if h]
@@ -345,6 +368,9 @@ def factor_block_cyclic(ops, comm, n: int, nb: int, lookahead: bool = True,
         owner = jblk % Q
         slot = jblk % 2
         lc = (jblk // Q) * nb                   # the panel's local column on its owner
+        if side_pending:                         # this panel came from the side stream
+            ops.join_side()
+            side_pending = False
         if jblk not in early:                    # receive (or, on the owner, send) now
             pbuf, ipiv = ops.panel_buffers(j, jb, slot)
             comm.bcast(pbuf, owner)              # L11/L21 of the factored panel
@@ -364,10 +390,16 @@ def factor_block_cyclic(ops, comm, n: int, nb: int, lookahead: bool = True,
             if mine_next:
                 jb2 = min(nb, n - nxt * nb)       # the next panel = my first trailing columns
                 ops.schur_cols(j, jb, lstart, nt, 0, jb2, slot)
-                if lookahead:
-                    factor_and_send(nxt, lstart, nxt % 2, Q > 1)
-                    ops.schur_cols(j, jb, lstart, nt, jb2, nt, slot,
-                                   reserve_sms if Q > 1 else 0)
+                m_next = n - nxt * nb
+                S = 0
+                if lookahead and m_next > jb2:
+                    S = (ops.lookahead_sms(m_next, nt) if reserve_sms is None
+                         else reserve_sms)
+                if S > 0:
+                    with ops.side_stream():
+                        factor_and_send(nxt, lstart, nxt % 2, Q > 1, S)
+                    side_pending = True
+                    ops.schur_cols(j, jb, lstart, nt, jb2, nt, slot, S)
                 else:
                     ops.schur_cols(j, jb, lstart, nt, jb2, nt, slot)
                     factor_and_send(nxt, lstart, nxt % 2, False)
@@ -375,6 +407,8 @@ def factor_block_cyclic(ops, comm, n: int, nb: int, lookahead: bool = True,
                 ops.schur_cols(j, jb, lstart, nt, 0, nt, slot)
         elif mine_next:                          # pragma: no cover (no trailing columns)
             factor_and_send(nxt, lstart, nxt % 2, False)
+    if side_pending:
+        ops.join_side()
     for hs in sends.values():
         for h in hs:
             h.wait()

@@ -38,13 +38,24 @@ class NumpyOps:
         return (torch.from_numpy(self.slab @ x if self.ncl else np.zeros(self.n)),
                 torch.from_numpy(np.abs(self.slab).sum(axis=1)))
 
+    def lookahead_sms(self, m, ncols):
+        return 16
+
+    # -- streams (the device ops run the look-ahead panel on a side stream)
+    def side_stream(self):
+        import contextlib
+        return contextlib.nullcontext()
+
+    def join_side(self):
+        pass
+
     # -- factorization
     def begin(self):
         self.info = 0
         self.seen = 0.0
         self.top = float(np.abs(self.slab).max()) if self.ncl else 0.0
 
-    def panel(self, lc, j, jb, slot=0):
+    def panel(self, lc, j, jb, slot=0, max_ctas=0):
         n = self.n
         a = self.slab
         for t in range(j, j + jb):                               # solve.py:75-90
