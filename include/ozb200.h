@@ -178,6 +178,22 @@ int oz_generate(int kind, int64_t n, int64_t depth, int64_t block, double alpha,
                 uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                 double* out, int64_t row_stride, int64_t col_stride, void* stream);
 
+/* oz_lu_factor while the caller is still uploading the matrix: only columns
+ * [0, 2*nb) must be in place on entry; the rest once cols_ready_event (a
+ * cudaEvent_t) has fired.  Panel 0, the update of panel 1's columns and panel
+ * 1 overlap the upload. */
+int oz_lu_factor_overlapped(double* a, int64_t n, int64_t lda, int64_t nb, int backend,
+                            int num_slices, int slice_bits, int npairs, const int32_t* pair_a,
+                            const int32_t* pair_b, const int32_t* pair_shift, int32_t* ipiv,
+                            double* stats, int32_t* info, void* workspace, size_t ws_bytes,
+                            void* cols_ready_event, void* stream);
+/* *flag <- 1 if any entry is NaN or infinite (flag is not cleared). */
+int oz_nonfinite_flag(const double* a, int64_t m, int64_t n, int64_t row_stride,
+                      int64_t col_stride, int32_t* flag, void* stream);
+/* cudaMemcpy2DAsync host -> device (a column block of a row-major host matrix). */
+int oz_memcpy2d_h2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                    size_t height, void* stream);
+
 /* Out-of-place strided copy (layout change), e.g. row-major -> column-major. */
 int oz_copy2d(const double* src, int64_t rows, int64_t cols, int64_t src_rs, int64_t src_cs,
               double* dst, int64_t dst_rs, int64_t dst_cs, void* stream);

@@ -30,6 +30,26 @@
 
 namespace oz {
 
+// Temporary buffers of the residual / row-sum paths come from the device's
+// default stream-ordered pool; keep its memory mapped between calls instead
+// of returning it to the driver at every synchronization.
+void keep_pool_mapped() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+  done = true;
+}
+
+}  // namespace oz
+
+namespace oz {
+
 int dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha, const double* a,
           int64_t lda, const double* b, int64_t ldb, double beta, double* c, int64_t ldc,
           cudaStream_t st, int sm_target = 0);
@@ -1526,10 +1546,14 @@ int side_stream(SideStream** out) {
 }  // namespace
 
 // ------------------------------------------------------------------- LU driver
+// cols_ready (may be null): the caller is still uploading the matrix; only the
+// first 2*nb columns are in place on entry, the rest once cols_ready fires.
+// Panel 0, the update of panel 1's columns and panel 1 (side stream) overlap
+// the upload; every other column is first touched after waiting for it.
 int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k, int q,
               int npairs, const int32_t* pa, const int32_t* pb, const int32_t* ps,
               int32_t* ipiv, double* stats, int32_t* info, void* workspace, size_t ws_bytes,
-              cudaStream_t st) {
+              cudaStream_t st, cudaEvent_t cols_ready = nullptr) {
   OZ_REQUIRE(n >= 1, OZ_INVALID_PARAMS, "empty matrices are not supported");
   OZ_REQUIRE(nb >= 1 && nb <= n, OZ_INVALID_PARAMS, "lu_block must be in 1..%lld, got %lld",
              (long long)n, (long long)nb);
@@ -1545,7 +1569,16 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
   OZ_CHECK_CUDA(cudaMemsetAsync(ws.cand, 0, sizeof(double) * 2 * 1024 * CAND_STRIDE, st));
   OZ_CHECK_CUDA(cudaMemsetAsync(ws.bits, 0, 4 * sizeof(unsigned long long), st));
   OZ_CHECK_CUDA(cudaMemsetAsync(info, 0, sizeof(int32_t), st));
-  OZ_TRY(max_abs(a, n, n, 1, lda, 0, 0, ws.bits + 1, st));
+  int64_t ready_cols = cols_ready ? std::min<int64_t>(n, 2 * nb) : n;
+  OZ_TRY(max_abs(a, n, ready_cols, 1, lda, 0, 0, ws.bits + 1, st));
+  auto wait_cols = [&]() -> int {  // the rest of the matrix: max |A| before any update
+    if (ready_cols < n) {
+      OZ_CHECK_CUDA(cudaStreamWaitEvent(st, cols_ready, 0));
+      OZ_TRY(max_abs(a + ready_cols * lda, n, n - ready_cols, 1, lda, 0, 0, ws.bits + 1, st));
+      ready_cols = n;
+    }
+    return OZ_OK;
+  };
 
   const int la_setting = lookahead_sms();
   SideStream* side = nullptr;
@@ -1571,6 +1604,7 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
     const bool la = side != nullptr && rest > jb2 && backend != 2;
     tr.mark(st);  // 0 step start
     // ---- the panel's interchanges: whole-row swaps (solve.py:80-82)
+    if (!la) OZ_TRY(wait_cols());
     if (la)
       OZ_TRY(laswp_ipiv(a, lda, j + jb, j + jb + jb2, 0, 0, j, ipiv + j, (int)jb, ws, st));
     else
@@ -1595,6 +1629,7 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
                             side->st, la_sms));
         OZ_CHECK_CUDA(cudaEventRecord(side->done, side->st));
         tr.mark(side->st);  // 5 side stream: panel done
+        OZ_TRY(wait_cols());
         OZ_TRY(laswp_ipiv(a, lda, 0, j, j + jb + jb2, n, j, ipiv + j, (int)jb, ws, st));
         tr.mark_sub(st);
         OZ_TRY(trsm_blocked(a, lda, j, jb, a12 + jb2 * lda, lda, rest - jb2, st));
@@ -1701,6 +1736,25 @@ extern "C" int oz_lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int b
                        pair_shift, ipiv, stats, info, workspace, ws_bytes, oz::as_stream(stream));
 }
 
+extern "C" int oz_lu_factor_overlapped(double* a, int64_t n, int64_t lda, int64_t nb,
+                                       int backend, int num_slices, int slice_bits, int npairs,
+                                       const int32_t* pair_a, const int32_t* pair_b,
+                                       const int32_t* pair_shift, int32_t* ipiv, double* stats,
+                                       int32_t* info, void* workspace, size_t ws_bytes,
+                                       void* cols_ready_event, void* stream) {
+  return oz::lu_factor(a, n, lda, nb, backend, num_slices, slice_bits, npairs, pair_a, pair_b,
+                       pair_shift, ipiv, stats, info, workspace, ws_bytes, oz::as_stream(stream),
+                       reinterpret_cast<cudaEvent_t>(cols_ready_event));
+}
+
+extern "C" int oz_memcpy2d_h2d(void* dst, size_t dpitch, const void* src, size_t spitch,
+                               size_t width, size_t height, void* stream) {
+  using namespace oz;
+  OZ_CHECK_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height,
+                                  cudaMemcpyHostToDevice, as_stream(stream)));
+  return OZ_OK;
+}
+
 extern "C" size_t oz_lu_solve_workspace_bytes(int64_t n) {
   return sizeof(int) * (2 + oz::ceil_div(n, 64) + 16);
 }
@@ -1724,6 +1778,7 @@ extern "C" int oz_residual_norms(const double* a, int64_t n, int64_t row_stride,
   const int nchunks = (int)ceil_div(n, GEMV_CHUNK);
   double* part = nullptr;
   unsigned long long* bits = nullptr;
+  keep_pool_mapped();
   OZ_CHECK_CUDA(cudaMallocAsync(&part, sizeof(double) * 2 * nchunks * n, st));
   OZ_CHECK_CUDA(cudaMallocAsync(&bits, sizeof(unsigned long long) * 4, st));
   OZ_CHECK_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned long long) * 4, st));
@@ -1744,6 +1799,7 @@ extern "C" int oz_row_sums(const double* a, int64_t n, int64_t row_stride, int64
   cudaStream_t st = as_stream(stream);
   const int nchunks = (int)ceil_div(n, GEMV_CHUNK);
   double* part = nullptr;
+  keep_pool_mapped();
   OZ_CHECK_CUDA(cudaMallocAsync(&part, sizeof(double) * nchunks * n, st));
   int s = gemv_rows(a, n, row_stride, col_stride, nullptr, nullptr, out, nullptr, nullptr, part,
                     st);
@@ -1857,6 +1913,36 @@ extern "C" int oz_schur_update(int backend, int64_t m, int64_t ncols, int64_t jb
 }
 
 // max |a| (optionally only the upper trapezoid c >= r) folded into *bits
+namespace oz {
+namespace {
+__global__ void nonfinite_kernel(const double* __restrict__ a, int64_t m, int64_t n, int64_t rs,
+                                 int64_t cs, int32_t* flag) {
+  bool bad = false;
+  const int64_t total = m * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / m, r = i - c * m;  // consecutive threads: consecutive rows
+    bad |= !isfinite(a[r * rs + c * cs]);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(flag, 1);
+}
+}  // namespace
+}  // namespace oz
+
+// *flag <- 1 if any entry of the m x n matrix is NaN or infinite (the
+// reference's NonFiniteEntryError check, split.py:104-105 / solve.py:107-108).
+extern "C" int oz_nonfinite_flag(const double* a, int64_t m, int64_t n, int64_t row_stride,
+                                 int64_t col_stride, int32_t* flag, void* stream) {
+  using namespace oz;
+  if (m <= 0 || n <= 0) return OZ_OK;
+  int64_t blocks = ceil_div(m * n, 256 * 8);
+  if (blocks > sm_count() * 8) blocks = sm_count() * 8;
+  nonfinite_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(a, m, n, row_stride,
+                                                                   col_stride, flag);
+  OZ_CHECK_LAUNCH();
+  return OZ_OK;
+}
+
 extern "C" int oz_max_abs_bits(const double* a, int64_t m, int64_t n, int64_t row_stride,
                                int64_t col_stride, int upper, unsigned long long* bits,
                                void* stream) {
@@ -1896,6 +1982,7 @@ extern "C" int oz_gemv_partial(const double* a, int64_t rows, int64_t cols, int6
   }
   const int nchunks = (int)ceil_div(cols, GEMV_CHUNK);
   double* part = nullptr;
+  keep_pool_mapped();
   OZ_CHECK_CUDA(cudaMallocAsync(&part, sizeof(double) * 2 * nchunks * rows, st));
   int s = gemv_rows(a, rows, row_stride, col_stride, x, nullptr, ax, nullptr, nullptr, part, st,
                     cols, asum);

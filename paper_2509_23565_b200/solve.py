@@ -110,6 +110,24 @@ def _is_host_tensor(x) -> bool:
         return False
 
 
+def _host_row_major(a):
+    """A square, C-contiguous float64 host matrix (numpy or CPU tensor) the
+    overlapped upload can read in place; None otherwise (device inputs and
+    other layouts take the plain path)."""
+    t = _dev.torch()
+    if _dev.is_device(a):
+        return None
+    if isinstance(a, t.Tensor):
+        if (a.dtype != t.float64 or a.ndim != 2 or a.shape[0] != a.shape[1] or a.shape[0] == 0
+                or not a.is_contiguous()):
+            return None
+        return a
+    if isinstance(a, np.ndarray) and a.dtype == np.float64 and a.ndim == 2 and \
+            a.shape[0] == a.shape[1] and a.shape[0] > 0 and a.flags.c_contiguous:
+        return a
+    return None
+
+
 def _upload(x):
     """numpy array or (pinned) CPU tensor -> CUDA float64 tensor."""
     t = _dev.torch()
@@ -169,9 +187,11 @@ def _backend_code(backend: GemmBackend) -> int:
     return 2 if backend.scaling is ScalingMode.GLOBAL else 1
 
 
-def factor_device(a_cm, nb: int, backend: GemmBackend):
+def factor_device(a_cm, nb: int, backend: GemmBackend, cols_ready=None):
     """In-place LU of a column-major CUDA matrix.  Returns (ipiv tensor,
-    stats tensor, info tensor) without synchronizing."""
+    stats tensor, info tensor) without synchronizing.  cols_ready: a
+    torch.cuda.Event after which columns >= 2*nb are in place (overlapped
+    upload); columns < 2*nb must be ready on the current stream."""
     t = _dev.torch()
     n = int(a_cm.shape[0])
     emulated = backend.kind is BackendKind.EMULATED_INT8
@@ -188,11 +208,62 @@ def factor_device(a_cm, nb: int, backend: GemmBackend):
     ipiv = t.empty((n,), dtype=t.int32, device="cuda")
     stats = t.zeros((4,), dtype=t.float64, device="cuda")
     info = t.zeros((1,), dtype=t.int32, device="cuda")
-    _lib.call("oz_lu_factor", a_cm.data_ptr(), n, int(a_cm.stride(1)), nb, _backend_code(backend),
-              k, backend.slice_bits, len(pa), pa.ctypes.data, pb.ctypes.data, sh.ctypes.data,
-              ipiv.data_ptr(), stats.data_ptr(), info.data_ptr(), ws.data_ptr(), ws_bytes,
-              _dev.stream())
+    if cols_ready is None:
+        _lib.call("oz_lu_factor", a_cm.data_ptr(), n, int(a_cm.stride(1)), nb,
+                  _backend_code(backend), k, backend.slice_bits, len(pa), pa.ctypes.data,
+                  pb.ctypes.data, sh.ctypes.data, ipiv.data_ptr(), stats.data_ptr(),
+                  info.data_ptr(), ws.data_ptr(), ws_bytes, _dev.stream())
+    else:
+        _lib.call("oz_lu_factor_overlapped", a_cm.data_ptr(), n, int(a_cm.stride(1)), nb,
+                  _backend_code(backend), k, backend.slice_bits, len(pa), pa.ctypes.data,
+                  pb.ctypes.data, sh.ctypes.data, ipiv.data_ptr(), stats.data_ptr(),
+                  info.data_ptr(), ws.data_ptr(), ws_bytes, cols_ready.cuda_event,
+                  _dev.stream())
     return ipiv, stats, info, ws
+
+
+_UPLOAD_STREAMS = {}
+
+
+def _upload_overlapped(host, nb: int):
+    """Row-major host matrix -> (row-major device copy, column-major working
+    copy, event 'all columns in place', non-finite flag) in column blocks: a
+    copy stream moves block c over PCIe (cudaMemcpy2DAsync) while a second
+    stream transposes block c-1 and checks it for NaN/inf; the current stream
+    waits only for the blocks covering the first two panels (solve_system then
+    factors with oz_lu_factor_overlapped)."""
+    t = _dev.torch()
+    n = int(host.shape[0])
+    dev = t.cuda.current_device()
+    if dev not in _UPLOAD_STREAMS:
+        _UPLOAD_STREAMS[dev] = (t.cuda.Stream(), t.cuda.Stream())
+    cs, ts = _UPLOAD_STREAMS[dev]
+    cur = t.cuda.current_stream()
+    ad = t.empty((n, n), dtype=t.float64, device="cuda")
+    work = t.empty((n, n), dtype=t.float64, device="cuda").t()
+    bad = t.zeros((1,), dtype=t.int32, device="cuda")
+    cs.wait_stream(cur)
+    ts.wait_stream(cur)
+    w = max(1024, nb)
+    need = min(n, 2 * nb)
+    hptr = host.data_ptr() if isinstance(host, t.Tensor) else host.ctypes.data
+    last = None
+    for c0 in range(0, n, w):
+        c1 = min(n, c0 + w)
+        _lib.call("oz_memcpy2d_h2d", ad.data_ptr() + 8 * c0, 8 * n, hptr + 8 * c0, 8 * n,
+                  8 * (c1 - c0), n, cs.cuda_stream)
+        copied = t.cuda.Event()
+        copied.record(cs)
+        ts.wait_event(copied)
+        _lib.call("oz_copy2d", ad.data_ptr() + 8 * c0, n, c1 - c0, n, 1,
+                  work.data_ptr() + 8 * n * c0, 1, n, ts.cuda_stream)
+        _lib.call("oz_nonfinite_flag", ad.data_ptr() + 8 * c0, n, c1 - c0, n, 1,
+                  bad.data_ptr(), ts.cuda_stream)
+        last = t.cuda.Event()
+        last.record(ts)
+        if c0 < need <= c1 or (c1 <= need and c1 == n):
+            cur.wait_event(last)                # the first two panels are in place
+    return ad, work, last, bad
 
 
 def ipiv_to_perm(ipiv_host: np.ndarray) -> np.ndarray:
@@ -318,15 +389,30 @@ def solve_system(a, b, lu_block: int = 64, backend: GemmBackend | None = None):
     t = _dev.torch()
     counter = FlopCounter()
     t0 = time.perf_counter()
-    ad, host = _as_square_device(a)
-    n = int(ad.shape[0])
-    bd = _vector_device(b, n, "rhs")
-    if not bool(t.isfinite(ad).all().item()):
-        raise NonFiniteEntryError("matrix contains NaN or infinite entries")
-    if not 1 <= lu_block <= n:
-        raise InvalidParamsError(f"lu_block must be in 1..{n}, got {lu_block}")
-    work = _col_major_copy(ad)
-    ipiv, stats, info, _ws = factor_device(work, lu_block, backend)
+    src = _host_row_major(a)
+    if src is not None:
+        # host matrix: overlapped upload (column blocks over PCIe while the
+        # first panels are factored); non-finite entries are caught from the
+        # max |a| folded into the upload, before any result is returned
+        n = int(src.shape[0])
+        host = True
+        if not 1 <= lu_block <= n:
+            raise InvalidParamsError(f"lu_block must be in 1..{n}, got {lu_block}")
+        bd = _vector_device(b, n, "rhs")
+        ad, work, ready, bad = _upload_overlapped(src, lu_block)
+        ipiv, stats, info, _ws = factor_device(work, lu_block, backend, cols_ready=ready)
+        if int(bad.item()):
+            raise NonFiniteEntryError("matrix contains NaN or infinite entries")
+    else:
+        ad, host = _as_square_device(a)
+        n = int(ad.shape[0])
+        bd = _vector_device(b, n, "rhs")
+        if not bool(t.isfinite(ad).all().item()):
+            raise NonFiniteEntryError("matrix contains NaN or infinite entries")
+        if not 1 <= lu_block <= n:
+            raise InvalidParamsError(f"lu_block must be in 1..{n}, got {lu_block}")
+        work = _col_major_copy(ad)
+        ipiv, stats, info, _ws = factor_device(work, lu_block, backend)
     perm, growth = _finish_factor(ipiv, stats, info)
     dperm = t.from_numpy(perm).to("cuda", non_blocking=True)
     x, flag = _solve_device(work, dperm, bd)

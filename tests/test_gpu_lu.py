@@ -234,3 +234,31 @@ def test_panel_exchange_variants(n, nb, k, tmp_path):
     assert np.array_equal(grid["ipiv"], nola["ipiv"])
     np.testing.assert_allclose(nola["lu"], grid["lu"], rtol=0,
                                atol=1e-9 * np.abs(grid["lu"]).max())
+
+
+@pytest.mark.parametrize("n,nb", [(1500, 256), (3000, 1024)])
+def test_solve_system_host_overlapped_upload_matches_device(n, nb):
+    """Host (row-major) inputs take the overlapped upload (column blocks over
+    PCIe while the first panels factor): same x bit for bit as a device input,
+    and non-finite entries still raise NonFiniteEntryError."""
+    import torch
+
+    import paper_2509_23565_b200 as oz
+    from paper_2509_23565_b200.errors import NonFiniteEntryError
+    from paper_2509_23565_b200.matgen import generate_device
+    a = generate_device(0, n, seed=5)
+    b = a.sum(1)
+    bk = oz.GemmBackend.int8(7)
+    x_dev, rep_dev = oz.solve_system(a, b, nb, bk)
+    a_np, b_np = a.cpu().numpy(), b.cpu().numpy()
+    x_np, rep_np = oz.solve_system(a_np, b_np, nb, bk)
+    pinned = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+    pinned.copy_(a.cpu())
+    x_pin, rep_pin = oz.solve_system(pinned, b_np, nb, bk)
+    assert np.array_equal(x_dev.cpu().numpy(), x_np)
+    assert np.array_equal(x_np, x_pin)
+    assert rep_np.scaled_residual == rep_dev.scaled_residual < 16.0
+    bad = a_np.copy()
+    bad[n - 3, n - 2] = np.nan                  # in the last upload block
+    with pytest.raises(NonFiniteEntryError):
+        oz.solve_system(bad, b_np, nb, bk)
