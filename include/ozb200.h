@@ -178,15 +178,16 @@ int oz_generate(int kind, int64_t n, int64_t depth, int64_t block, double alpha,
                 uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                 double* out, int64_t row_stride, int64_t col_stride, void* stream);
 
-/* oz_lu_factor while the caller is still uploading the matrix: only columns
- * [0, 2*nb) must be in place on entry; the rest once cols_ready_event (a
- * cudaEvent_t) has fired.  Panel 0, the update of panel 1's columns and panel
- * 1 overlap the upload. */
+/* oz_lu_factor while the caller is still uploading the matrix in column
+ * chunks: chunk_events[c] (cudaEvent_t) fires once columns [c*chunk_cols,
+ * (c+1)*chunk_cols) are in place.  Panel 0, the update of panel 1's columns
+ * and panel 1 start as soon as their chunks are in; step 0's update of the
+ * other columns follows the upload chunk by chunk. */
 int oz_lu_factor_overlapped(double* a, int64_t n, int64_t lda, int64_t nb, int backend,
                             int num_slices, int slice_bits, int npairs, const int32_t* pair_a,
                             const int32_t* pair_b, const int32_t* pair_shift, int32_t* ipiv,
                             double* stats, int32_t* info, void* workspace, size_t ws_bytes,
-                            void* cols_ready_event, void* stream);
+                            void* const* chunk_events, int64_t chunk_cols, void* stream);
 /* *flag <- 1 if any entry is NaN or infinite (flag is not cleared). */
 int oz_nonfinite_flag(const double* a, int64_t m, int64_t n, int64_t row_stride,
                       int64_t col_stride, int32_t* flag, void* stream);

@@ -43,7 +43,7 @@ _SIGNATURES = {
     "oz_lu_factor": [_vp, _i64, _i64, _i64, _int, _int, _int, _int, _vp, _vp, _vp, _vp, _vp,
                      _vp, _vp, C.c_size_t, _vp],
     "oz_lu_factor_overlapped": [_vp, _i64, _i64, _i64, _int, _int, _int, _int, _vp, _vp, _vp,
-                                _vp, _vp, _vp, _vp, C.c_size_t, _vp, _vp],
+                                _vp, _vp, _vp, _vp, C.c_size_t, _vp, _i64, _vp],
     "oz_memcpy2d_h2d": [_vp, C.c_size_t, _vp, C.c_size_t, C.c_size_t, C.c_size_t, _vp],
     "oz_nonfinite_flag": [_vp, _i64, _i64, _i64, _i64, _vp, _vp],
     "oz_ipiv_to_perm": [_vp, _i64, _vp],

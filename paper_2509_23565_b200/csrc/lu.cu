@@ -1546,14 +1546,16 @@ int side_stream(SideStream** out) {
 }  // namespace
 
 // ------------------------------------------------------------------- LU driver
-// cols_ready (may be null): the caller is still uploading the matrix; only the
-// first 2*nb columns are in place on entry, the rest once cols_ready fires.
-// Panel 0, the update of panel 1's columns and panel 1 (side stream) overlap
-// the upload; every other column is first touched after waiting for it.
+// chunk_ready (may be null): the caller is still uploading the matrix in
+// column chunks of chunk_cols; event c fires once columns [c*chunk_cols,
+// (c+1)*chunk_cols) are in place.  Panel 0, the update of panel 1's columns
+// and panel 1 (side stream) start as soon as their chunks are in; step 0's
+// update of every other column is streamed chunk by chunk behind the upload.
 int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k, int q,
               int npairs, const int32_t* pa, const int32_t* pb, const int32_t* ps,
               int32_t* ipiv, double* stats, int32_t* info, void* workspace, size_t ws_bytes,
-              cudaStream_t st, cudaEvent_t cols_ready = nullptr) {
+              cudaStream_t st, const cudaEvent_t* chunk_ready = nullptr,
+              int64_t chunk_cols = 0) {
   OZ_REQUIRE(n >= 1, OZ_INVALID_PARAMS, "empty matrices are not supported");
   OZ_REQUIRE(nb >= 1 && nb <= n, OZ_INVALID_PARAMS, "lu_block must be in 1..%lld, got %lld",
              (long long)n, (long long)nb);
@@ -1569,16 +1571,25 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
   OZ_CHECK_CUDA(cudaMemsetAsync(ws.cand, 0, sizeof(double) * 2 * 1024 * CAND_STRIDE, st));
   OZ_CHECK_CUDA(cudaMemsetAsync(ws.bits, 0, 4 * sizeof(unsigned long long), st));
   OZ_CHECK_CUDA(cudaMemsetAsync(info, 0, sizeof(int32_t), st));
-  int64_t ready_cols = cols_ready ? std::min<int64_t>(n, 2 * nb) : n;
-  OZ_TRY(max_abs(a, n, ready_cols, 1, lda, 0, 0, ws.bits + 1, st));
-  auto wait_cols = [&]() -> int {  // the rest of the matrix: max |A| before any update
-    if (ready_cols < n) {
-      OZ_CHECK_CUDA(cudaStreamWaitEvent(st, cols_ready, 0));
-      OZ_TRY(max_abs(a + ready_cols * lda, n, n - ready_cols, 1, lda, 0, 0, ws.bits + 1, st));
-      ready_cols = n;
+  // columns [0, ready_cols) are in place and folded into max |A|
+  int64_t ready_cols = 0;
+  auto wait_until = [&](int64_t c1) -> int {
+    if (c1 > n) c1 = n;
+    const int64_t from = ready_cols;
+    while (ready_cols < c1) {
+      if (chunk_ready) {
+        OZ_CHECK_CUDA(cudaStreamWaitEvent(st, chunk_ready[ready_cols / chunk_cols], 0));
+        ready_cols = std::min<int64_t>(n, (ready_cols / chunk_cols + 1) * chunk_cols);
+      } else {
+        ready_cols = n;
+      }
     }
+    if (ready_cols > from)
+      OZ_TRY(max_abs(a + from * lda, n, ready_cols - from, 1, lda, 0, 0, ws.bits + 1, st));
     return OZ_OK;
   };
+  auto wait_cols = [&]() -> int { return wait_until(n); };
+  OZ_TRY(wait_until(std::min<int64_t>(n, 2 * nb)));
 
   const int la_setting = lookahead_sms();
   SideStream* side = nullptr;
@@ -1629,14 +1640,30 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
                             side->st, la_sms));
         OZ_CHECK_CUDA(cudaEventRecord(side->done, side->st));
         tr.mark(side->st);  // 5 side stream: panel done
-        OZ_TRY(wait_cols());
-        OZ_TRY(laswp_ipiv(a, lda, 0, j, j + jb + jb2, n, j, ipiv + j, (int)jb, ws, st));
-        tr.mark_sub(st);
-        OZ_TRY(trsm_blocked(a, lda, j, jb, a12 + jb2 * lda, lda, rest - jb2, st));
-        tr.mark_sub(st);
-        OZ_TRY(schur_split_part(sc, false, jb2, rest, ws, st));
-        tr.mark_sub(st);
-        OZ_TRY(schur_cols(sc, jb2, rest, ws, st, sm_count() - la_sms));
+        if (ready_cols < n) {
+          // step 0 while the upload is still running: interchanges, trsm,
+          // split and update of each column chunk as soon as it is in place
+          for (int64_t c0 = j + jb + jb2; c0 < n;) {
+            OZ_TRY(wait_until(std::max<int64_t>(c0 + 1, ready_cols)));
+            const int64_t c1 = ready_cols;
+            OZ_TRY(laswp_ipiv(a, lda, c0, c1, 0, 0, j, ipiv + j, (int)jb, ws, st));
+            OZ_TRY(trsm_blocked(a, lda, j, jb, a + c0 * lda + j, lda, c1 - c0, st));
+            OZ_TRY(schur_split_part(sc, false, c0 - (j + jb), c1 - (j + jb), ws, st));
+            OZ_TRY(schur_cols(sc, c0 - (j + jb), c1 - (j + jb), ws, st, sm_count() - la_sms));
+            c0 = c1;
+          }
+          tr.mark_sub(st);
+          tr.mark_sub(st);
+          tr.mark_sub(st);
+        } else {
+          OZ_TRY(laswp_ipiv(a, lda, 0, j, j + jb + jb2, n, j, ipiv + j, (int)jb, ws, st));
+          tr.mark_sub(st);
+          OZ_TRY(trsm_blocked(a, lda, j, jb, a12 + jb2 * lda, lda, rest - jb2, st));
+          tr.mark_sub(st);
+          OZ_TRY(schur_split_part(sc, false, jb2, rest, ws, st));
+          tr.mark_sub(st);
+          OZ_TRY(schur_cols(sc, jb2, rest, ws, st, sm_count() - la_sms));
+        }
         tr.mark(st);  // 6 after the rest of the step
         OZ_CHECK_CUDA(cudaStreamWaitEvent(st, side->done, 0));
       } else {
@@ -1741,10 +1768,14 @@ extern "C" int oz_lu_factor_overlapped(double* a, int64_t n, int64_t lda, int64_
                                        const int32_t* pair_a, const int32_t* pair_b,
                                        const int32_t* pair_shift, int32_t* ipiv, double* stats,
                                        int32_t* info, void* workspace, size_t ws_bytes,
-                                       void* cols_ready_event, void* stream) {
-  return oz::lu_factor(a, n, lda, nb, backend, num_slices, slice_bits, npairs, pair_a, pair_b,
-                       pair_shift, ipiv, stats, info, workspace, ws_bytes, oz::as_stream(stream),
-                       reinterpret_cast<cudaEvent_t>(cols_ready_event));
+                                       void* const* chunk_events, int64_t chunk_cols,
+                                       void* stream) {
+  using namespace oz;
+  OZ_REQUIRE(chunk_events != nullptr && chunk_cols >= 1, OZ_INVALID_PARAMS,
+             "overlapped LU needs chunk events and a chunk width");
+  return lu_factor(a, n, lda, nb, backend, num_slices, slice_bits, npairs, pair_a, pair_b,
+                   pair_shift, ipiv, stats, info, workspace, ws_bytes, as_stream(stream),
+                   reinterpret_cast<const cudaEvent_t*>(chunk_events), chunk_cols);
 }
 
 extern "C" int oz_memcpy2d_h2d(void* dst, size_t dpitch, const void* src, size_t spitch,

@@ -187,11 +187,11 @@ def _backend_code(backend: GemmBackend) -> int:
     return 2 if backend.scaling is ScalingMode.GLOBAL else 1
 
 
-def factor_device(a_cm, nb: int, backend: GemmBackend, cols_ready=None):
+def factor_device(a_cm, nb: int, backend: GemmBackend, chunks=None):
     """In-place LU of a column-major CUDA matrix.  Returns (ipiv tensor,
-    stats tensor, info tensor) without synchronizing.  cols_ready: a
-    torch.cuda.Event after which columns >= 2*nb are in place (overlapped
-    upload); columns < 2*nb must be ready on the current stream."""
+    stats tensor, info tensor) without synchronizing.  chunks = (events,
+    width): the matrix is still being uploaded; events[c] (torch.cuda.Event)
+    fires once columns [c*width, (c+1)*width) are in place."""
     t = _dev.torch()
     n = int(a_cm.shape[0])
     emulated = backend.kind is BackendKind.EMULATED_INT8
@@ -208,17 +208,19 @@ def factor_device(a_cm, nb: int, backend: GemmBackend, cols_ready=None):
     ipiv = t.empty((n,), dtype=t.int32, device="cuda")
     stats = t.zeros((4,), dtype=t.float64, device="cuda")
     info = t.zeros((1,), dtype=t.int32, device="cuda")
-    if cols_ready is None:
+    if chunks is None:
         _lib.call("oz_lu_factor", a_cm.data_ptr(), n, int(a_cm.stride(1)), nb,
                   _backend_code(backend), k, backend.slice_bits, len(pa), pa.ctypes.data,
                   pb.ctypes.data, sh.ctypes.data, ipiv.data_ptr(), stats.data_ptr(),
                   info.data_ptr(), ws.data_ptr(), ws_bytes, _dev.stream())
     else:
+        import ctypes as _ct
+        events, width = chunks
+        handles = (_ct.c_void_p * len(events))(*[e.cuda_event for e in events])
         _lib.call("oz_lu_factor_overlapped", a_cm.data_ptr(), n, int(a_cm.stride(1)), nb,
                   _backend_code(backend), k, backend.slice_bits, len(pa), pa.ctypes.data,
                   pb.ctypes.data, sh.ctypes.data, ipiv.data_ptr(), stats.data_ptr(),
-                  info.data_ptr(), ws.data_ptr(), ws_bytes, cols_ready.cuda_event,
-                  _dev.stream())
+                  info.data_ptr(), ws.data_ptr(), ws_bytes, handles, width, _dev.stream())
     return ipiv, stats, info, ws
 
 
@@ -227,11 +229,10 @@ _UPLOAD_STREAMS = {}
 
 def _upload_overlapped(host, nb: int):
     """Row-major host matrix -> (row-major device copy, column-major working
-    copy, event 'all columns in place', non-finite flag) in column blocks: a
-    copy stream moves block c over PCIe (cudaMemcpy2DAsync) while a second
-    stream transposes block c-1 and checks it for NaN/inf; the current stream
-    waits only for the blocks covering the first two panels (solve_system then
-    factors with oz_lu_factor_overlapped)."""
+    copy, (per-block events, block width), non-finite flag) in column blocks:
+    a copy stream moves block c over PCIe (cudaMemcpy2DAsync) while a second
+    stream transposes block c-1 and checks it for NaN/inf; oz_lu_factor_
+    overlapped waits on each block's event just before it first touches it."""
     t = _dev.torch()
     n = int(host.shape[0])
     dev = t.cuda.current_device()
@@ -245,9 +246,8 @@ def _upload_overlapped(host, nb: int):
     cs.wait_stream(cur)
     ts.wait_stream(cur)
     w = max(1024, nb)
-    need = min(n, 2 * nb)
     hptr = host.data_ptr() if isinstance(host, t.Tensor) else host.ctypes.data
-    last = None
+    events = []
     for c0 in range(0, n, w):
         c1 = min(n, c0 + w)
         _lib.call("oz_memcpy2d_h2d", ad.data_ptr() + 8 * c0, 8 * n, hptr + 8 * c0, 8 * n,
@@ -259,11 +259,10 @@ def _upload_overlapped(host, nb: int):
                   work.data_ptr() + 8 * n * c0, 1, n, ts.cuda_stream)
         _lib.call("oz_nonfinite_flag", ad.data_ptr() + 8 * c0, n, c1 - c0, n, 1,
                   bad.data_ptr(), ts.cuda_stream)
-        last = t.cuda.Event()
-        last.record(ts)
-        if c0 < need <= c1 or (c1 <= need and c1 == n):
-            cur.wait_event(last)                # the first two panels are in place
-    return ad, work, last, bad
+        done = t.cuda.Event()
+        done.record(ts)
+        events.append(done)
+    return ad, work, (events, w), bad
 
 
 def ipiv_to_perm(ipiv_host: np.ndarray) -> np.ndarray:
@@ -399,8 +398,8 @@ def solve_system(a, b, lu_block: int = 64, backend: GemmBackend | None = None):
         if not 1 <= lu_block <= n:
             raise InvalidParamsError(f"lu_block must be in 1..{n}, got {lu_block}")
         bd = _vector_device(b, n, "rhs")
-        ad, work, ready, bad = _upload_overlapped(src, lu_block)
-        ipiv, stats, info, _ws = factor_device(work, lu_block, backend, cols_ready=ready)
+        ad, work, chunks, bad = _upload_overlapped(src, lu_block)
+        ipiv, stats, info, _ws = factor_device(work, lu_block, backend, chunks=chunks)
         if int(bad.item()):
             raise NonFiniteEntryError("matrix contains NaN or infinite entries")
     else:
