@@ -236,7 +236,7 @@ def test_panel_exchange_variants(n, nb, k, tmp_path):
                                atol=1e-9 * np.abs(grid["lu"]).max())
 
 
-@pytest.mark.parametrize("n,nb", [(1500, 256), (3000, 1024)])
+@pytest.mark.parametrize("n,nb", [(1500, 256), (3000, 1024), (2100, 64)])
 def test_solve_system_host_overlapped_upload_matches_device(n, nb):
     """Host (row-major) inputs take the overlapped upload (column blocks over
     PCIe while the first panels factor): same x bit for bit as a device input,
