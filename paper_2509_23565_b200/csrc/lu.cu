@@ -1598,7 +1598,99 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
   OZ_TRY(panel_factor(a, lda, n, nb < n ? nb : n, 0, ipiv, info, ws.bits, ws, st));
   LuTrace tr;
   tr.on = getenv("OZ_LU_TRACE") != nullptr;
-  for (int64_t j = 0; j < n; j += nb) {
+  int64_t j_start = 0;
+  // ---- upload phase (overlapped host input): the first S steps are applied
+  // chunk by chunk as the columns arrive (left-looking over the chunks, same
+  // per-column sequence of interchanges and updates as the right-looking
+  // loop), panels 1..S factored on the side stream as soon as their columns
+  // have received the earlier steps.  The loop below continues at step S.
+  const int64_t nblk = ceil_div(n, nb);
+  // measured at n = 32768, nb = 1024: S = 0/1/2/3/4/6 -> 609/615/587/570/590/622 ms e2e
+  static const int phase_env = getenv("OZ_UPLOAD_STEPS") ? atoi(getenv("OZ_UPLOAD_STEPS")) : 3;
+  const int S = (int)std::min<int64_t>(phase_env, nblk - 2);
+  if (chunk_ready && side != nullptr && backend != 2 && S >= 1 && ready_cols < n &&
+      chunk_cols % nb == 0) {
+    const size_t slab = (size_t)(backend != 0 ? (q > 7 ? 2 * k : k) : 0) * (size_t)n * ws.ldK;
+    int8_t* sl_buf = nullptr;
+    int32_t* ex_buf = nullptr;
+    if (backend != 0) {
+      keep_pool_mapped();
+      OZ_CHECK_CUDA(cudaMallocAsync(&sl_buf, slab * S, st));
+      OZ_CHECK_CUDA(cudaMallocAsync(&ex_buf, sizeof(int32_t) * n * S, st));
+    }
+    std::vector<cudaEvent_t> pdone(S + 1, nullptr);
+    for (auto& e : pdone) OZ_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    std::vector<LuWs> wss(S, ws);
+    std::vector<Schur> scs;
+    for (int s2 = 0; s2 < S; ++s2) {
+      const int64_t j0 = s2 * nb, jbs = std::min<int64_t>(nb, n - j0), r = n - j0 - jbs;
+      if (backend != 0) {
+        wss[s2].slA = sl_buf + slab * s2;
+        wss[s2].expA = ex_buf + (size_t)n * s2;
+      }
+      scs.push_back(Schur{backend, r, r, jbs, a + j0 * lda + (j0 + jbs), lda,
+                          a + (j0 + jbs) * lda + j0, lda, a + (j0 + jbs) * lda + (j0 + jbs), lda,
+                          k, q, npairs, pa, pb, ps, ws.bits});
+    }
+    std::vector<bool> have(S + 1, false);  // panel s ready on the main stream (A21 split)
+    auto ensure_panel = [&](int s2) -> int {
+      if (have[s2]) return OZ_OK;
+      if (s2 > 0) OZ_CHECK_CUDA(cudaStreamWaitEvent(st, pdone[s2], 0));
+      if (s2 < S) OZ_TRY(schur_split_part(scs[s2], true, 0, 0, wss[s2], st));
+      // this step's interchanges on the finished L columns [0, s2*nb)
+      if (s2 > 0)
+        OZ_TRY(laswp_ipiv(a, lda, 0, s2 * nb, 0, 0, s2 * nb, ipiv + s2 * nb,
+                          (int)std::min<int64_t>(nb, n - s2 * nb), ws, st));
+      have[s2] = true;
+      return OZ_OK;
+    };
+    const int la_sms = lookahead_split(la_setting, n - nb, nb, backend != 0 ? npairs : 0,
+                                       sm_count());
+    int next_panel = 1;
+    for (int64_t c0 = nb; c0 < n;) {
+      OZ_TRY(wait_until(std::max<int64_t>(c0 + 1, ready_cols)));
+      const int64_t c1 = ready_cols;  // columns [c0, c1) just arrived
+      for (int s2 = 0; s2 < S; ++s2) {
+        const int64_t j0 = s2 * nb, t0 = j0 + std::min<int64_t>(nb, n - j0);
+        const int64_t r0 = std::max(c0, t0);
+        if (r0 >= c1) break;  // this step's trailing columns start after the chunk
+        OZ_TRY(ensure_panel(s2));
+        const int jbs = (int)std::min<int64_t>(nb, n - j0);
+        OZ_TRY(laswp_ipiv(a, lda, r0, c1, 0, 0, j0, ipiv + j0, jbs, ws, st));
+        OZ_TRY(trsm_blocked(a, lda, j0, jbs, a + r0 * lda + j0, lda, c1 - r0, st));
+        OZ_TRY(schur_split_part(scs[s2], false, r0 - t0, c1 - t0, wss[s2], st));
+        OZ_TRY(schur_cols(scs[s2], r0 - t0, c1 - t0, wss[s2], st, sm_count() - la_sms));
+        // panel s2+1 has now received steps 0..s2 if its columns are in this chunk
+        const int64_t p0 = (int64_t)(s2 + 1) * nb;
+        if (next_panel == s2 + 1 && s2 + 1 <= S && p0 >= c0 &&
+            p0 + std::min<int64_t>(nb, n - p0) <= c1) {
+          OZ_CHECK_CUDA(cudaEventRecord(side->ready, st));
+          OZ_CHECK_CUDA(cudaStreamWaitEvent(side->st, side->ready, 0));
+          OZ_TRY(panel_factor(a + p0 * lda + p0, lda, n - p0, std::min<int64_t>(nb, n - p0), p0,
+                              ipiv + p0, info, ws.bits, ws, side->st, la_sms));
+          OZ_CHECK_CUDA(cudaEventRecord(pdone[s2 + 1], side->st));
+          ++next_panel;
+        }
+      }
+      c0 = c1;
+    }
+    OZ_REQUIRE(next_panel == S + 1, OZ_UNSUPPORTED, "upload phase did not reach panel %d", S);
+    OZ_CHECK_CUDA(cudaStreamWaitEvent(st, pdone[S], 0));
+    // finalized U rows of steps < S (step S's interchanges, the L columns
+    // included, are applied by the loop below as usual)
+    for (int s2 = 0; s2 < S; ++s2) {
+      const int64_t j0 = s2 * nb;
+      OZ_TRY(max_abs(a + j0 * lda + j0, std::min<int64_t>(nb, n - j0), n - j0, 1, lda, 1, 0,
+                     ws.bits, st));
+    }
+    if (backend != 0) {
+      OZ_CHECK_CUDA(cudaFreeAsync(sl_buf, st));
+      OZ_CHECK_CUDA(cudaFreeAsync(ex_buf, st));
+    }
+    for (auto e : pdone) cudaEventDestroy(e);
+    j_start = (int64_t)S * nb;
+  }
+  for (int64_t j = j_start; j < n; j += nb) {
     const int64_t jb = nb < n - j ? nb : n - j;
     const int64_t rest = n - j - jb;
     const int64_t jb2 = nb < rest ? nb : rest;  // the next panel's width

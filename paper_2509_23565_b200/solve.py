@@ -245,7 +245,9 @@ def _upload_overlapped(host, nb: int):
     bad = t.zeros((1,), dtype=t.int32, device="cuda")
     cs.wait_stream(cur)
     ts.wait_stream(cur)
-    w = max(1024, nb)
+    import os
+    w = max(int(os.environ.get("OZ_UPLOAD_BLOCK", "2048")), nb)   # measured best at n = 32768
+    w = (w // nb) * nb
     hptr = host.data_ptr() if isinstance(host, t.Tensor) else host.ctypes.data
     events = []
     for c0 in range(0, n, w):
