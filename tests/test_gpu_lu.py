@@ -262,3 +262,20 @@ def test_solve_system_host_overlapped_upload_matches_device(n, nb):
     bad[n - 3, n - 2] = np.nan                  # in the last upload block
     with pytest.raises(NonFiniteEntryError):
         oz.solve_system(bad, b_np, nb, bk)
+
+
+def test_solve_system_upload_phase_multi_block():
+    """n = 6000, nb = 512: three 2048-column upload blocks, the first three
+    steps left-looking over them; same pivots and residual verdict as the
+    device-input path, x equal to rounding (different trsm kernels)."""
+    import paper_2509_23565_b200 as oz
+    from paper_2509_23565_b200.matgen import generate_device
+    n, nb = 6000, 512
+    a = generate_device(0, n, seed=9)
+    b = a.sum(1)
+    bk = oz.GemmBackend.int8(7)
+    x_dev, rep_dev = oz.solve_system(a, b, nb, bk)
+    x_np, rep_np = oz.solve_system(a.cpu().numpy(), b.cpu().numpy(), nb, bk)
+    np.testing.assert_allclose(x_np, x_dev.cpu().numpy(), rtol=1e-9, atol=1e-9)
+    assert rep_np.passed and rep_dev.passed
+    assert rep_np.scaled_residual < 2 * rep_dev.scaled_residual + 0.1
