@@ -1644,8 +1644,12 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
       have[s2] = true;
       return OZ_OK;
     };
-    const int la_sms = lookahead_split(la_setting, n - nb, nb, backend != 0 ? npairs : 0,
-                                       sm_count());
+    // tuning: SMs of the phase's side-stream panels (default: the look-ahead
+    // model; 48 measured equal, 74 slower at n = 32768)
+    static const int phase_sms_env = getenv("OZ_UPLOAD_SMS") ? atoi(getenv("OZ_UPLOAD_SMS")) : 0;
+    const int la_sms = phase_sms_env > 0 ? (phase_sms_env & ~1)
+                                         : lookahead_split(la_setting, n - nb, nb,
+                                                           backend != 0 ? npairs : 0, sm_count());
     int next_panel = 1;
     for (int64_t c0 = nb; c0 < n;) {
       OZ_TRY(wait_until(std::max<int64_t>(c0 + 1, ready_cols)));
