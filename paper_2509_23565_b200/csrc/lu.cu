@@ -1605,7 +1605,7 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
   // loop), panels 1..S factored on the side stream as soon as their columns
   // have received the earlier steps.  The loop below continues at step S.
   const int64_t nblk = ceil_div(n, nb);
-  // measured at n = 32768, nb = 1024: S = 0/1/2/3/4/6 -> 609/615/587/570/590/622 ms e2e
+  // measured at n = 32768, nb = 1024 (wavefront): S = 0/3/4/5/6 -> 609/567/578/585/592 ms e2e
   static const int phase_env = getenv("OZ_UPLOAD_STEPS") ? atoi(getenv("OZ_UPLOAD_STEPS")) : 3;
   const int S = (int)std::min<int64_t>(phase_env, nblk - 2);
   if (chunk_ready && side != nullptr && backend != 2 && S >= 1 && ready_cols < n &&
@@ -1651,22 +1651,28 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
                                          : lookahead_split(la_setting, n - nb, nb,
                                                            backend != 0 ? npairs : 0, sm_count());
     int next_panel = 1;
-    for (int64_t c0 = nb; c0 < n;) {
-      OZ_TRY(wait_until(std::max<int64_t>(c0 + 1, ready_cols)));
-      const int64_t c1 = ready_cols;  // columns [c0, c1) just arrived
+    // wavefront over (step, block): diagonal d applies step s to block d - s,
+    // so step 0 keeps up with the upload while later steps wait for their
+    // panels (each block still receives steps 0, 1, ... in order)
+    const int64_t nch = ceil_div(n, chunk_cols);
+    for (int64_t d = 0; d < nch + S - 1; ++d) {
       for (int s2 = 0; s2 < S; ++s2) {
+        const int64_t c = d - s2;
+        if (c < 0 || c >= nch) continue;
+        const int64_t c0 = c * chunk_cols, c1 = std::min<int64_t>(n, c0 + chunk_cols);
+        OZ_TRY(wait_until(c1));
         const int64_t j0 = s2 * nb, t0 = j0 + std::min<int64_t>(nb, n - j0);
         const int64_t r0 = std::max(c0, t0);
-        if (r0 >= c1) break;  // this step's trailing columns start after the chunk
+        if (r0 >= c1) continue;  // this step's trailing columns start after the block
         OZ_TRY(ensure_panel(s2));
         const int jbs = (int)std::min<int64_t>(nb, n - j0);
         OZ_TRY(laswp_ipiv(a, lda, r0, c1, 0, 0, j0, ipiv + j0, jbs, ws, st));
         OZ_TRY(trsm_blocked(a, lda, j0, jbs, a + r0 * lda + j0, lda, c1 - r0, st));
         OZ_TRY(schur_split_part(scs[s2], false, r0 - t0, c1 - t0, wss[s2], st));
         OZ_TRY(schur_cols(scs[s2], r0 - t0, c1 - t0, wss[s2], st, sm_count() - la_sms));
-        // panel s2+1 has now received steps 0..s2 if its columns are in this chunk
+        // panel s2+1 has now received steps 0..s2 if its columns are in this block
         const int64_t p0 = (int64_t)(s2 + 1) * nb;
-        if (next_panel == s2 + 1 && s2 + 1 <= S && p0 >= c0 &&
+        if (next_panel == s2 + 1 && s2 + 1 <= S && p0 >= r0 &&
             p0 + std::min<int64_t>(nb, n - p0) <= c1) {
           OZ_CHECK_CUDA(cudaEventRecord(side->ready, st));
           OZ_CHECK_CUDA(cudaStreamWaitEvent(side->st, side->ready, 0));
@@ -1676,7 +1682,6 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
           ++next_panel;
         }
       }
-      c0 = c1;
     }
     OZ_REQUIRE(next_panel == S + 1, OZ_UNSUPPORTED, "upload phase did not reach panel %d", S);
     OZ_CHECK_CUDA(cudaStreamWaitEvent(st, pdone[S], 0));
