@@ -13,6 +13,7 @@ asynchronously on the current stream.
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -214,9 +215,8 @@ def factor_device(a_cm, nb: int, backend: GemmBackend, chunks=None):
                   pb.ctypes.data, sh.ctypes.data, ipiv.data_ptr(), stats.data_ptr(),
                   info.data_ptr(), ws.data_ptr(), ws_bytes, _dev.stream())
     else:
-        import ctypes as _ct
         events, width = chunks
-        handles = (_ct.c_void_p * len(events))(*[e.cuda_event for e in events])
+        handles = (ctypes.c_void_p * len(events))(*[e.cuda_event for e in events])
         _lib.call("oz_lu_factor_overlapped", a_cm.data_ptr(), n, int(a_cm.stride(1)), nb,
                   _backend_code(backend), k, backend.slice_bits, len(pa), pa.ctypes.data,
                   pb.ctypes.data, sh.ctypes.data, ipiv.data_ptr(), stats.data_ptr(),
@@ -245,7 +245,6 @@ def _upload_overlapped(host, nb: int):
     bad = t.zeros((1,), dtype=t.int32, device="cuda")
     cs.wait_stream(cur)
     ts.wait_stream(cur)
-    import os
     w = max(int(os.environ.get("OZ_UPLOAD_BLOCK", "2048")), nb)   # measured best at n = 32768
     w = (w // nb) * nb
     hptr = host.data_ptr() if isinstance(host, t.Tensor) else host.ctypes.data
@@ -428,4 +427,3 @@ def solve_system(a, b, lu_block: int = 64, backend: GemmBackend | None = None):
     return (x.cpu().numpy() if host else x), report
 
 
-del ctypes
