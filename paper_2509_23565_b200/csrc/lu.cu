@@ -1279,10 +1279,17 @@ int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t b
 // values) to columns [c0a,c1a) U [c0b,c1b) of a: compose once, gather once.
 int laswp_ipiv(double* a, int64_t lda, int64_t c0a, int64_t c1a, int64_t c0b, int64_t c1b,
                int64_t k1, const int32_t* ipiv, int npiv, const LuWs& ws, cudaStream_t st) {
-  OZ_REQUIRE(npiv >= 0 && npiv <= COMPOSE_MAX, OZ_UNSUPPORTED, "at most %d interchanges per call",
-             COMPOSE_MAX);
+  OZ_REQUIRE(npiv >= 0, OZ_INVALID_PARAMS, "negative interchange count");
   const int64_t ncols = (c1a - c0a) + (c1b - c0b);
   if (npiv == 0 || ncols <= 0) return OZ_OK;
+  if (npiv > COMPOSE_MAX) {
+    // lu_block > COMPOSE_MAX: the sequential interchanges compose chunk by
+    // chunk (LAPACK dlaswp order is preserved)
+    for (int off = 0; off < npiv; off += COMPOSE_MAX)
+      OZ_TRY(laswp_ipiv(a, lda, c0a, c1a, c0b, c1b, k1 + off, ipiv + off,
+                        std::min(COMPOSE_MAX, npiv - off), ws, st));
+    return OZ_OK;
+  }
   static bool attr = false;
   if (!attr) {
     OZ_CHECK_CUDA(cudaFuncSetAttribute(laswp_list_kernel,
@@ -1559,7 +1566,6 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
   OZ_REQUIRE(n >= 1, OZ_INVALID_PARAMS, "empty matrices are not supported");
   OZ_REQUIRE(nb >= 1 && nb <= n, OZ_INVALID_PARAMS, "lu_block must be in 1..%lld, got %lld",
              (long long)n, (long long)nb);
-  OZ_REQUIRE(nb <= SWAP_MAX / 2, OZ_UNSUPPORTED, "lu_block > %d not supported", SWAP_MAX / 2);
   OZ_REQUIRE(lda >= n, OZ_INVALID_PARAMS, "lda < n");
   OZ_REQUIRE(backend >= 0 && backend <= 2, OZ_INVALID_PARAMS, "bad backend %d", backend);
   LuWs ws;
@@ -1637,10 +1643,10 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
       if (have[s2]) return OZ_OK;
       if (s2 > 0) OZ_CHECK_CUDA(cudaStreamWaitEvent(st, pdone[s2], 0));
       if (s2 < S) OZ_TRY(schur_split_part(scs[s2], true, 0, 0, wss[s2], st));
-      // this step's interchanges on the finished L columns [0, s2*nb)
-      if (s2 > 0)
-        OZ_TRY(laswp_ipiv(a, lda, 0, s2 * nb, 0, 0, s2 * nb, ipiv + s2 * nb,
-                          (int)std::min<int64_t>(nb, n - s2 * nb), ws, st));
+      // The interchanges of step s2 on the finished L columns [0, s2*nb) are
+      // deferred to the end of the phase: they reorder the A21 rows of the
+      // earlier steps, whose updates of later blocks are still pending (the
+      // native backend reads A21 from the matrix itself).
       have[s2] = true;
       return OZ_OK;
     };
@@ -1685,6 +1691,12 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
     }
     OZ_REQUIRE(next_panel == S + 1, OZ_UNSUPPORTED, "upload phase did not reach panel %d", S);
     OZ_CHECK_CUDA(cudaStreamWaitEvent(st, pdone[S], 0));
+    // the deferred interchanges of steps 1..S-1 on their L columns, in step
+    // order (every A21 of those steps has been consumed by now); step S's
+    // follow in the loop below, before anything reads those columns again
+    for (int s2 = 1; s2 < S; ++s2)
+      OZ_TRY(laswp_ipiv(a, lda, 0, s2 * nb, 0, 0, s2 * nb, ipiv + s2 * nb,
+                        (int)std::min<int64_t>(nb, n - s2 * nb), ws, st));
     // finalized U rows of steps < S (step S's interchanges, the L columns
     // included, are applied by the loop below as usual)
     for (int s2 = 0; s2 < S; ++s2) {

@@ -152,6 +152,18 @@ def _sm_count() -> int:
     return int(out[0])
 
 
+def check_scaling(backend: GemmBackend, ranks: int) -> None:
+    """GLOBAL scaling takes ONE exponent over a whole operand (split.py:131-134);
+    a rank only sees its own A21 rows / U12 columns, so a distributed split
+    would pick per-rank exponents and diverge from the reference.  Refuse it
+    rather than return different factors."""
+    from .split import ScalingMode
+    if ranks > 1 and backend.kind is BackendKind.EMULATED_INT8 and \
+            backend.scaling is ScalingMode.GLOBAL:
+        raise InvalidParamsError("GLOBAL scaling is single-GPU only: the distributed drivers "
+                                 "split per rank (use PER_VECTOR or one rank)")
+
+
 # ------------------------------------------------------------ device ops
 class DeviceOps:
     """Rank-local block operations on the GPU, all through the C ABI
@@ -163,6 +175,7 @@ class DeviceOps:
         self.t = t
         self.n, self.nb, self.Q, self.q = n, nb, Q, q
         self.ncl = local_ncols(n, nb, Q, q)
+        check_scaling(backend, Q)
         self.backend = backend
         self.emulated = backend.kind is BackendKind.EMULATED_INT8
         from .solve import _backend_code
@@ -508,6 +521,7 @@ class HplProblem:
         from .matgen import GEN_PARAWILK_RANDOMIZED, GEN_UNIFORM
         self.backend = backend or GemmBackend.native()
         self.comm = comm or Comm()
+        check_scaling(self.backend, self.comm.size)
         if not 1 <= nb <= min(n, 1024):
             raise InvalidParamsError(f"nb must be in 1..{min(n, 1024)}, got {nb}")
         P, Q = grid if grid is not None else (1, self.comm.size)

@@ -39,7 +39,7 @@ import numpy as np
 from . import _dev, _lib
 from .errors import InvalidParamsError, SingularPivotError
 from .gemm import BackendKind, GemmBackend, pair_table
-from .hpl import Comm, _sm_count, local_cols_before, local_ncols
+from .hpl import Comm, _sm_count, check_scaling, local_cols_before, local_ncols
 
 __all__ = ["Grid", "DeviceOps2D", "compose_interchanges", "factor_2d", "solve_2d", "rhs_2d",
            "residual_2d", "global_rows", "REC_HDR"]
@@ -109,6 +109,7 @@ class DeviceOps2D:
         self.n, self.nb, self.P, self.Q, self.p, self.q = n, nb, P, Q, p, q
         self.mloc = local_ncols(n, nb, P, p)
         self.ncl = local_ncols(n, nb, Q, q)
+        check_scaling(backend, P * Q)
         self.backend = backend
         from .solve import _backend_code
         self.code = _backend_code(backend)

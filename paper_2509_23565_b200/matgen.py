@@ -15,10 +15,12 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _dev, _lib
-from .errors import InvalidDimError, InvalidParamsError
+from .errors import (InvalidDimError, InvalidParamsError, InvalidPermutationError,
+                     NonPowerOfTwoScaleError, ShapeMismatchError)
 
 __all__ = ["ParaWilkParams", "parawilk", "parawilk_randomized", "hpl_uniform", "wilkinson",
-           "turing", "generate_device", "pcg64_state"]
+           "turing", "turing_inverse", "generalized_fibonacci", "nnz_pattern", "DiagonalScale",
+           "Permutation", "apply_scaling", "generate_device", "pcg64_state"]
 
 GEN_UNIFORM, GEN_PARAWILK, GEN_PARAWILK_RANDOMIZED = 0, 1, 2
 
@@ -118,3 +120,115 @@ def turing(n: int, depth: int) -> np.ndarray:
     if not 1 <= depth <= n - 1:
         raise InvalidDimError(f"depth must be in 1..{n - 1}")
     return _to_host(generate_device(GEN_PARAWILK, n, None, depth, n, 1.0))
+
+
+# ---------------------------------------------------------------------------
+# Host test-matrix utilities (matgen.py:98-130, 174-251).  Tiny exact-integer
+# and exact-scaling helpers the reference exports next to its generators; no
+# configuration of the hot path uses them, so they stay host code.
+
+def generalized_fibonacci(order: int, count: int) -> list[int]:
+    """f[0] = 1, f[i] = f[i-1] + ... + f[i-order] (missing terms count as 0)
+    (matgen.py:116-130); order 2 is Fibonacci."""
+    if order < 1:
+        raise InvalidParamsError("order must be >= 1")
+    if count < 1:
+        raise InvalidParamsError("count must be >= 1")
+    f = [1]
+    window = 1                      # running sum of the last `order` terms
+    for i in range(1, count):
+        f.append(window)
+        window += f[i]
+        if i - order >= 0:
+            window -= f[i - order]
+    return f
+
+
+def turing_inverse(n: int, depth: int) -> np.ndarray:
+    """Exact inverse of turing(n, depth) as an object array of Python ints
+    (matgen.py:98-113).  turing() is unit lower triangular Toeplitz with -1 on
+    subdiagonals 1..depth, so its inverse is lower triangular Toeplitz with
+    the order-`depth` generalized Fibonacci numbers down each column."""
+    if n < 2:
+        raise InvalidDimError("n must be >= 2")
+    if not 1 <= depth <= n - 1:
+        raise InvalidDimError(f"depth must be in 1..{n - 1}")
+    f = generalized_fibonacci(depth, n)
+    inv = np.empty((n, n), dtype=object)
+    for i in range(n):
+        for j in range(n):
+            inv[i, j] = f[i - j] if i >= j else 0
+    return inv
+
+
+def nnz_pattern(a) -> np.ndarray:
+    """uint8 indicator of the nonzero entries (matgen.py:174-176)."""
+    return np.not_equal(a, 0).astype(np.uint8)
+
+
+@dataclass(frozen=True)
+class DiagonalScale:
+    """Diagonal scaling by signed powers of two, exact in FP64 (matgen.py:179-195)."""
+
+    entries: np.ndarray
+
+    def __post_init__(self):
+        e = np.atleast_1d(np.asarray(self.entries, dtype=np.float64))
+        if e.ndim != 1 or e.size == 0:
+            raise InvalidParamsError("diagonal entries must form a nonempty vector")
+        frac, _ = np.frexp(e)
+        if not np.isfinite(e).all() or not (np.abs(frac) == 0.5).all():
+            raise NonPowerOfTwoScaleError("diagonal entries must be nonzero signed powers of two")
+        e = e.copy()
+        e.setflags(write=False)
+        object.__setattr__(self, "entries", e)
+
+
+@dataclass(frozen=True)
+class Permutation:
+    """Gather permutation: output position i takes input index indices[i]
+    (matgen.py:198-216)."""
+
+    indices: np.ndarray
+
+    def __post_init__(self):
+        idx = np.atleast_1d(np.asarray(self.indices))
+        if idx.ndim != 1 or idx.size == 0 or not np.issubdtype(idx.dtype, np.integer):
+            raise InvalidPermutationError("indices must form a nonempty integer vector")
+        seen = np.zeros(idx.size, dtype=bool)
+        ok = bool(((idx >= 0) & (idx < idx.size)).all())
+        if ok:
+            seen[idx] = True
+            ok = bool(seen.all())
+        if not ok:
+            raise InvalidPermutationError("indices are not a permutation of 0..n-1")
+        idx = idx.copy()
+        idx.setflags(write=False)
+        object.__setattr__(self, "indices", idx)
+
+
+def _apply_side(out: np.ndarray, op, axis: int, side: str) -> np.ndarray:
+    size = out.shape[axis]
+    what = "row" if axis == 0 else "column"
+    if isinstance(op, DiagonalScale):
+        if op.entries.size != size:
+            raise ShapeMismatchError(f"{side} diagonal length must match {what} count")
+        return out * (op.entries[:, None] if axis == 0 else op.entries[None, :])
+    if isinstance(op, Permutation):
+        if op.indices.size != size:
+            raise ShapeMismatchError(f"{side} permutation length must match {what} count")
+        return np.take(out, op.indices, axis=axis)
+    raise InvalidParamsError(f"{side} must be DiagonalScale or Permutation")
+
+
+def apply_scaling(a, left=None, right=None) -> np.ndarray:
+    """Exact power-of-two scalings / permutations of rows (left) and columns
+    (right) (matgen.py:219-251); returns a new array."""
+    out = np.array(a, dtype=np.float64, copy=True)
+    if out.ndim != 2:
+        raise ShapeMismatchError("expected a 2-D matrix")
+    if left is not None:
+        out = _apply_side(out, left, 0, "left")
+    if right is not None:
+        out = _apply_side(out, right, 1, "right")
+    return out

@@ -383,7 +383,11 @@ def scaled_residual(a, x, b, **metadata) -> SolveReport:
 
 def solve_system(a, b, lu_block: int = 64, backend: GemmBackend | None = None):
     """Factor, solve and verify in one call; wall time covers factor + solve
-    (solve.py:217-239).  Device work is synchronized before the clock stops."""
+    (solve.py:217-239).  Device work is synchronized before the clock stops.
+
+    Errors surface in the reference's order: lu_factor's checks (square,
+    empty, non-finite, lu_block, singular pivot) before lu_solve's rhs shape
+    check (solve.py:227-228)."""
     if backend is None:
         backend = GemmBackend.native()
     t = _dev.torch()
@@ -392,21 +396,29 @@ def solve_system(a, b, lu_block: int = 64, backend: GemmBackend | None = None):
     src = _host_row_major(a)
     if src is not None:
         # host matrix: overlapped upload (column blocks over PCIe while the
-        # first panels are factored); non-finite entries are caught from the
-        # max |a| folded into the upload, before any result is returned
+        # first panels are factored); non-finite entries are caught by a flag
+        # folded into the upload, before any result is returned
         n = int(src.shape[0])
         host = True
         if not 1 <= lu_block <= n:
+            hv = src.numpy() if isinstance(src, t.Tensor) else src
+            if not np.isfinite(hv).all():
+                raise NonFiniteEntryError("matrix contains NaN or infinite entries")
             raise InvalidParamsError(f"lu_block must be in 1..{n}, got {lu_block}")
-        bd = _vector_device(b, n, "rhs")
-        ad, work, chunks, bad = _upload_overlapped(src, lu_block)
-        ipiv, stats, info, _ws = factor_device(work, lu_block, backend, chunks=chunks)
-        if int(bad.item()):
-            raise NonFiniteEntryError("matrix contains NaN or infinite entries")
+        try:
+            ad, work, chunks, bad = _upload_overlapped(src, lu_block)
+            ipiv, stats, info, _ws = factor_device(work, lu_block, backend, chunks=chunks)
+            if int(bad.item()):
+                raise NonFiniteEntryError("matrix contains NaN or infinite entries")
+        except BaseException:
+            # the copy/transpose side streams may still be writing into
+            # ad/work/bad (and reading the host matrix): drain the device
+            # before those buffers go back to the caching allocator
+            t.cuda.synchronize()
+            raise
     else:
         ad, host = _as_square_device(a)
         n = int(ad.shape[0])
-        bd = _vector_device(b, n, "rhs")
         if not bool(t.isfinite(ad).all().item()):
             raise NonFiniteEntryError("matrix contains NaN or infinite entries")
         if not 1 <= lu_block <= n:
@@ -414,6 +426,7 @@ def solve_system(a, b, lu_block: int = 64, backend: GemmBackend | None = None):
         work = _col_major_copy(ad)
         ipiv, stats, info, _ws = factor_device(work, lu_block, backend)
     perm, growth = _finish_factor(ipiv, stats, info)
+    bd = _vector_device(b, n, "rhs")                       # lu_solve's check (solve.py:147-148)
     dperm = t.from_numpy(perm).to("cuda", non_blocking=True)
     x, flag = _solve_device(work, dperm, bd)
     if int(flag[0].item()):
@@ -425,5 +438,3 @@ def solve_system(a, b, lu_block: int = 64, backend: GemmBackend | None = None):
     report = _report(raw, na, nx, nbv, n, backend=backend.describe(), lu_block=lu_block,
                      growth=growth, flops=counter, seconds=seconds)
     return (x.cpu().numpy() if host else x), report
-
-

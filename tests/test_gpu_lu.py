@@ -279,3 +279,73 @@ def test_solve_system_upload_phase_multi_block():
     np.testing.assert_allclose(x_np, x_dev.cpu().numpy(), rtol=1e-9, atol=1e-9)
     assert rep_np.passed and rep_dev.passed
     assert rep_np.scaled_residual < 2 * rep_dev.scaled_residual + 0.1
+
+
+def test_solve_system_upload_phase_native_backend():
+    """The upload phase with the native FP64 Schur update (solve_system's
+    default backend): the deferred L-column interchanges keep every step's
+    A21 rows in the order its pending block updates need.
+    n = 6000, nb = 512 -> three 2048-column upload blocks."""
+    import paper_2509_23565_b200 as oz
+    from paper_2509_23565_b200.matgen import generate_device
+    n, nb = 6000, 512
+    a = generate_device(0, n, seed=11)
+    b = a.sum(1)
+    bk = oz.GemmBackend.native()
+    x_dev, rep_dev = oz.solve_system(a, b, nb, bk)
+    x_np, rep_np = oz.solve_system(a.cpu().numpy(), b.cpu().numpy(), nb)
+    assert rep_dev.passed and rep_np.passed, (rep_dev.scaled_residual, rep_np.scaled_residual)
+    assert rep_np.scaled_residual < 2 * rep_dev.scaled_residual + 0.1
+    np.testing.assert_allclose(x_np, x_dev.cpu().numpy(), rtol=1e-9, atol=1e-9)
+    # and the factors themselves: host-input LU == device-input LU to rounding
+    f_dev = oz.lu_factor(a, nb)
+    f_np = oz.lu_factor(a.cpu().numpy(), nb)
+    assert np.array_equal(np.asarray(f_np.pivots), f_dev.pivots.cpu().numpy())
+
+
+@pytest.mark.parametrize("k", [0, 7])
+def test_lu_block_above_1024(k):
+    """lu_block may be anything in 1..n (solve.py:109-110): nb = 1100 > 1024
+    interchanges per panel compose chunk by chunk; pivots equal the oracle's."""
+    oz = _oz()
+    from oracle import ozaki_oracle as orc
+    n, nb = 1200, 1100
+    a = np.random.default_rng(5).random((n, n)) - 0.5
+    bk = oz.GemmBackend.int8(k) if k else oz.GemmBackend.native()
+    f = oz.lu_factor(a, nb, bk)
+    lu_ref, perm_ref, _ = orc.lu_factor(a, nb, k if k else None)
+    assert np.array_equal(f.pivots, perm_ref)
+    assert np.abs(f.lu - lu_ref).max() <= 2.0**-30
+    x, rep = oz.solve_system(a, a @ np.ones(n), nb, bk)
+    assert rep.passed
+    x2, rep2 = oz.solve_system(a, a @ np.ones(n), n, bk)      # lu_block = n: one panel
+    assert rep2.passed
+
+
+def test_solve_system_error_order():
+    """lu_factor's checks come before lu_solve's rhs check (solve.py:227-228):
+    NaN matrix + bad rhs -> NonFiniteEntryError, singular matrix + bad rhs ->
+    SingularPivotError, bad lu_block + NaN -> NonFiniteEntryError; host and
+    device inputs alike."""
+    import torch
+    oz = _oz()
+    n = 300
+    nan = np.random.default_rng(2).random((n, n))
+    nan[5, 7] = np.nan
+    sing = np.random.default_rng(2).random((n, n))
+    sing[:, 3] = 0.0
+    bad_rhs = np.ones(n + 1)
+    for conv in (lambda x: x, lambda x: torch.from_numpy(x).cuda()):
+        with pytest.raises(oz.NonFiniteEntryError):
+            oz.solve_system(conv(nan), bad_rhs, 64)
+        with pytest.raises(oz.SingularPivotError):
+            oz.solve_system(conv(sing), bad_rhs, 64)
+        with pytest.raises(oz.NonFiniteEntryError):
+            oz.solve_system(conv(nan), np.ones(n), 0)
+        with pytest.raises(oz.InvalidParamsError):
+            oz.solve_system(conv(sing), np.ones(n), n + 1)
+        with pytest.raises(oz.ShapeMismatchError):
+            oz.solve_system(conv(np.eye(n)), bad_rhs, 64)
+    # the device stays usable after an exception in the overlapped path
+    x, rep = oz.solve_system(np.eye(n) * 2.0, np.ones(n) * 2.0, 64)
+    assert np.array_equal(x, np.ones(n))

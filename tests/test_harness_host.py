@@ -71,7 +71,8 @@ def test_search_and_bench_rows_csv():
     ["solve", "--n", "64", "--seed", "1", "--backend", "int8", "--splits", "7",
      "--truncation", "bogus"],
     ["sweep-splits", "--n", "64", "--seed", "1", "--splits", "9:3"],
-    ["gemm", "--n", "8", "--matrix", "uniform", "--seed", "1"],       # not on the B200 path
+    ["gemm", "--n", "8", "--matrix", "uniform"],                      # seed needed for uniform
+    ["gemm", "--n", "8", "--matrix", "uniform", "--seed", "1", "--backend", "int8"],
     ["nonsense"],
 ])
 def test_cli_usage_errors_exit_2(argv):
