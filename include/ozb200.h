@@ -127,6 +127,15 @@ int oz_dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k, double alp
              const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
              double* c, int64_t ldc, void* stream);
 
+/* The reference's alpha/beta epilogue on a finished product (gemm.py:266-270),
+ * elementwise over `count` contiguous doubles, each step rounded on its own:
+ * out = ab; if alpha != 1: out = alpha*out; if use_c: out = out + beta*c.
+ * (The native path computes ab with oz_dgemm(alpha=1, beta=0) first, so the
+ * result equals numpy's `alpha*(a@b) + beta*c` bit for bit whenever the
+ * products agree.)  ab and out may alias; c may be NULL when use_c == 0. */
+int oz_axpby(int64_t count, double alpha, const double* ab, double beta, const double* c,
+             int use_c, double* out, void* stream);
+
 /*
  * Blocked right-looking LU with partial pivoting (solve.py:66-140) on a
  * column-major n x n matrix, in place.  backend 0 = native FP64 Schur update

@@ -36,6 +36,7 @@ _SIGNATURES = {
                  _vp],
     "oz_gemm_emu": [_i64, _i64, _i64, _vp, _i64, _i64, _int, _vp, _vp, _i64, _i64, _int, _vp,
                     _int, _vp, _vp, _vp, _int, _dbl, _dbl, _vp, _i64, _int, _vp, _vp],
+    "oz_axpby": [_i64, _dbl, _vp, _dbl, _vp, _int, _vp, _vp],
     "oz_plan_groups": [_int, _vp, _i64, _int, _vp, _vp],
     "oz_gemm_pair_i32": [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp],
     "oz_dgemm": [_int, _int, _i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64, _vp],

@@ -170,6 +170,33 @@ extern "C" int oz_dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k,
                    oz::as_stream(stream), 0);
 }
 
+namespace {
+__global__ void axpby_kernel(int64_t count, double alpha, const double* __restrict__ ab,
+                             double beta, const double* __restrict__ c, int use_c,
+                             double* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    double v = ab[i];
+    if (alpha != 1.0) v = __dmul_rn(alpha, v);
+    if (use_c) v = __dadd_rn(v, __dmul_rn(beta, c[i]));
+    out[i] = v;
+  }
+}
+}  // namespace
+
+extern "C" int oz_axpby(int64_t count, double alpha, const double* ab, double beta,
+                        const double* c, int use_c, double* out, void* stream) {
+  OZ_REQUIRE(count >= 0, OZ_INVALID_PARAMS, "negative count");
+  OZ_REQUIRE(!use_c || c != nullptr, OZ_INVALID_PARAMS, "use_c without c");
+  if (count == 0) return OZ_OK;
+  int64_t blocks = (count + 255) / 256;
+  if (blocks > oz::sm_count() * 8) blocks = oz::sm_count() * 8;
+  axpby_kernel<<<(unsigned)blocks, 256, 0, oz::as_stream(stream)>>>(count, alpha, ab, beta, c,
+                                                                     use_c, out);
+  OZ_CHECK_LAUNCH();
+  return OZ_OK;
+}
+
 // LAPACK-style interchanges -> permutation vector: pivots[i] is the original
 // row index that ends at position i (solve.py:80-82 perm bookkeeping).
 extern "C" int oz_ipiv_to_perm(const int32_t* ipiv, int64_t n, int64_t* perm) {

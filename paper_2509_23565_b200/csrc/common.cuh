@@ -26,6 +26,16 @@ const char* last_error();
     }                                                                             \
   } while (0)
 
+// One-time, per-process setup (kernel attributes): C++11 thread-safe static
+// initialisation, so concurrent callers (harness worker threads on their own
+// streams) never race on it; the error of the first attempt is sticky.
+#define OZ_ONCE(expr)                                          \
+  do {                                                         \
+    static const cudaError_t oz_once_err_ = [&] { return (expr); }(); \
+    OZ_CHECK_CUDA(oz_once_err_);                               \
+  } while (0)
+
+
 // Every kernel launched by this library is counted (bench.py reports it as
 // gpu_launches); cuBLAS launches are not ours and are not counted.
 void count_launch();

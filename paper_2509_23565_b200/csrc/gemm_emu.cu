@@ -555,15 +555,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
 // ------------------------------------------------------------------ host side
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* ptr = nullptr;
     cudaDriverEntryPointQueryResult qres;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qres) ==
             cudaSuccess &&
         qres == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+  }();
   return fn;
 }
 
@@ -651,19 +651,18 @@ StartLog& start_log() {
 
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStream_t st,
                 int max_ctas = 0) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    OZ_CHECK_CUDA(cudaFuncSetAttribute(emu_gemm_pair_kernel<false, false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)P_SMEM_BYTES));
-    OZ_CHECK_CUDA(cudaFuncSetAttribute(emu_gemm_pair_kernel<false, true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)P_SMEM_BYTES));
-    OZ_CHECK_CUDA(cudaFuncSetAttribute(emu_gemm_pair_kernel<true, false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)P_SMEM_BYTES));
-    attr_set = true;
-  }
+  OZ_ONCE([] {
+    cudaError_t e = cudaFuncSetAttribute(emu_gemm_pair_kernel<false, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)P_SMEM_BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(emu_gemm_pair_kernel<false, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P_SMEM_BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(emu_gemm_pair_kernel<true, false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P_SMEM_BYTES);
+    return e;
+  }());
   p.num_m_tiles = (int)ceil_div(p.m, P_BM);
   p.num_n_tiles = (int)ceil_div(p.n, P_BN);
   p.num_tiles = p.num_m_tiles * p.num_n_tiles;

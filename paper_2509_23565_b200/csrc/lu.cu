@@ -24,6 +24,7 @@
 // (native comparator) or the Ozaki-INT8 tcgen05 GEMM (gemm_emu.cu).
 #include <stdlib.h>
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -34,16 +35,18 @@ namespace oz {
 // default stream-ordered pool; keep its memory mapped between calls instead
 // of returning it to the driver at every synchronization.
 void keep_pool_mapped() {
-  static bool done = false;
-  if (done) return;
-  int dev = 0;
-  cudaMemPool_t pool;
-  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t keep = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-  }
-  cudaGetLastError();
-  done = true;
+  static const bool done = [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+    return true;
+  }();
+  (void)done;
 }
 
 }  // namespace oz
@@ -152,13 +155,15 @@ struct PanelShared {
 };
 
 unsigned long long* panel_dbg() {
-  static unsigned long long* dbg = nullptr;
-  static const bool on = getenv("OZ_PANEL_TIMING") != nullptr;
-  if (on && !dbg) {
-    cudaMalloc(&dbg, 8 * sizeof(unsigned long long));
-    cudaMemset(dbg, 0, 8 * sizeof(unsigned long long));
-  }
-  return on ? dbg : nullptr;
+  static unsigned long long* const dbg = [] {
+    unsigned long long* d = nullptr;
+    if (getenv("OZ_PANEL_TIMING") != nullptr) {  // tuning only
+      cudaMalloc(&d, 8 * sizeof(unsigned long long));
+      cudaMemset(d, 0, 8 * sizeof(unsigned long long));
+    }
+    return d;
+  }();
+  return dbg;
 }
 
 size_t panel_smem_bytes(int w, int R) {
@@ -1064,13 +1069,8 @@ int apply_list(double* a, int64_t lda, const LuWs& ws, int64_t c0a, int64_t c1a,
 template <int NC>
 int trsm_fused(const double* L, int64_t lda, int64_t jb, double* b, int64_t ldb, int64_t ncols,
                cudaStream_t st, int max_ctas) {
-  static bool attr = false;
-  if (!attr) {
-    OZ_CHECK_CUDA(cudaFuncSetAttribute(trsm_fused_kernel<NC>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)trsmf_smem<NC>(TRSMF_MAXJB)));
-    attr = true;
-  }
+  OZ_ONCE(cudaFuncSetAttribute(trsm_fused_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)trsmf_smem<NC>(TRSMF_MAXJB)));
   int64_t grid = ceil_div(ncols, NC);
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   trsm_fused_kernel<NC><<<(unsigned)grid, TRSMF_THREADS, trsmf_smem<NC>((int)jb), st>>>(
@@ -1117,13 +1117,8 @@ int trsm_blocked(double* a, int64_t lda, int64_t j, int64_t jb, double* b, int64
     prof_stop(tag, st, PROF_TRSM, (double)jb * jb * ncols);
     return s;
   }
-  static bool attr = false;
-  if (!attr) {
-    OZ_CHECK_CUDA(cudaFuncSetAttribute(trsm_unit_lower_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)TRSM_SMEM));
-    attr = true;
-  }
+  OZ_ONCE(cudaFuncSetAttribute(trsm_unit_lower_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)TRSM_SMEM));
   return trsm_rec(a, lda, j, jb, b, ldb, ncols, st, max_ctas);
 }
 
@@ -1144,17 +1139,19 @@ int64_t panel_cluster_rows() {
   return v;
 }
 int panel_smem_cap() {
-  static int max_smem = 0;
-  if (!max_smem) {
-    int dev = 0;
+  static const int max_smem = [] {
+    int dev = 0, v = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  }
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v;
+  }();
   return max_smem - (int)sizeof(PanelShared) - 1024;
 }
 // can a cluster of G panel CTAs (smem bytes each) be resident at all?
 bool cluster_fits(int G, size_t smem) {
+  static std::mutex mu;
   static std::vector<std::pair<long long, bool>> memo;
+  std::lock_guard<std::mutex> lock(mu);
   const long long key = (long long)G << 32 | (long long)smem;
   for (auto& kv : memo)
     if (kv.first == key) return kv.second;
@@ -1180,18 +1177,18 @@ bool cluster_fits(int G, size_t smem) {
 int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t base,
                  int32_t* ipiv, int32_t* info, unsigned long long* growth, const LuWs& ws,
                  cudaStream_t st, int max_ctas) {
-  static bool attr = false;
-  if (!attr) {
-    OZ_CHECK_CUDA(cudaFuncSetAttribute(panel_window_kernel<false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       panel_smem_cap()));
-    OZ_CHECK_CUDA(cudaFuncSetAttribute(panel_window_kernel<true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       panel_smem_cap()));
-    OZ_CHECK_CUDA(cudaFuncSetAttribute(panel_window_kernel<true>,
-                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr = true;
-  }
+  OZ_ONCE([] {
+    cudaError_t e = cudaFuncSetAttribute(panel_window_kernel<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         panel_smem_cap());
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(panel_window_kernel<true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem_cap());
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(panel_window_kernel<true>,
+                               cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return e;
+  }());
   const int sms = max_ctas > 0 && max_ctas < sm_count() ? max_ctas : sm_count();
   const size_t cap = (size_t)panel_smem_cap();
   // cluster variant: as few CTAs as the slab allows, at most the cluster size
@@ -1290,13 +1287,8 @@ int laswp_ipiv(double* a, int64_t lda, int64_t c0a, int64_t c1a, int64_t c0b, in
                         std::min(COMPOSE_MAX, npiv - off), ws, st));
     return OZ_OK;
   }
-  static bool attr = false;
-  if (!attr) {
-    OZ_CHECK_CUDA(cudaFuncSetAttribute(laswp_list_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)LSWP_SMEM));
-    attr = true;
-  }
+  OZ_ONCE(cudaFuncSetAttribute(laswp_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)LSWP_SMEM));
   struct Stop {
     int tag;
     cudaStream_t st;

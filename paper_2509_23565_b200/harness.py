@@ -9,12 +9,21 @@ Differences from the reference that do not change any row value:
   matgen.py:133-171) and stay there for every cell of a sweep;
 * b = A @ ones is formed on the device (harness.py:126) — the same FP64
   values up to summation order, which the residual verdicts do not see;
-* cells run one after another on the GPU; ``OZEMU_THREADS`` is accepted and
-  ignored (rows are emitted in scan order either way, harness.py:56-72).
+* with ``OZEMU_THREADS`` > 1, independent cells run concurrently, each on
+  its own CUDA stream from a worker thread (harness.py:56-72 uses a thread
+  pool the same way); the parameter search scans its cells in batches of
+  that many concurrent solves.  Rows and the first-failing cell are taken in
+  scan order, so the results do not depend on the concurrency (the solver is
+  deterministic and reentrant).  Default 1: a 256-order cell takes ~1.6 ms
+  on the B200 and concurrent Python workers measured slower
+  (profiles/r02_search_bench.log).
 """
 
 from __future__ import annotations
 
+import os
+import threading
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -122,9 +131,52 @@ def _rhs_ones(a_dev):
     return b
 
 
-def _solve_cell(a_dev, backend: GemmBackend, lu_block: int) -> SolveReport:
+def _solve_once(a_dev, backend: GemmBackend, lu_block: int) -> SolveReport:
+    """Solve A x = A @ ones and report (harness.py:124-128); the module-level
+    hook the drivers call (and the reference's tests monkeypatch)."""
     _, report = solve_system(a_dev, _rhs_ones(a_dev), lu_block=lu_block, backend=backend)
     return report
+
+
+def _worker_count(default: int = 1) -> int:
+    """OZEMU_THREADS (harness.py:56-61); unset -> default."""
+    try:
+        return max(1, int(os.environ["OZEMU_THREADS"]))
+    except (KeyError, ValueError):
+        return default
+
+
+_tls = threading.local()
+
+
+def _own_stream():
+    """This worker thread's CUDA stream (created once per thread)."""
+    s = getattr(_tls, "stream", None)
+    if s is None:
+        s = _tls.stream = _dev.torch().cuda.Stream()
+    return s
+
+
+def _map_in_order(fn, items, workers: int):
+    """fn over items, results in item order; with workers > 1 each call runs
+    on its worker thread's own stream, after the caller's stream (which
+    produced the inputs), so independent solves overlap on the GPU."""
+    items = list(items)
+    if workers <= 1 or len(items) <= 1:
+        return [fn(x) for x in items]
+    t = _dev.torch()
+    origin = t.cuda.current_stream()
+    dev = t.cuda.current_device()
+
+    def run(x):
+        t.cuda.set_device(dev)
+        s = _own_stream()
+        s.wait_stream(origin)
+        with t.cuda.stream(s):
+            return fn(x)
+
+    with ThreadPoolExecutor(max_workers=min(workers, len(items))) as pool:
+        return list(pool.map(run, items))
 
 
 # ------------------------------------------------------------------ rows
@@ -241,17 +293,18 @@ def sweep_splits(spec: MatrixSpec, splits_list, *, lu_block: int | None = None,
         raise InvalidParamsError("splits range is empty")
     a = spec.build_device()
     nb = _clamp_block(lu_block, spec.n)
-    rows = []
-    for k in ks + ([None] if include_baseline else []):
+
+    def run(k):
         bk = GemmBackend.native() if k is None else GemmBackend.int8(k, slice_bits,
                                                                      scaling=scaling)
         try:
-            rows.append(SolveRow.from_report(k, _solve_cell(a, bk, nb)))
+            return SolveRow.from_report(k, _solve_once(a, bk, nb))
         except OzemuError as exc:
-            rows.append(SolveRow(splits=k, scaled_residual=float("nan"), passed=False,
-                                 int_macs=0, f64_macs=0, slice_pairs=0, seconds=0.0,
-                                 backend=bk.describe(), error=f"{type(exc).__name__}: {exc}"))
-    return rows
+            return SolveRow(splits=k, scaled_residual=float("nan"), passed=False,
+                            int_macs=0, f64_macs=0, slice_pairs=0, seconds=0.0,
+                            backend=bk.describe(), error=f"{type(exc).__name__}: {exc}")
+
+    return _map_in_order(run, ks + ([None] if include_baseline else []), _worker_count())
 
 
 def search_params(n: int, splits: int, alpha: float, seed: int, *,
@@ -268,16 +321,24 @@ def search_params(n: int, splits: int, alpha: float, seed: int, *,
         raise InvalidParamsError("search bounds too small")
     bk = GemmBackend.int8(splits, slice_bits, scaling=scaling)
     nb = _clamp_block(lu_block, n)
+    cells = [(d, b) for d in range(1, depth_max + 1) for b in range(2, block_max + 1)]
+
+    def run(cell):
+        d, b = cell
+        spec = MatrixSpec("parawilk", n, d, b, alpha, randomize=True, seed=seed)
+        try:
+            rep = _solve_once(spec.build_device(), bk, nb)
+        except OzemuError:
+            return True, float("inf")
+        return not rep.passed, rep.scaled_residual
+
+    # batches of concurrent solves, consumed in scan order
+    batch = _worker_count()
     scanned = 0
-    for d in range(1, depth_max + 1):
-        for b in range(2, block_max + 1):
+    for start in range(0, len(cells), batch):
+        chunk = cells[start:start + batch]
+        for (d, b), (failed, resid) in zip(chunk, _map_in_order(run, chunk, batch)):
             scanned += 1
-            spec = MatrixSpec("parawilk", n, d, b, alpha, randomize=True, seed=seed)
-            try:
-                rep = _solve_cell(spec.build_device(), bk, nb)
-                failed, resid = not rep.passed, rep.scaled_residual
-            except OzemuError:
-                failed, resid = True, float("inf")
             if failed:
                 return SearchResult(n=n, splits=splits, depth=d, block=b,
                                     scaled_residual=resid, cells_scanned=scanned,
@@ -299,7 +360,7 @@ def bench(n_values, lu_blocks, backend: GemmBackend, seed: int) -> list[BenchRow
                                      model_gops=0.0, scaled_residual=float("nan"),
                                      skipped=f"lu_block {nb} does not divide n {n}"))
                 continue
-            rep = _solve_cell(a, backend, nb)
+            rep = _solve_once(a, backend, nb)
             if backend.kind is BackendKind.EMULATED_INT8:
                 model = len(retained_pairs(backend.splits, backend.truncation)) * n ** 3
             else:

@@ -431,7 +431,7 @@ def solve_system(a, b, lu_block: int = 64, backend: GemmBackend | None = None):
     x, flag = _solve_device(work, dperm, bd)
     if int(flag[0].item()):
         raise SingularPivotError("zero diagonal entry in U")
-    t.cuda.synchronize()
+    t.cuda.current_stream().synchronize()   # this call's stream only (concurrent callers)
     seconds = time.perf_counter() - t0
     _count_flops(counter, n, lu_block, backend)
     raw, na, nx, nbv = _norms(ad, x, bd)

@@ -124,8 +124,10 @@ def main():
     res["int8_tops_sustained"] = best
     res["int8_tops_burst"] = best_b
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    with open(os.path.join(ROOT, "profiles", f"{tag}_int8_peak.json"), "w") as f:
-        json.dump(res, f, indent=1)
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    for d in ("profiles", "gpurun_out"):
+        with open(os.path.join(ROOT, d, f"{tag}_int8_peak.json"), "w") as f:
+            json.dump(res, f, indent=1)
     print(json.dumps({"int8_tops_sustained": best, "int8_tops_burst": best_b}))
 
 

@@ -1,14 +1,7 @@
-import os
-import sys
-
 import numpy as np
 import pytest
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-if ROOT not in sys.path:
-    sys.path.insert(0, ROOT)
-
-GOLDEN = os.path.join(ROOT, "tests", "golden")
+from testutil import GOLDEN, ROOT, load_golden  # noqa: F401  (re-exported for old imports)
 
 
 def pytest_configure(config):
@@ -35,7 +28,3 @@ def pytest_collection_modifyitems(config, items):
 @pytest.fixture
 def rng():
     return np.random.default_rng(20240901)
-
-
-def load_golden(name):
-    return np.load(os.path.join(GOLDEN, name + ".npz"))

@@ -11,7 +11,7 @@ Bars:
 import numpy as np
 import pytest
 
-from conftest import load_golden
+from testutil import load_golden
 
 pytestmark = pytest.mark.gpu
 

@@ -9,7 +9,7 @@ per-pair INT32 products and the emulated GEMM output.
 import numpy as np
 import pytest
 
-from conftest import load_golden
+from testutil import load_golden
 from oracle import ozaki_oracle as orc
 
 pytestmark = pytest.mark.gpu
