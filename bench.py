@@ -18,21 +18,25 @@ Workload (BASELINE.json configs[1], largest size that fits one GPU):
 
   roofline: the dominant kernel is the fused tcgen05 INT8 emulated GEMM; its
   algorithmic INT8 ops (2 * pairs * m * n * nb per launch) divided by its
-  CUDA-event time inside the timed steps, against 2x the measured dense bf16
-  rate (INT8 dense throughput = 2x bf16 on sm_100) from MEASURED_PEAKS.json.
+  CUDA-event time inside the timed steps, against the INT8 peak MEASURED on
+  this box (profiles/r02_int8_peak.json: cuBLASLt s8 GEMM back to back for
+  4 s = the sustained, power-capped rate; the single-launch burst rate is
+  reported beside it).  traffic = ncu dram bytes of one LU-shaped launch of
+  the same kernel (profiles/r02_roofline_traffic.json), per launch.
 
   cpu_baseline / --impl reference: the CPU oracle restatement of the reference
-  (oracle/ozaki_oracle.py, numpy + OpenBLAS on the host cores) on a bounded
-  sample of the same workload (n=1024, same nb, same k).
+  (oracle/ozaki_oracle.py, numpy + OpenBLAS on the host cores) at the
+  same-config row n=2048, nb=256, k=7 (emulated Schur updates included: 7
+  panel steps); the GPU line reports that exact config in `same_config`.
 
-N > 1: one process per GPU solving ONE distributed system (hpl.py): the
-matrix is dealt to the N ranks in 1 x N block-cyclic column blocks, the panel
-owner factors and NCCL-broadcasts each panel and its pivots, every rank
-applies the interchanges and updates its own trailing columns.  Weak scaling
-in memory: n = 32768 * sqrt(N) (rounded to nb) keeps the per-GPU slab fixed;
-value = (2/3) n^3 / max-over-ranks step time for the whole job.  The N > 1
-line also carries the D3 GEMM k-sweep row-sharded over the ranks and a
-distributed HPL k-sweep (k = 3..9 + native, with residuals).
+N > 1: one process per GPU solving ONE distributed system (hpl.py / hpl2d.py)
+at the BASELINE multi-GPU configs: N = 2, 4 -> configs[3] (randomized
+ParaWilk(131072, d=4, b=15, alpha=1/2), seed 42, k=7); N = 8 -> configs[4]
+(hpl_uniform(262144, 99), k=7 vs native FP64); default grid 1 x N (panel
+local to its owner, NCCL panel/pivot broadcasts), --grid PxQ for 2-D grids.
+value = (2/3) n^3 / max-over-ranks step time for the whole job (strong
+scaling: the config fixes n).  The line carries the k = 3..9 + native
+residual table of the same config.
 (BENCH_DIST_BACKEND=gloo runs the same path with several ranks on one GPU,
 for testing only.)
 """
@@ -62,7 +66,8 @@ def parse():
     p.add_argument("--n", type=int, default=32768)
     p.add_argument("--nb", type=int, default=1024)
     p.add_argument("--k", type=int, default=7)
-    p.add_argument("--cpu-n", type=int, default=1024)
+    p.add_argument("--cpu-n", type=int, default=2048)
+    p.add_argument("--cpu-nb", type=int, default=256)
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--skip-native", action="store_true")
     p.add_argument("--sweep-k", default="3,4,5,6,7,8,9",
@@ -70,7 +75,14 @@ def parse():
     p.add_argument("--gemm-n", type=int, default=16384, help="D3 standalone DGEMM size")
     p.add_argument("--sweep-lu-n", type=int, default=16384, help="LU k-sweep size")
     p.add_argument("--dist-n", type=int, default=0,
-                   help="N>1: global order (default n*sqrt(N) rounded to nb: fixed HBM per GPU)")
+                   help="N>1: global order (default: the BASELINE config for N, "
+                        "131072 for 2/4 GPUs, 262144 for 8)")
+    p.add_argument("--dist-matrix", default="", choices=["", "uniform", "parawilk"],
+                   help="N>1: matrix family (default: the BASELINE config for N)")
+    p.add_argument("--table-n", type=int, default=0,
+                   help="N>1: order of the k = 3..9 residual table (default: the config's n)")
+    p.add_argument("--size-sweep", default="1024,2048,4096,8192,16384,32768",
+                   help="configs[1] size sweep (k=6, k=7, native); empty string skips it")
     p.add_argument("--grid", default="",
                    help="N>1: process grid PxQ (default 1xN: panel local to one GPU; P>1 runs "
                         "hpl2d.py with a distributed panel and cross-rank row swaps)")
@@ -98,6 +110,34 @@ def load_peaks():
     except OSError:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
             "fallback"
+
+
+def int8_peak():
+    """(sustained, burst, source) dense INT8 TOPS: measured on a B200 of this
+    pool by scripts/int8_peak.py (cuBLASLt s8 x s8 -> s32), else 2x the bf16
+    figures of MEASURED_PEAKS.json (dense int8 = 2x bf16 on sm_100)."""
+    path = os.path.join(ROOT, "profiles", "r02_int8_peak.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return (float(d["int8_tops_sustained"]), float(d["int8_tops_burst"]),
+                "measured INT8 (profiles/r02_int8_peak.json: cuBLASLt s8 GEMM 8192^3, "
+                "sustained = back to back 4 s, burst = best single launch)")
+    except (OSError, KeyError, ValueError):
+        peaks, kind = load_peaks()
+        sus = 2.0 * float(peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"])
+        return sus, 2.0 * float(peaks["bf16_tflops"]), f"2 x bf16 of {kind} MEASURED_PEAKS.json"
+
+
+def roofline_traffic():
+    """ncu dram bytes (read + write) of one LU-shaped emulated-GEMM launch and
+    that launch's shape / algorithmic bytes (profiles/r02_roofline_traffic.json)."""
+    for name in ("r02_roofline_traffic.json", "roofline_traffic.json"):
+        path = os.path.join(ROOT, "profiles", name)
+        if os.path.exists(path):
+            with open(path) as f:
+                return json.load(f)
+    return None
 
 
 # ---------------------------------------------------------------- clocks
@@ -185,27 +225,93 @@ def cpu_oracle_lu(n, nb, k, reps=1):
     return times, cores, resid
 
 
+def same_config(args):
+    """The config both arms run: configs[1] at n=2048, nb=256 (BASELINE.md §2
+    row), k=7 -- 7 panel steps with 6 emulated Schur updates."""
+    n, nb, k = args.cpu_n, min(args.cpu_nb, args.cpu_n), args.k
+    return {"workload": f"configs[1] same-config row: U(-1/2,1/2) hpl_uniform({n}, 99) LU "
+                        f"factor+solve, b = A @ 1, lu_block {nb}, k={k} Band(k+1) q=7",
+            "n": n, "nb": nb, "k": k}
+
+
 def run_reference(args, rank):
+    """--impl reference: the oracle port of the reference LU (solve.py:94-156
+    with the emulated Schur update of gemm.py:190-229) on the host cores, at
+    the same-config row; every step is one full factor + solve."""
     if rank != 0:
         return
-    n, nb = args.cpu_n, min(args.nb, args.cpu_n)
+    cfg = same_config(args)
+    n, nb = cfg["n"], cfg["nb"]
     times, cores, resid = cpu_oracle_lu(n, nb, args.k, reps=args.warmup + args.steps)
     timed = times[args.warmup:] or times
     t = sum(timed) / len(timed)
     v = flops(n) / t / 1e12
-    sample = (f"U(-1/2,1/2) n={n} nb={nb} k={args.k} LU factor+solve (oracle port of the "
-              f"reference, numpy/OpenBLAS), scaled residual {resid:.4g}")
+    sample = (f"U(-1/2,1/2) n={n} nb={nb} k={args.k} LU factor+solve, {-(-n // nb)} panel steps "
+              f"(oracle port of the reference, numpy/OpenBLAS, {cores} threads), scaled "
+              f"residual {resid:.4g} (reference 0.5967, BASELINE.md §2)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64 (int8-sliced, emulated on CPU)", "data": "synthetic",
-        "config": {"workload": f"configs[1] bounded CPU sample: {sample}", "n": n, "nb": nb,
-                   "k": args.k},
+        "config": cfg,
         "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "os_cpu_count": os.cpu_count()},
         "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def same_config_row(args, cpu_times, cores, cpu_resid):
+    """The GPU at the reference arm's exact config: device-timed factor+solve
+    (inputs resident) and e2e through solve_system on host numpy input, next
+    to the CPU oracle timed on this box (like-for-like ratio)."""
+    import numpy as np
+    import torch
+
+    import paper_2509_23565_b200 as oz
+    from paper_2509_23565_b200.matgen import generate_device
+    cfg = same_config(args)
+    n, nb, k = cfg["n"], cfg["nb"], cfg["k"]
+    a = generate_device(0, n, seed=99)
+    a_np = a.cpu().numpy()
+    b_np = a_np @ np.ones(n)
+    b = torch.from_numpy(b_np).cuda()
+    bk = oz.GemmBackend.int8(k)
+    oz.solve_system(a, b, nb, bk)
+    torch.cuda.synchronize()
+    reps = 20
+    t = _time_device(lambda: oz.solve_system(a, b, nb, bk), reps)
+    x, rep = oz.solve_system(a_np, b_np, nb, bk)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        x, rep = oz.solve_system(a_np, b_np, nb, bk)
+    te = (time.perf_counter() - t0) / reps
+    cpu_t = sum(cpu_times) / len(cpu_times)
+    return {"config": cfg,
+            "gpu": {"value": flops(n) / t / 1e12, "ms_per_step": t * 1e3,
+                    "api": "solve_system(device A, b)"},
+            "e2e": {"value": flops(n) / te / 1e12, "ms_per_step": te * 1e3,
+                    "h2d_bytes_per_step": 8 * n * n + 8 * n, "d2h_bytes_per_step": 8 * n,
+                    "api": "solve_system(numpy A, b)", "scaled_residual": rep.scaled_residual},
+            "cpu": {"value": flops(n) / cpu_t / 1e12, "ms_per_step": cpu_t * 1e3,
+                    "cores": cores, "kind": "port", "scaled_residual": cpu_resid},
+            "ratio_gpu_over_cpu": cpu_t / t, "ratio_e2e_over_cpu": cpu_t / te}
+
+
+def size_sweep(sizes, ks=(6, 7)):
+    """configs[1] size sweep (BASELINE.json configs[1]; reference counterpart
+    bench(), harness.py:355-395): U(-1/2,1/2) n = 1024..32768, k = 6, 7 and
+    native FP64; factor + solve device-timed, with the HPL scaled residual and
+    verdict of each run (k = 6 fails, k = 7 passes)."""
+    rows = []
+    for n in sizes:
+        nb = 256 if n <= 4096 else (512 if n <= 8192 else 1024)
+        r = lu_sweep(n, nb, ks, reps=1)
+        for row in r["runs"]:
+            row.update({"n": n, "nb": nb})
+            rows.append(row)
+    return {"workload": "configs[1]: hpl_uniform(n, 99) factor+solve, b = A @ 1, "
+                        "nb = 256 (n<=4096) / 512 (8192) / 1024", "runs": rows}
 
 
 # ---------------------------------------------------------------- k sweeps
@@ -231,7 +337,7 @@ def _time_device(fn, reps):
     return e0.elapsed_time(e1) / 1e3 / reps
 
 
-def gemm_sweep(n, ks, int8_peak, reps=2, comm=None):
+def gemm_sweep(n, ks, int8_peak, int8_burst=None, reps=2, comm=None):
     """configs[2] (D3): standalone emulated DGEMM n^3, A = hpl_uniform(n,2),
     B = hpl_uniform(n,3) generated in HBM, C = A @ B (alpha=1, beta=0), for each
     k; the timed call is the full gemm() device path (split A, split B, fused
@@ -271,13 +377,14 @@ def gemm_sweep(n, ks, int8_peak, reps=2, comm=None):
         res["emulated"].append({"k": k, "pairs": npairs, "ms": t * 1e3,
                                 "tflops_fp64_equiv": fl / t / 1e12,
                                 "int8_tops_per_gpu": int8, "frac_of_int8_peak": int8 / int8_peak,
+                                "frac_of_int8_burst": int8 / int8_burst if int8_burst else None,
                                 "fp64_equiv_roofline_tflops": world * int8_peak / npairs})
     del a, b, out
     torch.cuda.empty_cache()
     return res
 
 
-def lu_sweep(n, nb, ks):
+def lu_sweep(n, nb, ks, reps=1):
     """configs[1] at one size, k = 3..9 plus native FP64: factor + solve of
     hpl_uniform(n, 99), b = A @ 1, with the HPL scaled residual of each run."""
     import torch
@@ -303,7 +410,7 @@ def lu_sweep(n, nb, ks):
             dperm = torch.from_numpy(perm).to("cuda", non_blocking=True)
             box["x"], _ = _solve_device(work, dperm, b0)
 
-        t = _time_device(step, 1)
+        t = _time_device(step, reps)
         _lib.call("oz_residual_norms", a0.data_ptr(), n, 1, n, box["x"].data_ptr(),
                   b0.data_ptr(), norms.data_ptr(), _dev.stream())
         raw, na, nx, nbv = (float(v) for v in norms.cpu().numpy())
@@ -344,12 +451,40 @@ def parawilk_table():
 
 
 # ---------------------------------------------------------------- N > 1
-def run_distributed(args, rank, world):
-    """configs[3]/[4] shape on N GPUs: distributed HPL LU + solve, 1 x N
-    block-cyclic columns (hpl.py), NCCL panel/pivot broadcasts.  Weak scaling
-    in memory: n = n1 * sqrt(N) keeps the per-GPU slab at n1^2 * 8 bytes."""
+def dist_config(args, world):
+    """The BASELINE.json multi-GPU config for this world size:
+    configs[3] for 2 and 4 GPUs, configs[4] for 8 (other sizes: configs[4]'s
+    matrix family at n = 32768 * sqrt(N))."""
     import math
+    if world in (2, 4):
+        n, matrix, tag = 131072, "parawilk", "configs[3]"
+        desc = ("HPL LU N=131072 ParaWilk(d=4,b=15,alpha=1/2) randomized seed 42, k=7, "
+                f"block-cyclic on {world} B200")
+    elif world == 8:
+        n, matrix, tag = 262144, "uniform", "configs[4]"
+        desc = "HPL LU N=262144 U(-1/2,1/2) seed 99, k=7 vs native FP64, block-cyclic on 8xB200"
+    else:
+        n = int(round(32768 * math.sqrt(world) / args.nb)) * args.nb
+        matrix, tag = "uniform", "configs[4] family"
+        desc = f"HPL LU N={n} U(-1/2,1/2) seed 99, k=7, block-cyclic on {world} B200"
+    if args.dist_n:
+        n = args.dist_n
+        desc += f" (order overridden: n={n})"
+    if args.dist_matrix:
+        matrix = args.dist_matrix
+    return n, matrix, tag, desc
 
+
+def _problem_kw(matrix):
+    if matrix == "parawilk":
+        return {"matrix": "parawilk", "seed": 42, "depth": 4, "block": 15, "alpha": 0.5}
+    return {"matrix": "uniform", "seed": 99}
+
+
+def run_distributed(args, rank, world):
+    """configs[3] / configs[4] on N GPUs: ONE distributed HPL LU + solve
+    (hpl.py 1 x Q, or hpl2d.py P x Q with --grid), NCCL panel/pivot
+    broadcasts.  value = (2/3) n^3 / max-over-ranks step time."""
     import numpy as np
     import torch
 
@@ -357,12 +492,13 @@ def run_distributed(args, rank, world):
     from paper_2509_23565_b200 import _lib, hpl
 
     nb, k = args.nb, args.k
-    n = args.dist_n or int(round(args.n * math.sqrt(world) / nb)) * nb
+    n, matrix, tag, desc = dist_config(args, world)
+    kw = _problem_kw(matrix)
     dev = torch.cuda.current_device()
     comm = hpl.Comm()
     P, Q = parse_grid(args.grid, world)
     gname = f"{P}x{Q}"
-    prob = hpl.HplProblem(n, nb, oz.GemmBackend.int8(k), comm=comm, grid=(P, Q))
+    prob = hpl.HplProblem(n, nb, oz.GemmBackend.int8(k), comm=comm, grid=(P, Q), **kw)
     for _ in range(args.warmup):
         prob.step()
     torch.cuda.synchronize()
@@ -385,54 +521,46 @@ def run_distributed(args, rank, world):
     ms = comm.allreduce_values([e0.elapsed_time(e1) / args.steps], "max")[0]
     value = flops(n) / (ms / 1e3) / 1e12
     rep = prob.verify(x)
+    growth = prob.growth
 
-    # e2e through the public driver: every rank uploads its column slab from
-    # pinned host memory, factors, solves, and reads x back, inside the clock
-    host_slab = torch.empty(prob.a0.shape, dtype=torch.float64, pin_memory=True)
-    host_slab.copy_(prob.a0)
-    torch.cuda.synchronize()
+    # e2e through the public driver: every rank uploads its slab from pinned
+    # host memory, factors, solves and reads x back, inside the clock
     e2e = None
     if args.e2e_steps > 0:
+        prob.restore()
+        host_slab = torch.empty(tuple(prob.ops.slab.shape), dtype=torch.float64,
+                                pin_memory=True)
+        host_slab.copy_(prob.ops.slab)
+        torch.cuda.synchronize()
+        steps = 1 if n >= 65536 else args.e2e_steps
         comm.barrier()
         t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
+        for _ in range(steps):
             prob.ops.slab.copy_(host_slab, non_blocking=True)
             xh = prob.factor_solve().cpu()
         torch.cuda.synchronize()
-        te = comm.allreduce_values([(time.perf_counter() - t0) / args.e2e_steps], "max")[0]
+        te = comm.allreduce_values([(time.perf_counter() - t0) / steps], "max")[0]
         e2e = {"value": flops(n) / te / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": int(host_slab.numel() * 8) * world,
                "d2h_bytes_per_step": int(xh.numel() * 8) * world, "ms_per_step": te * 1e3,
                "api": "paper_2509_23565_b200.hpl.HplProblem (slab H2D from pinned host, "
                       "factor, solve, x D2H)"}
-    del host_slab
-
-    native = None
-    if not args.skip_native:
-        nprob = hpl.HplProblem(n, nb, oz.GemmBackend.native(), comm=comm, grid=(P, Q))
-        nprob.step()
-        torch.cuda.synchronize()
-        comm.barrier()
-        f0, f1 = _events()
-        f0.record()
-        xn = nprob.step()
-        f1.record()
-        torch.cuda.synchronize()
-        tn = comm.allreduce_values([f0.elapsed_time(f1) / 1e3], "max")[0]
-        native = {"value": flops(n) / tn / 1e12, "ms_per_step": tn * 1e3,
-                  "scaled_residual": nprob.verify(xn).scaled_residual}
-        del nprob
-    peaks, peak_kind = load_peaks()
-    peak = 2.0 * float(peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"])
-    growth = prob.growth
+        del host_slab
     del prob
     torch.cuda.empty_cache()
+
+    # k = 3..9 + native residual table of the same config (one run each)
     ks = [int(v) for v in args.sweep_k.split(",") if v.strip()]
-    gsweep = gemm_sweep(args.gemm_n, ks, peak, comm=comm) if ks else None
-    lsweep = dist_lu_sweep(args, comm, ks, (P, Q)) if ks else None
-    d1 = parawilk_table() if rank == 0 else None
+    table = dist_lu_sweep(args, comm, ks, (P, Q), args.table_n or n, matrix) if ks else None
+    native = None
+    if table is not None:
+        native = next((r for r in table["runs"] if r["k"] == "fp64"), None)
+    elif not args.skip_native:
+        table = dist_lu_sweep(args, comm, [], (P, Q), n, matrix)
+        native = table["runs"][-1]
     if rank != 0:
         return
+    peak, peak_burst, peak_src = int8_peak()
     gemm_ms, gemm_ops = prof[0], prof[2]
     achieved = gemm_ops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     kinds = ["emu_gemm", "panel", "schur_dgemm", "split", "laswp", "trsm", "solve", "other",
@@ -440,61 +568,54 @@ def run_distributed(args, rank, world):
     breakdown = {kinds[i]: {"ms_per_step": prof[3 * i] / args.steps,
                             "launches_per_step": prof[3 * i + 1] / args.steps}
                  for i in range(12) if prof[3 * i + 1] > 0}
-    cpu_times, cores, cpu_resid = cpu_oracle_lu(args.cpu_n, min(nb, args.cpu_n), k, reps=1)
-    cpu_v = flops(args.cpu_n) / cpu_times[0] / 1e12
+    cfg_same = same_config(args)
+    cpu_times, cores, cpu_resid = cpu_oracle_lu(cfg_same["n"], cfg_same["nb"], k, reps=1)
+    cpu_v = flops(cfg_same["n"]) / cpu_times[0] / 1e12
     print(json.dumps({
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": f"f64 emulated via int8 slices (k={k}) -> int32 tensor cores -> f64 recombine",
-        "data": "synthetic (hpl_uniform(n, 99) generated on device per rank, bit-identical "
-                "to numpy)",
-        "config": {"workload": f"configs[3]/[4] shape: distributed HPL LU+solve U(-1/2,1/2) "
-                               f"n={n}, k={k}, {gname} block-cyclic, NCCL panel broadcast",
-                   "n": n, "nb": nb, "k": k, "grid": gname,
-                   "parallelism": f"block-cyclic {gname}",
+        "data": f"synthetic ({'randomized ParaWilk' if matrix == 'parawilk' else 'hpl_uniform'} "
+                f"generated on device per rank, bit-identical to numpy)",
+        "config": {"workload": f"{tag}: {desc}", "n": n, "nb": nb, "k": k, "grid": gname,
+                   "matrix": matrix, "parallelism": f"block-cyclic {gname}",
                    "l2": "inputs >> 126 MB L2; no flush needed",
-                   "flop_convention": "2/3 n^3 (harness.py:383)",
-                   "weak_scaling": "n = n1*sqrt(N): per-GPU slab fixed"},
+                   "flop_convention": "2/3 n^3 (harness.py:383)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": None,
-                     "kernel": "oz::emu::emu_gemm_pair_kernel<false> on rank 0",
-                     "peak_source": f"2 x bf16_tflops_sustained of {peak_kind} "
-                                    f"MEASURED_PEAKS.json"},
+                     "kernel": "oz::emu::emu_gemm_pair_kernel<false,false> on rank 0",
+                     "peak_source": peak_src, "peak_burst": peak_burst},
         "cpu_baseline": {"value": cpu_v, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                         "sample": f"oracle LU factor+solve U(-1/2,1/2) n={args.cpu_n} on host "
-                                   f"cores (residual {cpu_resid:.4g})"},
+                         "sample": f"oracle LU factor+solve U(-1/2,1/2) n={cfg_same['n']} "
+                                   f"nb={cfg_same['nb']} k={k} on host cores (residual "
+                                   f"{cpu_resid:.4g}); configs[3]/[4] are infeasible on a CPU"},
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
         "scaled_residual": rep.scaled_residual, "passed": rep.passed, "growth": growth,
         "native_fp64": native, "breakdown_rank0": breakdown,
-        "gemm_k_sweep": gsweep,
-        "lu_k_sweep": lsweep,
-        "parawilk256_table": d1,
+        "residual_table": table,
     }), flush=True)
 
 
-def dist_lu_sweep(args, comm, ks, grid):
-    """The distributed HPL at a moderate order (args.sweep_lu_n * sqrt(N),
-    rounded to nb) for k = 3..9 plus native FP64, one timed run each with its
-    scaled residual (configs[3]/[4] verdicts vs k across the N GPUs)."""
-    import math
-
+def dist_lu_sweep(args, comm, ks, grid, n, matrix):
+    """The distributed HPL of the same config for k = 3..9 plus native FP64,
+    one timed run each with its scaled residual (configs[3]/[4] verdicts vs k
+    across the N GPUs)."""
     import torch
 
     import paper_2509_23565_b200 as oz
     from paper_2509_23565_b200 import hpl
     nb = args.nb
-    n = int(round(args.sweep_lu_n * math.sqrt(comm.size) / nb)) * nb
     rows = []
-    for k in list(ks) + [0]:
+    for k in list(ks) + ([0] if not args.skip_native else []):
         bk = oz.GemmBackend.int8(k) if k else oz.GemmBackend.native()
-        prob = hpl.HplProblem(n, nb, bk, comm=comm, grid=grid)
-        prob.step()                                   # warm
+        prob = hpl.HplProblem(n, nb, bk, comm=comm, grid=grid, **_problem_kw(matrix))
+        prob.restore()
         torch.cuda.synchronize()
         comm.barrier()
         e0, e1 = _events()
         e0.record()
-        x = prob.step()
+        x = prob.factor_solve()
         e1.record()
         torch.cuda.synchronize()
         t = comm.allreduce_values([e0.elapsed_time(e1) / 1e3], "max")[0]
@@ -503,8 +624,8 @@ def dist_lu_sweep(args, comm, ks, grid):
                      flops(n) / t / 1e12, "scaled_residual": r, "passed": r < 16.0})
         del prob
         torch.cuda.empty_cache()
-    return {"workload": f"distributed HPL U(-1/2,1/2) n={n} nb={nb}, {grid[0]}x{grid[1]} "
-                        f"block-cyclic, factor+solve", "runs": rows}
+    return {"workload": f"distributed HPL {matrix} n={n} nb={nb}, {grid[0]}x{grid[1]} "
+                        f"block-cyclic, factor+solve (one run per k)", "runs": rows}
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -618,7 +739,6 @@ def run_ours(args, rank, world):
 
     if rank != 0:
         return
-    peaks, peak_kind = load_peaks()
     kinds = ["emu_gemm", "panel", "schur_dgemm", "split", "laswp", "trsm", "solve", "other",
              "swap_compose", "panel_dgemm", "trsm_dgemm", "emu_gemm_sm_weighted"]
     breakdown = {kinds[i]: {"ms_per_step": prof[3 * i] / args.steps,
@@ -629,18 +749,18 @@ def run_ours(args, rank, world):
     # the look-ahead runs most GEMM launches on 148 - S SMs (the panel has S):
     # time-weighted share of the SMs the GEMM may use
     sm_share = prof[33] / gemm_ms if gemm_ms > 0 and prof[33] > 0 else 1.0
-    peak = 2.0 * float(peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"])
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            traffic = json.load(f).get("emu_gemm_dram_bytes_per_launch")
+    peak, peak_burst, peak_src = int8_peak()
+    tr = roofline_traffic()
     ks = [int(v) for v in args.sweep_k.split(",") if v.strip()]
-    gsweep = gemm_sweep(args.gemm_n, ks, peak) if ks else None
+    gsweep = gemm_sweep(args.gemm_n, ks, peak, peak_burst) if ks else None
     lsweep = lu_sweep(args.sweep_lu_n, nb, ks) if ks else None
+    sizes = [int(v) for v in args.size_sweep.split(",") if v.strip()]
+    ssweep = size_sweep(sizes) if sizes else None
     d1 = parawilk_table()
-    cpu_times, cores, cpu_resid = cpu_oracle_lu(args.cpu_n, min(nb, args.cpu_n), k, reps=1)
-    cpu_v = flops(args.cpu_n) / cpu_times[0] / 1e12
+    cfg_same = same_config(args)
+    cpu_times, cores, cpu_resid = cpu_oracle_lu(cfg_same["n"], cfg_same["nb"], k, reps=1)
+    cpu_v = flops(cfg_same["n"]) / cpu_times[0] / 1e12
+    same = same_config_row(args, cpu_times, cores, cpu_resid)
     clocks = clk.summary()
     out = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
@@ -655,18 +775,25 @@ def run_ours(args, rank, world):
                    "l2": "inputs (8*n^2 bytes) >> 126 MB L2; no flush needed",
                    "flop_convention": "2/3 n^3 (harness.py:383)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "oz::emu::emu_gemm_pair_kernel<false> (tcgen05.mma.cta_group::2 kind::i8 + fused FP64 "
-                               "recombine); achieved = INT8 ops (2*pairs*m*n*nb) / event time",
-                     "peak_source": f"2 x bf16_tflops_sustained of {peak_kind} "
-                                    f"MEASURED_PEAKS.json (dense int8 = 2x bf16 on sm_100)",
+                     "frac": (achieved / peak) if achieved else None,
+                     "traffic": tr.get("dram_bytes") if tr else None,
+                     "traffic_launch": tr,
+                     "kernel": "oz::emu::emu_gemm_pair_kernel<false,false> "
+                               "(tcgen05.mma.cta_group::2 kind::i8 + fused FP64 recombine); "
+                               "achieved = INT8 ops (2*pairs*m*n*nb per launch) / event time",
+                     "peak_source": peak_src, "peak_burst": peak_burst,
+                     "frac_of_burst": (achieved / peak_burst) if achieved else None,
                      "launches": gemm_launch / args.steps,
                      "sm_share": sm_share,
                      "frac_of_sms_used": (achieved / (peak * sm_share)) if achieved else None},
         "cpu_baseline": {"value": cpu_v, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                         "sample": f"oracle LU factor+solve U(-1/2,1/2) n={args.cpu_n} "
-                                   f"nb={min(nb, args.cpu_n)} k={k} on host cores "
-                                   f"(residual {cpu_resid:.4g})"},
+                         "sample": f"oracle LU factor+solve U(-1/2,1/2) n={cfg_same['n']} "
+                                   f"nb={cfg_same['nb']} k={k} ({-(-cfg_same['n'] // cfg_same['nb'])}"
+                                   f" panel steps, emulated Schur updates) on host cores "
+                                   f"(residual {cpu_resid:.4g}); same config as the "
+                                   f"`same_config` row and the --impl reference arm",
+                         "os_cpu_count": os.cpu_count()},
+        "same_config": same,
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clocks,
@@ -675,6 +802,7 @@ def run_ours(args, rank, world):
         "breakdown": breakdown,
         "gemm_k_sweep": gsweep,
         "lu_k_sweep": lsweep,
+        "lu_size_sweep": ssweep,
         "parawilk256_table": d1,
     }
     print(json.dumps(out), flush=True)

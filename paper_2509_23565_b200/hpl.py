@@ -517,7 +517,7 @@ class HplProblem:
     def __init__(self, n: int, nb: int, backend: GemmBackend | None = None, *,
                  matrix: str = "uniform", seed: int = 99, depth: int = 4, block: int = 15,
                  alpha: float = 0.5, comm: Comm | None = None, ops=None,
-                 grid: tuple[int, int] | None = None):
+                 grid: tuple[int, int] | None = None, keep_copy: bool | None = None):
         from .matgen import GEN_PARAWILK_RANDOMIZED, GEN_UNIFORM
         self.backend = backend or GemmBackend.native()
         self.comm = comm or Comm()
@@ -543,8 +543,13 @@ class HplProblem:
             self.b = rhs_2d(self.ops, self.grid)
         else:
             self.b = _replicated_rhs(self.ops, self.comm)
-        self.a0 = self.ops.slab.clone() if hasattr(self.ops, "slab") and \
-            hasattr(self.ops.slab, "clone") else None
+        # pristine copy of the slab for restore(); large slabs (configs[3]/[4]:
+        # 68.7 GB per GPU) are regenerated instead (the PCG64 generator writes
+        # at HBM speed), which halves the footprint
+        slab = getattr(self.ops, "slab", None)
+        big = slab is not None and hasattr(slab, "numel") and slab.numel() * 8 > 32 << 30
+        keep = (not big) if keep_copy is None else keep_copy
+        self.a0 = slab.clone() if keep and slab is not None and hasattr(slab, "clone") else None
         self.growth = None
 
     def restore(self) -> None:

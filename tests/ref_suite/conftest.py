@@ -27,9 +27,16 @@ if os.path.isdir(STAGED):
         [ROOT, SHIM] + [p for p in os.environ.get("PYTHONPATH", "").split(os.pathsep) if p])
     import ozemu  # noqa: F401,E402  (installs the alias before the suite imports it)
 
-# test node id suffix -> reason.  Empty: nothing is deselected unless a
-# reference test exercises something outside SURVEY §8 (listed here if so).
-DESELECT: dict[str, str] = {}
+# test node id suffix -> reason.
+DESELECT: dict[str, str] = {
+    "test_gemm.py::TestNativeGemm::test_alpha_beta":
+        "asserts the NATIVE product bit-equal to numpy/OpenBLAS `c - a @ b`; the native "
+        "backend is cuBLAS DGEMM (the north star's FP64 comparator), whose 4x4x4 kernel "
+        "sums in a different order than OpenBLAS's FMA chain (6 of 16 elements differ by "
+        "1 ulp, profiles/r02_native_small_check.log).  The epilogue itself is the "
+        "reference's (oz_axpby, separately rounded); SURVEY §8c pins native FP64 GEMM by "
+        "tolerance only (test_gemm.py:145-154, which passes).",
+}
 
 
 def pytest_collection_modifyitems(config, items):
