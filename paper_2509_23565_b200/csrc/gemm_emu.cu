@@ -64,6 +64,7 @@ struct Params {
   int group_m;  // raster band height in tiles
   int experiment;  // tuning only (OZ_GEMM_EXPERIMENT): 1 = skip FP64 math, 2 = also skip final pass
   int wide;        // slice_bits > 7: (hi, lo) int8 planes per slice
+  int prefetch_c;  // C is read by the final pass: stage it into L2 ahead of it
   unsigned long long* starts;  // tuning only (OZ_GEMM_STARTS): per-CTA start/end globaltimer
   uint8_t pa[MAX_PAIRS];
   uint8_t pb[MAX_PAIRS];
@@ -426,7 +427,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       for (int i = 0; i < 64; ++i) acc[i] = 0.0;
       const int row = mt * P_BM + (int)rank * 128 + quad * 32 + lane;
       const int col0 = nt * P_BN + half * 64;
+      const int pf_group = p.ngroups > 3 ? p.ngroups - 3 : 0;
       for (int q = 0; q < p.ngroups; ++q, ++it) {
+        if (q == pf_group && p.prefetch_c && row < p.m) {
+          // The final pass reads this thread's row of the tile's C block
+          // (64 columns).  Pull those lines into L2 about three groups ahead,
+          // so the read-modify-write runs at L2 rather than DRAM latency and
+          // the next tile's MMAs (at most 4 TMEM slots ahead) wait less on it.
+          const char* pf = reinterpret_cast<const char*>(p.c + (int64_t)col0 * p.ldc + row);
+          const int pc = min(64, p.n - col0);
+          for (int i = 0; i < pc; ++i)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + (int64_t)i * p.ldc * 8));
+        }
         if constexpr (kWide) {
           // slot triple: exact 16384*hh + 128*mid + ll per element, then one
           // reference-order FMA; 16 columns at a time keeps registers in budget
@@ -673,6 +685,8 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, Params& p, cudaStr
   p.group_m = p.inner >= 4096 ? 2 : GROUP_M;
   if (const char* g = getenv("OZ_GEMM_GROUPM")) p.group_m = atoi(g) > 0 ? atoi(g) : p.group_m;
   if (const char* e = getenv("OZ_GEMM_EXPERIMENT")) p.experiment = atoi(e);
+  p.prefetch_c = p.c_is_input && p.beta != 0.0 && p.debug_out == nullptr &&
+                 getenv("OZ_GEMM_NO_PREFETCH") == nullptr;  // tuning switch
   int grid = sm_count() & ~1;
   if (const char* g = getenv("OZ_GEMM_GRID")) grid = atoi(g) > 0 ? (atoi(g) & ~1) : grid;
   if (max_ctas > 0 && grid > (max_ctas & ~1)) grid = max_ctas & ~1;

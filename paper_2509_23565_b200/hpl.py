@@ -89,7 +89,9 @@ class Comm:
         if self.size == 1 or t.numel() == 0:
             return
         if self.stage and t.is_cuda:
-            h = t.cpu()
+            import torch
+            # gloo stages through the host; only the root's contents matter
+            h = t.cpu() if self.rank == src else torch.empty(tuple(t.shape), dtype=t.dtype)
             self.dist.broadcast(h, self._grank(src), group=self.group)
             t.copy_(h)
         else:
