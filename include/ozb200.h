@@ -337,6 +337,15 @@ int oz_scatter_rows(double* a, int64_t lda, const int32_t* rows, int64_t nrows, 
 int oz_scatter_vec(const double* src, int64_t lr0, int64_t count, int64_t nb, int64_t P,
                    int64_t p, double* dst, void* stream);
 
+/* P x Q gathered panel (hpl2d.py): dst[i + c*ldd] = src[blk[i]*src_block +
+ * c*src_ld + row[i]] for i < nrows, c < ncols.  Assembles the all-gathered
+ * local panel slabs of a process column (P stacked column-major blocks of
+ * leading dimension src_ld) into the global panel in row order, and (blk =
+ * NULL) copies a rank's own rows of the factored panel back into its slab. */
+int oz_assemble_rows(const double* src, int64_t src_ld, int64_t src_block, const int32_t* blk,
+                     const int32_t* row, int64_t nrows, int64_t ncols, double* dst, int64_t ldd,
+                     void* stream);
+
 /* Tuning only: with OZ_GEMM_STARTS=1 in the environment every emulated-GEMM
  * launch logs its CTAs' start/end times; this prints the spreads to stderr. */
 int oz_gemm_starts_dump(void);

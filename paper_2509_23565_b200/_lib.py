@@ -81,6 +81,7 @@ _SIGNATURES = {
     "oz_gather_rows": [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp],
     "oz_scatter_rows": [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp],
     "oz_scatter_vec": [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp],
+    "oz_assemble_rows": [_vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _i64, _vp],
     "oz_gemm_starts_dump": [],
     "oz_lookahead_sms": [_i64, _i64, _i64, _int],
 }

@@ -161,6 +161,21 @@ __global__ void scatter_vec_kernel(const double* __restrict__ src, int64_t lr0, 
   if (i < cnt) dst[local_to_global(lr0 + i, nb, P, p)] = src[i];
 }
 
+// dst[i + c*ldd] = src[blk[i]*src_block + c*src_ld + row[i]]: rows picked
+// from P stacked column-major blocks (the all-gathered panel slabs of a
+// process column) into one matrix in global row order, or (blk = null) a
+// plain row gather; one thread per element, coalesced on the dst rows.
+__global__ void assemble_rows_kernel(const double* __restrict__ src, int64_t src_ld,
+                                     int64_t src_block, const int32_t* __restrict__ blk,
+                                     const int32_t* __restrict__ row, int64_t nrows,
+                                     double* __restrict__ dst, int64_t ldd) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t c = blockIdx.y;
+  if (i >= nrows) return;
+  const int64_t b = blk ? blk[i] : 0;
+  dst[i + c * ldd] = src[b * src_block + c * src_ld + row[i]];
+}
+
 }  // namespace
 }  // namespace oz
 
@@ -231,6 +246,20 @@ extern "C" int oz_scatter_vec(const double* src, int64_t lr0, int64_t count, int
   if (count <= 0) return OZ_OK;
   scatter_vec_kernel<<<(unsigned)ceil_div(count, 256), 256, 0, as_stream(stream)>>>(
       src, lr0, count, nb, P, p, dst);
+  OZ_CHECK_LAUNCH();
+  return OZ_OK;
+}
+
+extern "C" int oz_assemble_rows(const double* src, int64_t src_ld, int64_t src_block,
+                                const int32_t* blk, const int32_t* row, int64_t nrows,
+                                int64_t ncols, double* dst, int64_t ldd, void* stream) {
+  using namespace oz;
+  OZ_REQUIRE(nrows >= 0 && ncols >= 0 && ncols <= 65535 && ldd >= nrows, OZ_INVALID_PARAMS,
+             "bad row-assembly shape");
+  if (nrows == 0 || ncols == 0) return OZ_OK;
+  dim3 grid((unsigned)ceil_div(nrows, 256), (unsigned)ncols);
+  assemble_rows_kernel<<<grid, 256, 0, as_stream(stream)>>>(src, src_ld, src_block, blk, row,
+                                                            nrows, dst, ldd);
   OZ_CHECK_LAUNCH();
   return OZ_OK;
 }

@@ -42,7 +42,7 @@ from .gemm import BackendKind, GemmBackend, pair_table
 from .hpl import Comm, _sm_count, check_scaling, local_cols_before, local_ncols
 
 __all__ = ["Grid", "DeviceOps2D", "compose_interchanges", "factor_2d", "solve_2d", "rhs_2d",
-           "residual_2d", "global_rows", "REC_HDR"]
+           "residual_2d", "global_rows", "panel_mode", "REC_HDR"]
 
 REC_HDR = 3                                       # dpanel.cu record header
 
@@ -199,6 +199,45 @@ class DeviceOps2D:
                   int(owns_g), self.nb, self.P, self.p, recs.data_ptr(), self.ipiv_buf.data_ptr(),
                   self.info.data_ptr(), self.bits.data_ptr(), self._st())
 
+    # -- gathered panel (default): one all-gather per panel, then the
+    #    single-GPU recursive panel factorization on every rank of the column
+    def panel_pack(self, lc: int, lr_j: int, jb: int, R: int):
+        """This rank's panel rows lr_j.. (jb columns) as an R x jb column-major
+        block (rows past the local count are zero padding)."""
+        t = self.t
+        buf = t.zeros((max(R, 1) * jb,), dtype=t.float64, device="cuda")
+        mine = self.mloc - lr_j
+        if mine > 0:
+            _lib.call("oz_copy2d", self._a(lc, lr_j), mine, jb, 1, self.ld, buf.data_ptr(), 1, R,
+                      self._st())
+        return buf
+
+    def panel_from_gathered(self, allp, lc: int, lr_j: int, j: int, jb: int, R: int) -> None:
+        """Assemble the global m x jb panel (rows j..n) from the P gathered
+        blocks, factor it with the single-GPU panel kernels (oz_lu_panel:
+        recursive leaves, partial pivoting, interchanges inside the panel),
+        and write this rank's rows of the result back into its slab."""
+        t = self.t
+        n, nb, P = self.n, self.nb, self.P
+        m = n - j
+        g = np.arange(j, n, dtype=np.int64)
+        owner = (g // nb) % P
+        lrj = np.array([local_cols_before(j, nb, P, o) for o in range(P)], dtype=np.int64)
+        row = ((g // nb) // P) * nb + g % nb - lrj[owner]
+        blk_d = self._rows_dev(owner)
+        row_d = self._rows_dev(row)
+        apan = t.empty((m * jb,), dtype=t.float64, device="cuda")
+        _lib.call("oz_assemble_rows", allp.data_ptr(), R, R * jb, blk_d.data_ptr(),
+                  row_d.data_ptr(), m, jb, apan.data_ptr(), m, self._st())
+        _lib.call("oz_lu_panel", apan.data_ptr(), m, m, jb, j, self.ipiv_buf.data_ptr(),
+                  self.info.data_ptr(), self.bits.data_ptr(), self.ws.data_ptr(), self.wsb,
+                  self.n, self.nb, self.planes, 0, self._st())
+        mine = self.mloc - lr_j
+        if mine > 0:
+            back = self._rows_dev(global_rows(n, nb, P, self.p)[lr_j:] - j)
+            _lib.call("oz_assemble_rows", apan.data_ptr(), m, 0, None, back.data_ptr(), mine,
+                      jb, self._a(lc, lr_j), self.ld, self._st())
+
     def panel_finish(self, lc: int, lr_j: int, jb: int, diag: bool) -> None:
         """Growth over the finalized U rows of the diagonal block; pack the
         local panel rows lr_j.. into the broadcast buffer (F-order)."""
@@ -299,12 +338,32 @@ class DeviceOps2D:
 
 
 # ------------------------------------------------------------ the driver
-def factor_2d(ops, grid: Grid, n: int, nb: int):
+def panel_mode() -> str:
+    """OZ_PANEL_2D: 'gather' (default) or 'column' (the per-column exchange)."""
+    import os
+    m = os.environ.get("OZ_PANEL_2D", "gather")
+    if m not in ("gather", "column"):
+        raise InvalidParamsError(f"OZ_PANEL_2D must be gather or column, got {m!r}")
+    return m
+
+
+def factor_2d(ops, grid: Grid, n: int, nb: int, mode: str | None = None):
     """Blocked right-looking LU (solve.py:94-140) on the P x Q grid.
-    Returns (ipiv int32[n] global LAPACK-style, growth)."""
+    Returns (ipiv int32[n] global LAPACK-style, growth).
+
+    Panel modes (the P ranks of the owner process column):
+    * 'gather' (default): ONE all-gather of the ranks' panel rows per panel,
+      then every rank of the column factors the whole m x jb panel with the
+      single-GPU recursive panel kernels (identical inputs -> identical
+      pivots and factors on every rank) and keeps its own rows -- one host
+      round trip per panel instead of jb, and the blocked panel instead of
+      the level-2 column loop;
+    * 'column': one all-gather of small candidate records per panel column,
+      the reference's unblocked loop (solve.py:75-90) distributed."""
     P, Q, p, q = grid.P, grid.Q, grid.p, grid.q
     ncl = ops.ncl
     nblk = -(-n // nb)
+    mode = mode or panel_mode()
     ops.begin()
     for jblk in range(nblk):
         j = jblk * nb
@@ -312,7 +371,12 @@ def factor_2d(ops, grid: Grid, n: int, nb: int):
         pr, pc = jblk % P, jblk % Q
         lc = (jblk // Q) * nb
         lr_j = local_cols_before(j, nb, P, p)
-        if q == pc:                                   # panel, one column at a time
+        if q == pc and mode == "gather":              # panel: one exchange
+            R = max(local_ncols(n, nb, P, o) - local_cols_before(j, nb, P, o) for o in range(P))
+            allp = grid.col.allgather(ops.panel_pack(lc, lr_j, jb, R))
+            ops.panel_from_gathered(allp, lc, lr_j, j, jb, R)
+            ops.panel_finish(lc, lr_j, jb, p == pr)
+        elif q == pc:                                 # panel, one column at a time
             for t in range(jb):
                 g = j + t
                 owns_g = (g // nb) % P == p

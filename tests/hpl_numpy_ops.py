@@ -224,6 +224,43 @@ class NumpyOps2D:
                 a[r0:, lc + t + 1:lc + jb] -= np.outer(a[r0:, lc + t], rw[3 + t + 1:3 + jb])
                 self.seen = max(self.seen, float(np.abs(a[r0:, lc + t + 1:lc + jb]).max()))
 
+    def panel_pack(self, lc, lr_j, jb, R):
+        buf = np.zeros((jb, max(R, 1)))
+        mine = self.mloc - lr_j
+        if mine > 0:
+            buf[:, :mine] = self.slab[lr_j:, lc:lc + jb].T
+        return torch.from_numpy(buf.ravel().copy())
+
+    def panel_from_gathered(self, allp, lc, lr_j, j, jb, R):
+        """The gathered panel factored by the reference's unblocked loop
+        (solve.py:75-90) on the global m x jb panel; own rows written back."""
+        from paper_2509_23565_b200.hpl import local_cols_before
+        n, nb, P = self.n, self.nb, self.P
+        blocks = allp.numpy().reshape((P, jb, max(R, 1)))
+        g = np.arange(j, n)
+        owner = (g // nb) % P
+        lrj = np.array([local_cols_before(j, nb, P, o) for o in range(P)])
+        row = ((g // nb) // P) * nb + g % nb - lrj[owner]
+        pan = np.asfortranarray(blocks[owner, :, row])          # m x jb
+        m = n - j
+        for t in range(jb):
+            pr = t + int(np.argmax(np.abs(pan[t:, t])))
+            self.ipiv_buf[t] = j + pr
+            if pan[pr, t] == 0.0:
+                if not self.info:
+                    self.info = j + t + 1
+                continue
+            if pr != t:
+                pan[[t, pr], :] = pan[[pr, t], :]
+            if t + 1 < m:
+                pan[t + 1:, t] /= pan[t, t]
+                if t + 1 < jb:
+                    pan[t + 1:, t + 1:] -= np.outer(pan[t + 1:, t], pan[t, t + 1:])
+                    self.seen = max(self.seen, float(np.abs(pan[t + 1:, t + 1:]).max()))
+        mine = self.mloc - lr_j
+        if mine > 0:
+            self.slab[lr_j:, lc:lc + jb] = pan[self.grows[lr_j:] - j, :]
+
     def panel_finish(self, lc, lr_j, jb, diag):
         if diag:
             self.seen = max(self.seen, float(np.abs(np.triu(
