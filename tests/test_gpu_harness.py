@@ -96,7 +96,12 @@ def test_gemm_error_profile_on_device_output():
     assert rc == 0
     lines = buf.getvalue().splitlines()
     assert lines[0] == "# ozemu csv v1 experiment=gemm"
-    fields = dict(zip(lines[1].split(","), lines[2].split(",")))
+    # the reference writes the backend tag (which contains commas) unquoted
+    # (cli.py:164-170), so the row is parsed from both ends
+    head, row = lines[1].split(","), lines[2].split(",")
+    assert head[:3] == ["m", "n", "p"] and row[:3] == ["24", "24", "24"]
+    fields = dict(zip(head[-4:], row[-4:]))
+    assert ",".join(row[3:-5]) == GemmBackend.int8(5).describe() and row[-5] == "1"
     prof = gemm_error_profile(GemmBackend.int8(5), oz_uniform(24, 3), oz_uniform(24, 4),
                               rng_seed=3)
     assert float(fields["max_rel_error"]) == float(f"{prof.max_rel_error:.10g}")
