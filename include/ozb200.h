@@ -349,6 +349,10 @@ int oz_assemble_rows(const double* src, int64_t src_ld, int64_t src_block, const
 /* Tuning only: with OZ_GEMM_STARTS=1 in the environment every emulated-GEMM
  * launch logs its CTAs' start/end times; this prints the spreads to stderr. */
 int oz_gemm_starts_dump(void);
+/* Tuning only (OZ_PANEL_TIMING=1): copy and clear the 8 panel-leaf phase
+ * counters (clock64 sums of CTA 0 thread 0: argmax, reduce, push, deferred
+ * update, wait, step tail; [6] owner record+push; [7] steps). */
+int oz_panel_debug_counters(unsigned long long* out8);
 
 #ifdef __cplusplus
 }

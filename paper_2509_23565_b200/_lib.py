@@ -83,6 +83,7 @@ _SIGNATURES = {
     "oz_scatter_vec": [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp],
     "oz_assemble_rows": [_vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _i64, _vp],
     "oz_gemm_starts_dump": [],
+    "oz_panel_debug_counters": [_vp],
     "oz_lookahead_sms": [_i64, _i64, _i64, _int],
 }
 _RESTYPES = {

@@ -461,6 +461,8 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
   }
 }
 
+#include "panel_leaf.cuh"
+
 // Apply a gather list (<= 2*PANEL_W entries) to columns [c0a,c1a) U [c0b,c1b):
 // one warp per column, entries staged in registers (read all, then write).
 constexpr int LIST_PER_LANE = (2 * PANEL_W + 31) / 32;
@@ -1174,6 +1176,124 @@ bool cluster_fits(int G, size_t smem) {
   return ok;
 }
 
+// Register-resident leaf (panel_leaf.cuh) for short panels: OZ_PANEL_LEAF=0
+// disables it (tuning / A-B).  Variant = W*10 + RPT: rows per CTA 256*RPT,
+// at most LEAF_MAXG CTAs in the cluster, W*RPT <= 64 doubles per thread.
+bool leaf_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("OZ_PANEL_LEAF");
+    return e == nullptr || atoi(e) != 0;
+  }();
+  return v;
+}
+// Measured (scripts/panel_probe.py, standalone m x 1024 panels): the register
+// leaf wins where it keeps the 64-column window (m <= 16 x 256 rows: 2.0 vs
+// 3.1 ms of leaf time at m = 2048); the narrower windows it would need for
+// taller panels double the recursion's inner nodes and lose inside the LU.
+// OZ_PANEL_LEAF_RPT=2/4 admits those variants (tuning).
+int leaf_max_rpt() {
+  static const int v = [] {
+    const char* e = getenv("OZ_PANEL_LEAF_RPT");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+int leaf_variant(int64_t m, int w, int max_ctas) {
+  if (!leaf_enabled() || m < 1) return 0;
+  const int rpt = leaf_max_rpt();
+  int v = 0, rows = 0;
+  if (w <= 64 && m <= (int64_t)LEAF_MAXG * 128) {
+    v = 6411;  // 128 threads x 1 row
+    rows = 128;
+  } else if (w <= 64 && m <= (int64_t)LEAF_MAXG * 256) {
+    v = w <= 32 ? 3212 : 6412;
+    rows = 256;
+  } else if (rpt >= 2 && w <= 32 && m <= (int64_t)LEAF_MAXG * 512) {
+    v = 3222;
+    rows = 512;
+  } else if (rpt >= 4 && w <= 16 && m <= (int64_t)LEAF_MAXG * 1024) {
+    v = 1642;
+    rows = 1024;
+  }
+  // the cluster must fit in the SMs the caller may use (look-ahead side stream)
+  if (v != 0 && max_ctas > 0 && ceil_div(m, (int64_t)rows) > max_ctas) return 0;
+  return v;
+}
+// widest leaf the register variant takes at this height (0: none)
+int leaf_width_for(int64_t m, int max_ctas) {
+  const int rpt = leaf_max_rpt();
+  if (!leaf_enabled()) return 0;
+  if (m <= (int64_t)LEAF_MAXG * 256)
+    return ceil_div(m, (int64_t)(m <= (int64_t)LEAF_MAXG * 128 ? 128 : 256)) <= max_ctas ? 64 : 0;
+  if (rpt >= 2 && m <= (int64_t)LEAF_MAXG * 512) return ceil_div(m, (int64_t)512) <= max_ctas ? 32 : 0;
+  if (rpt >= 4 && m <= (int64_t)LEAF_MAXG * 1024) return ceil_div(m, (int64_t)1024) <= max_ctas ? 16 : 0;
+  return 0;
+}
+
+template <int W, int RPT, int NT>
+int panel_leaf_launch(const PanelArgs& pa, cudaStream_t st) {
+  constexpr size_t smem = leaf_smem_bytes<W, RPT, NT>();
+  OZ_ONCE([] {
+    cudaError_t e = cudaFuncSetAttribute(panel_leaf_kernel<W, RPT, NT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(panel_leaf_kernel<W, RPT, NT>,
+                               cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return e;
+  }());
+  const int G = (int)ceil_div(pa.m, (int64_t)NT * RPT);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = G;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  OZ_CHECK_CUDA(cudaLaunchKernelEx(&cfg, panel_leaf_kernel<W, RPT, NT>, pa));
+  return OZ_OK;
+}
+
+int panel_leaf(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t base, int32_t* ipiv,
+               int32_t* info, unsigned long long* growth, const LuWs& ws, cudaStream_t st,
+               int max_ctas) {
+  PanelArgs pa;
+  pa.a = a;
+  pa.lda = lda;
+  pa.r0 = r0;
+  pa.m = m;
+  pa.base = base;
+  pa.w = w;
+  pa.rows_per_cta = 0;
+  pa.ipiv = ipiv;
+  pa.growth = growth;
+  pa.info = info;
+  pa.bar = ws.bar;
+  pa.cand = ws.cand;
+  pa.list_dst = ws.swap_dst;
+  pa.list_src = ws.swap_src;
+  pa.list_cnt = ws.swap_cnt;
+  pa.dbg = panel_dbg();
+  OZ_CHECK_CUDA(cudaMemsetAsync(ws.swap_cnt, 0, sizeof(int32_t), st));
+  const int tag = prof_start(st);
+  count_launch();
+  int s = OZ_OK;
+  switch (leaf_variant(m, w, max_ctas)) {
+    case 6411: s = panel_leaf_launch<64, 1, 128>(pa, st); break;
+    case 6412: s = panel_leaf_launch<64, 1, 256>(pa, st); break;
+    case 3212: s = panel_leaf_launch<32, 1, 256>(pa, st); break;
+    case 3222: s = panel_leaf_launch<32, 2, 256>(pa, st); break;
+    case 1642: s = panel_leaf_launch<16, 4, 256>(pa, st); break;
+    default: s = OZ_UNSUPPORTED;
+  }
+  prof_stop(tag, st, PROF_PANEL, (double)m * w);
+  return s;
+}
+
 int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t base,
                  int32_t* ipiv, int32_t* info, unsigned long long* growth, const LuWs& ws,
                  cudaStream_t st, int max_ctas) {
@@ -1190,6 +1310,8 @@ int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t b
     return e;
   }());
   const int sms = max_ctas > 0 && max_ctas < sm_count() ? max_ctas : sm_count();
+  if (leaf_variant(m, w, max_ctas) != 0)
+    return panel_leaf(a, lda, r0, m, w, base, ipiv, info, growth, ws, st, max_ctas);
   const size_t cap = (size_t)panel_smem_cap();
   // cluster variant: as few CTAs as the slab allows, at most the cluster size
   const int cmax = panel_cluster_max();
@@ -1321,6 +1443,7 @@ int laswp_ipiv(double* a, int64_t lda, int64_t c0a, int64_t c1a, int64_t c0b, in
 // Widest window (<= PANEL_W) whose m-row slab fits in the shared memory of
 // max_ctas CTAs: tall panels (distributed runs, m ~ 1e5) use narrower windows.
 int panel_width_for(int64_t m, int max_ctas) {
+  if (const int lw = leaf_width_for(m, max_ctas)) return lw;
   const int64_t cap = panel_smem_cap();
   // short panels go to the cluster variant (<= panel_cluster_max() CTAs):
   // the window must fit m / cmax rows per CTA
@@ -2163,4 +2286,17 @@ extern "C" int oz_schur_cols(int backend, int64_t m, int64_t ncols, int64_t jb,
   const Schur s{backend, m, ncols, jb, a21, lda21, u12, ldu, a22, lda22, num_slices, slice_bits,
                 npairs, pair_a, pair_b, pair_shift, growth_bits};
   return schur_cols(s, c0, c1, w, as_stream(stream), max_ctas);
+}
+
+// Tuning only (OZ_PANEL_TIMING=1): copy and clear the 8 panel debug counters.
+extern "C" int oz_panel_debug_counters(unsigned long long* out8) {
+  unsigned long long* d = oz::panel_dbg();
+  if (d == nullptr) {
+    for (int i = 0; i < 8; ++i) out8[i] = 0;
+    return OZ_OK;
+  }
+  OZ_CHECK_CUDA(cudaDeviceSynchronize());
+  OZ_CHECK_CUDA(cudaMemcpy(out8, d, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  OZ_CHECK_CUDA(cudaMemset(d, 0, 8 * sizeof(unsigned long long)));
+  return OZ_OK;
 }
