@@ -1186,15 +1186,17 @@ bool leaf_enabled() {
   }();
   return v;
 }
-// Measured (scripts/panel_probe.py, standalone m x 1024 panels): the register
-// leaf wins where it keeps the 64-column window (m <= 16 x 256 rows: 2.0 vs
-// 3.1 ms of leaf time at m = 2048); the narrower windows it would need for
-// taller panels double the recursion's inner nodes and lose inside the LU.
-// OZ_PANEL_LEAF_RPT=2/4 admits those variants (tuning).
+// Rows per thread the register leaf may use (OZ_PANEL_LEAF_RPT, tuning).
+// Measured, LU factor time n = 8192 / 16384 / 32768, k = 7
+// (profiles/r02_leaf_rpt_ab.txt): RPT 1 (64-column windows up to 4096 rows)
+// 43.8 / 119.0 / 507 ms; RPT 2 (also 32-column windows up to 8192 rows)
+// 38.9 / 114.0 / 504 ms; RPT 4 (also 16-column windows up to 16384 rows)
+// 38.9 / 134.6 / 528 ms (the narrow windows double the recursion's inner
+// nodes); shared-memory leaf only 49.9 / 123.7 / 508 ms.
 int leaf_max_rpt() {
   static const int v = [] {
     const char* e = getenv("OZ_PANEL_LEAF_RPT");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 2;
   }();
   return v;
 }
