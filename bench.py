@@ -352,7 +352,8 @@ def gemm_sweep(n, ks, int8_peak, int8_burst=None, reps=2, comm=None):
     rank = comm.rank if comm is not None else 0
     lo, hi = row_shard(n, world, rank)            # N > 1: rows of A and C, B replicated
     mrows = hi - lo
-    a = generate_device(0, n, seed=2)[lo:hi]
+    a_full_view = generate_device(0, n, seed=2)
+    a = a_full_view[lo:hi]
     b = generate_device(0, n, seed=3)
     out = torch.empty((mrows, n), dtype=torch.float64, device="cuda")
     fl = 2.0 * n ** 3
@@ -369,17 +370,33 @@ def gemm_sweep(n, ks, int8_peak, int8_burst=None, reps=2, comm=None):
            "native_fp64": {"ms": t * 1e3, "tflops": fl / t / 1e12,
                            "frac_of_fp64_nominal": fl / t / 1e12 / world / FP64_NOMINAL_TFLOPS},
            "emulated": []}
+    from paper_2509_23565_b200.dist import gemm_row_sharded
+
+    def shard_into(bk_, alpha, aa, bb, beta, cc):   # the rank's shard, in place
+        emulated_into(bk_, aa, bb, alpha, beta, out, False)
+        return out
+
     for k in ks:
         bk = oz.GemmBackend.int8(k)
         npairs = k * (k + 1) // 2
-        t = tmax(lambda: emulated_into(bk, a, b, 1.0, 0.0, out, False))
+        if comm is not None:
+            # N > 1: the public row-sharded entry (dist.gemm_row_sharded) on the
+            # full A view, no gather (each rank keeps its rows of C)
+            a_full = a_full_view
+
+            def step():
+                gemm_row_sharded(bk, 1.0, a_full, b, 0.0, None, gather=False,
+                                 rank_world=(rank, world), compute=shard_into)
+            t = tmax(step)
+        else:
+            t = tmax(lambda: emulated_into(bk, a, b, 1.0, 0.0, out, False))
         int8 = npairs * fl / t / 1e12 / world       # per-GPU fraction of the roofline
         res["emulated"].append({"k": k, "pairs": npairs, "ms": t * 1e3,
                                 "tflops_fp64_equiv": fl / t / 1e12,
                                 "int8_tops_per_gpu": int8, "frac_of_int8_peak": int8 / int8_peak,
                                 "frac_of_int8_burst": int8 / int8_burst if int8_burst else None,
                                 "fp64_equiv_roofline_tflops": world * int8_peak / npairs})
-    del a, b, out
+    del a, a_full_view, b, out
     torch.cuda.empty_cache()
     return res
 

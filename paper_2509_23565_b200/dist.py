@@ -1,23 +1,16 @@
-"""Multi-GPU plumbing for the hot path.
+"""Multi-GPU standalone GEMM (SURVEY §8(e), configs[2] at N > 1).
 
 One process per GPU over torch.distributed (NCCL on B200s, gloo in the CPU
-tests).  Two pieces:
-
-* ``row_shard`` / ``gemm_row_sharded``: the standalone emulated DGEMM shards
-  naturally — A and C are split by rows, B is replicated, no exchange in the
-  data path except the final optional all-gather of C.
-* ``BlockCyclic``: the 2D block-cyclic index maps (P x Q process grid, nb x nb
-  blocks) of the distributed HPL layout: owner of a global block, global <->
-  local index translation and local extents.  These are the maps the
-  distributed LU driver uses for the panel / U12 broadcasts along process
-  rows / columns.
+tests).  The emulated DGEMM shards naturally: A and C are split by rows
+(``row_shard``), B is replicated, and there is no exchange in the data path
+except the optional final all-gather of C (``gemm_row_sharded``).  bench.py's
+N > 1 D3 row times exactly this per-rank shard.  The distributed LU keeps
+its own block-cyclic maps (hpl.py: local_cols_before / global_cols).
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass
-
-__all__ = ["row_shard", "BlockCyclic", "gemm_row_sharded"]
+__all__ = ["row_shard", "gemm_row_sharded"]
 
 
 def row_shard(m: int, world: int, rank: int) -> tuple[int, int]:
@@ -30,55 +23,12 @@ def row_shard(m: int, world: int, rank: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < extra else 0)
 
 
-@dataclass(frozen=True)
-class BlockCyclic:
-    """2D block-cyclic distribution of an n x n matrix over a P x Q grid."""
-
-    n: int
-    nb: int
-    P: int
-    Q: int
-
-    def owner(self, gi: int, gj: int) -> tuple[int, int]:
-        """(process row, process column) owning global element (gi, gj)."""
-        return (gi // self.nb) % self.P, (gj // self.nb) % self.Q
-
-    def rank_of(self, prow: int, pcol: int) -> int:
-        return prow * self.Q + pcol            # row-major grid
-
-    def coords(self, rank: int) -> tuple[int, int]:
-        return divmod(rank, self.Q)
-
-    @staticmethod
-    def _local_extent(n, nb, p, iproc):
-        nblocks = -(-n // nb)
-        full, rem = divmod(nblocks, p)
-        count = full + (1 if iproc < rem else 0)
-        size = count * nb
-        last_block = nblocks - 1
-        if last_block % p == iproc and n % nb:
-            size -= nb - n % nb
-        return max(size, 0)
-
-    def local_shape(self, rank: int) -> tuple[int, int]:
-        pr, pc = self.coords(rank)
-        return (self._local_extent(self.n, self.nb, self.P, pr),
-                self._local_extent(self.n, self.nb, self.Q, pc))
-
-    def g2l(self, g: int, p: int) -> int:
-        """Global index -> local index on its owner (along one dimension)."""
-        return (g // (self.nb * p)) * self.nb + g % self.nb
-
-    def l2g(self, l: int, iproc: int, p: int) -> int:
-        """Local index on process `iproc` -> global index (along one dimension)."""
-        return ((l // self.nb) * p + iproc) * self.nb + l % self.nb
-
-
 def gemm_row_sharded(backend, alpha, a, b, beta, c=None, *, group=None, gather=True,
-                     compute=None):
+                     compute=None, rank_world=None):
     """Row-sharded alpha*A@B + beta*C.  Every rank holds the full A/B/C (or
     views of them) and computes rows row_shard(m) with the emulated GEMM on
-    its own GPU; with `gather` the shards are all-gathered so every rank
+    its own GPU (rank_world=(rank, world) overrides the process group, e.g.
+    bench.py's own communicator); with `gather` the shards are all-gathered so every rank
     returns the full product.  `compute` defaults to the package's gemm()."""
     import torch
     import torch.distributed as dist
@@ -86,8 +36,11 @@ def gemm_row_sharded(backend, alpha, a, b, beta, c=None, *, group=None, gather=T
     from . import gemm as _gemm
 
     compute = compute or _gemm.gemm
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if rank_world is not None:
+        rank, world = rank_world
+    else:
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
     m = int(a.shape[0])
     lo, hi = row_shard(m, world, rank)
     part = compute(backend, alpha, a[lo:hi], b, beta, None if c is None else c[lo:hi])

@@ -1,5 +1,5 @@
-"""CPU: the multi-GPU host plumbing (row sharding, block-cyclic index maps,
-all-gather of shards) with world_size=2 over gloo.  The per-shard compute is
+"""CPU: the multi-GPU host plumbing (row sharding, the block-cyclic column
+maps of the distributed LU, all-gather of shards) with world_size=2 over gloo.  The per-shard compute is
 the oracle here (no GPU in this container); on B200s it is the tcgen05 GEMM."""
 
 import os
@@ -9,7 +9,8 @@ import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
-from paper_2509_23565_b200.dist import BlockCyclic, row_shard
+from paper_2509_23565_b200.dist import row_shard
+from paper_2509_23565_b200.hpl import global_cols, local_cols_before, local_ncols
 
 
 def test_row_shard_partitions():
@@ -22,23 +23,21 @@ def test_row_shard_partitions():
             assert max(sizes) - min(sizes) <= 1
 
 
-@pytest.mark.parametrize("n,nb,P,Q", [(1000, 64, 2, 4), (130, 16, 1, 8), (512, 512, 2, 2),
-                                      (777, 50, 3, 2)])
-def test_block_cyclic_maps_roundtrip(n, nb, P, Q):
-    bc = BlockCyclic(n, nb, P, Q)
-    counts = np.zeros((P, Q), dtype=np.int64)
-    rows_per = [bc.local_shape(bc.rank_of(p, 0))[0] for p in range(P)]
-    cols_per = [bc.local_shape(bc.rank_of(0, q))[1] for q in range(Q)]
-    assert sum(rows_per) == n and sum(cols_per) == n
-    for g in range(n):
-        p = (g // nb) % P
-        l = bc.g2l(g, P)
-        assert bc.l2g(l, p, P) == g
-        assert 0 <= l < rows_per[p]
-    for gi in range(0, n, 37):
-        for gj in range(0, n, 41):
-            counts[bc.owner(gi, gj)] += 1
-    assert counts.sum() > 0
+@pytest.mark.parametrize("n,nb,Q", [(1000, 64, 4), (130, 16, 8), (512, 512, 2), (777, 50, 3),
+                                    (262144, 1024, 8)])
+def test_block_cyclic_maps_roundtrip(n, nb, Q):
+    """The 1 x Q (and, per process row/column, P x Q) maps hpl.py / hpl2d.py
+    use: column block b lives on rank b % Q as local block b // Q."""
+    cols = [global_cols(n, nb, Q, q) for q in range(Q)]
+    assert sum(local_ncols(n, nb, Q, q) for q in range(Q)) == n
+    allc = np.sort(np.concatenate(cols))
+    assert np.array_equal(allc, np.arange(n))
+    for q in range(Q):
+        assert len(cols[q]) == local_ncols(n, nb, Q, q)
+        assert all(((g // nb) % Q) == q for g in cols[q][:: max(1, len(cols[q]) // 50)])
+        for g in range(0, n, max(1, n // 97)):
+            # local index of the first of q's columns at or after g
+            assert local_cols_before(g, nb, Q, q) == int(np.searchsorted(cols[q], g))
 
 
 def _free_port():
