@@ -1622,6 +1622,53 @@ int lookahead_split(int setting, int64_t m, int64_t nb, int npairs, int sms, int
   return best;
 }
 
+// Two-phase look-ahead (emulated backend, single GPU): the next panel runs on S
+// CTAs of a side stream while the first X columns of this step's Schur update
+// run on the other sms - S; the remaining columns start once the panel is done,
+// on every SM.  A tall panel is latency-bound (it speeds up far less than
+// linearly in S), so a larger S for a shorter time beats a narrow S for the
+// whole step.  Model (fit to OZ_LU_TRACE timelines at n = 32768, in-LU times,
+// GEMM running beside the panel): panel ~ nb * (5.2 us + 0.012 us * m / S);
+// GEMM 2.4e15 INT8 ops/s on all SMs; interchanges + trsm + split of the rest
+// before the GEMM ~ 0.8 ms + 0.117 us per column.  OZ_LA_TWO_PHASE=0 keeps the
+// single-phase split (lookahead_split).
+struct LaPlan {
+  int sms;         // panel CTAs
+  int64_t cols1;   // columns of the rest updated beside the panel (phase 1)
+};
+bool la_two_phase() {
+  static const bool v = [] {
+    const char* e = getenv("OZ_LA_TWO_PHASE");
+    return e == nullptr || atoi(e) != 0;
+  }();
+  return v;
+}
+LaPlan lookahead_plan(int setting, int64_t m, int64_t nb, int npairs, int sms, int64_t rest) {
+  LaPlan best{lookahead_split(setting, m, nb, npairs, sms), rest};
+  if (!la_two_phase() || setting >= 0 || npairs <= 0 || rest <= 0) return best;
+  const double rate = 2.4e15;
+  const double ops_per_col = 2.0 * npairs * (double)m * (double)nb;
+  const double t_lt = 0.8e-3 + 1.17e-7 * (double)rest;
+  double best_t = 1e30;
+  for (int s = 16; s <= sms - 16; s += 2) {
+    const double tp = (double)nb * (5.2e-6 + 1.2e-8 * (double)m / s);
+    const double r1 = rate * (double)(sms - s) / sms;
+    // phase-1 columns: what the reduced grid finishes while the panel runs
+    double x = (tp - t_lt) * r1 / ops_per_col;
+    if (x < 0) x = 0;
+    if (x > (double)rest) x = (double)rest;
+    const double t1 = t_lt + x * ops_per_col / r1;
+    const double t = (t1 > tp ? t1 : tp) + ((double)rest - x) * ops_per_col / rate;
+    if (t < best_t) {
+      best_t = t;
+      best.sms = s;
+      // round phase 1 to whole 128-column GEMM tiles
+      best.cols1 = std::min<int64_t>(rest, ((int64_t)x + 127) / 128 * 128);
+    }
+  }
+  return best;
+}
+
 // OZ_LU_TRACE=1: per-step event timeline of the driver on stderr (tuning only)
 struct LuTrace {
   bool on = false;
@@ -1861,8 +1908,12 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
       tr.mark(st);  // 4 after the update of the next panel's columns
       double* p2 = a + (j + jb) * lda + (j + jb);
       if (la) {
-        const int la_sms = lookahead_split(la_setting, rest, jb, backend != 0 ? npairs : 0,
-                                           sm_count());
+        // columns [jb2, rest) of this step: phase 1 [jb2, jb2 + cols1) beside
+        // the panel on sms - S CTAs, phase 2 on every SM after it
+        const LaPlan plan = lookahead_plan(la_setting, rest, jb, backend != 0 ? npairs : 0,
+                                           sm_count(), rest - jb2);
+        const int la_sms = plan.sms;
+        const int64_t p1_end = jb2 + plan.cols1;
         if (tr.on) tr.split.push_back(la_sms);
         OZ_CHECK_CUDA(cudaEventRecord(side->ready, st));
         OZ_CHECK_CUDA(cudaStreamWaitEvent(side->st, side->ready, 0));
@@ -1892,7 +1943,11 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
           tr.mark_sub(st);
           OZ_TRY(schur_split_part(sc, false, jb2, rest, ws, st));
           tr.mark_sub(st);
-          OZ_TRY(schur_cols(sc, jb2, rest, ws, st, sm_count() - la_sms));
+          OZ_TRY(schur_cols(sc, jb2, p1_end, ws, st, sm_count() - la_sms));
+          if (p1_end < rest) {
+            OZ_CHECK_CUDA(cudaStreamWaitEvent(st, side->done, 0));
+            OZ_TRY(schur_cols(sc, p1_end, rest, ws, st));
+          }
         }
         tr.mark(st);  // 6 after the rest of the step
         OZ_CHECK_CUDA(cudaStreamWaitEvent(st, side->done, 0));
