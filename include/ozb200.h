@@ -239,10 +239,15 @@ int oz_lu_panel(double* a, int64_t lda, int64_t m, int64_t jb, int64_t base, int
                 int32_t* info, unsigned long long* growth_bits, void* workspace,
                 size_t workspace_bytes, int64_t ws_n, int64_t ws_nb, int ws_slices,
                 int max_ctas, void* stream);
-/* SMs the look-ahead model gives a panel of m rows factored beside a trailing
- * update of m x ncols (0: no look-ahead); npairs = 0 for the native backend.
- * With ncols = m it is the single-GPU driver's split. */
+/* SMs the look-ahead model gives the panel of an m-row trailing matrix
+ * (0: no look-ahead); npairs = 0 for the native backend.  A function of m
+ * only (ncols is accepted for ABI stability), identical in every driver, so
+ * the panel's factors do not depend on how the columns are distributed. */
 int oz_lookahead_sms(int64_t m, int64_t ncols, int64_t nb, int npairs);
+/* Two-phase look-ahead: how many of this rank's rest_cols trailing columns
+ * (the next panel's excluded) to update on sms - panel_sms SMs while the
+ * panel runs; the remaining columns go on every SM once it is done. */
+int64_t oz_lookahead_cols1(int64_t m, int64_t rest_cols, int64_t nb, int npairs, int panel_sms);
 int oz_laswp(double* a, int64_t lda, int64_t c0a, int64_t c1a, int64_t c0b, int64_t c1b,
              int64_t k1, const int32_t* ipiv, int npiv, void* workspace,
              size_t workspace_bytes, int64_t ws_n, int64_t ws_nb, int ws_slices, void* stream);

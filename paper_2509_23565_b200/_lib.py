@@ -85,10 +85,12 @@ _SIGNATURES = {
     "oz_gemm_starts_dump": [],
     "oz_panel_debug_counters": [_vp],
     "oz_lookahead_sms": [_i64, _i64, _i64, _int],
+    "oz_lookahead_cols1": [_i64, _i64, _i64, _int, _int],
 }
 _RESTYPES = {
     "oz_launch_count": C.c_longlong,
     "oz_lookahead_sms": C.c_int,
+    "oz_lookahead_cols1": C.c_int64,
     "oz_split_aux_bytes": C.c_size_t,
     "oz_lu_workspace_bytes": C.c_size_t,
     "oz_lu_solve_workspace_bytes": C.c_size_t,

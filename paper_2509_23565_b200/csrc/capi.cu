@@ -116,6 +116,25 @@ int dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha,
   return OZ_OK;
 }
 
+// B (jb x n) <- L^{-1} B, L unit lower triangular (cuBLAS DTRSM; the wide
+// trsm of the LU when OZ_TRSM_CUBLAS=1, tuning A/B against trsm_rec)
+int dtrsm_lunit(int64_t jb, int64_t n, const double* l, int64_t ldl, double* b, int64_t ldb,
+                cudaStream_t st, int sm_target) {
+  if (jb == 0 || n == 0) return OZ_OK;
+  cublasHandle_t h = cublas_handle(st);
+  OZ_REQUIRE(h != nullptr, OZ_CUDA_ERROR, "cublasCreate failed");
+  OZ_REQUIRE(cublasSetStream(h, st) == CUBLAS_STATUS_SUCCESS, OZ_CUDA_ERROR,
+             "cublasSetStream failed");
+  OZ_REQUIRE(cublasSetSmCountTarget(h, sm_target > 0 ? sm_target : 0) == CUBLAS_STATUS_SUCCESS,
+             OZ_CUDA_ERROR, "cublasSetSmCountTarget failed");
+  const double one = 1.0;
+  cublasStatus_t s = cublasDtrsm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
+                                 CUBLAS_DIAG_UNIT, (int)jb, (int)n, &one, l, (int)ldl, b,
+                                 (int)ldb);
+  OZ_REQUIRE(s == CUBLAS_STATUS_SUCCESS, OZ_CUDA_ERROR, "cublasDtrsm failed (%d)", (int)s);
+  return OZ_OK;
+}
+
 }  // namespace oz
 
 extern "C" const char* oz_last_error(void) { return oz::last_error(); }

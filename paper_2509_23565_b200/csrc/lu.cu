@@ -53,6 +53,8 @@ void keep_pool_mapped() {
 
 namespace oz {
 
+int dtrsm_lunit(int64_t jb, int64_t n, const double* l, int64_t ldl, double* b, int64_t ldb,
+                cudaStream_t st, int sm_target);
 int dgemm(int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha, const double* a,
           int64_t lda, const double* b, int64_t ldb, double beta, double* c, int64_t ldc,
           cudaStream_t st, int sm_target = 0);
@@ -1119,6 +1121,13 @@ int trsm_blocked(double* a, int64_t lda, int64_t j, int64_t jb, double* b, int64
     prof_stop(tag, st, PROF_TRSM, (double)jb * jb * ncols);
     return s;
   }
+  static const bool use_cublas = getenv("OZ_TRSM_CUBLAS") != nullptr;  // tuning A/B
+  if (use_cublas) {
+    const int tag = prof_start(st);
+    const int s = dtrsm_lunit(jb, ncols, a + j * lda + j, lda, b, ldb, st, max_ctas);
+    prof_stop(tag, st, PROF_TRSM, (double)jb * jb * ncols);
+    return s;
+  }
   OZ_ONCE(cudaFuncSetAttribute(trsm_unit_lower_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)TRSM_SMEM));
   return trsm_rec(a, lda, j, jb, b, ldb, ncols, st, max_ctas);
@@ -1643,6 +1652,20 @@ bool la_two_phase() {
   }();
   return v;
 }
+// phase-1 width for a given S: the columns sms - S SMs update while the panel runs
+int64_t phase1_cols(int s, int64_t m, int64_t nb, int npairs, int sms, int64_t rest) {
+  if (rest <= 0 || npairs <= 0) return rest > 0 ? rest : 0;
+  const double rate = 2.4e15;
+  const double ops_per_col = 2.0 * npairs * (double)m * (double)nb;
+  const double t_lt = 0.8e-3 + 1.17e-7 * (double)rest;
+  const double tp = (double)nb * (5.2e-6 + 1.2e-8 * (double)m / s);
+  const double r1 = rate * (double)(sms - s) / sms;
+  double x = (tp - t_lt) * r1 / ops_per_col;
+  if (x < 0) x = 0;
+  if (x > (double)rest) x = (double)rest;
+  return std::min<int64_t>(rest, ((int64_t)x + 127) / 128 * 128);  // whole 128-column tiles
+}
+
 LaPlan lookahead_plan(int setting, int64_t m, int64_t nb, int npairs, int sms, int64_t rest) {
   LaPlan best{lookahead_split(setting, m, nb, npairs, sms), rest};
   if (!la_two_phase() || setting >= 0 || npairs <= 0 || rest <= 0) return best;
@@ -1667,6 +1690,16 @@ LaPlan lookahead_plan(int setting, int64_t m, int64_t nb, int npairs, int sms, i
     }
   }
   return best;
+}
+
+// SMs of the look-ahead panel that factors columns [j, j + nb) of an m-row
+// trailing matrix (m = n - j) beside the update of the step before it, whose
+// other columns number m - min(nb, m).  Every driver (the right-looking loop,
+// the upload phase, the distributed 1 x Q driver through oz_lookahead_sms)
+// sizes a given panel the same way: the panel's leaf widths depend on its SM
+// cap, so equal caps keep the factors bit-identical across the drivers.
+int panel_sms(int setting, int64_t m, int64_t nb, int npairs, int sms) {
+  return lookahead_plan(setting, m, nb, npairs, sms, m - std::min<int64_t>(nb, m)).sms;
 }
 
 // OZ_LU_TRACE=1: per-step event timeline of the driver on stderr (tuning only)
@@ -1817,9 +1850,12 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
     // tuning: SMs of the phase's side-stream panels (default: the look-ahead
     // model; 48 measured equal, 74 slower at n = 32768)
     static const int phase_sms_env = getenv("OZ_UPLOAD_SMS") ? atoi(getenv("OZ_UPLOAD_SMS")) : 0;
-    const int la_sms = phase_sms_env > 0 ? (phase_sms_env & ~1)
-                                         : lookahead_split(la_setting, n - nb, nb,
-                                                           backend != 0 ? npairs : 0, sm_count());
+    auto phase_panel_sms = [&](int64_t p0) {
+      return phase_sms_env > 0 ? (phase_sms_env & ~1)
+                               : panel_sms(la_setting, n - p0, nb, backend != 0 ? npairs : 0,
+                                           sm_count());
+    };
+    const int la_sms = phase_panel_sms(nb);  // the phase's GEMM leaves panel 1's SMs free
     int next_panel = 1;
     // wavefront over (step, block): diagonal d applies step s to block d - s,
     // so step 0 keeps up with the upload while later steps wait for their
@@ -1847,7 +1883,7 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
           OZ_CHECK_CUDA(cudaEventRecord(side->ready, st));
           OZ_CHECK_CUDA(cudaStreamWaitEvent(side->st, side->ready, 0));
           OZ_TRY(panel_factor(a + p0 * lda + p0, lda, n - p0, std::min<int64_t>(nb, n - p0), p0,
-                              ipiv + p0, info, ws.bits, ws, side->st, la_sms));
+                              ipiv + p0, info, ws.bits, ws, side->st, phase_panel_sms(p0)));
           OZ_CHECK_CUDA(cudaEventRecord(pdone[s2 + 1], side->st));
           ++next_panel;
         }
@@ -2171,10 +2207,19 @@ extern "C" int oz_lu_ws_init(void* ws, size_t ws_bytes, int64_t n, int64_t nb, i
 
 // The look-ahead SM split for a panel of m rows beside a trailing update of
 // ncols columns (the single-GPU driver's model; 0 = no look-ahead).
+extern "C" int64_t oz_lookahead_cols1(int64_t m, int64_t rest_cols, int64_t nb, int npairs,
+                                      int panel_sms) {
+  if (oz::lookahead_sms() == 0 || !oz::la_two_phase() || panel_sms <= 0) return rest_cols;
+  return oz::phase1_cols(panel_sms, m, nb, npairs, oz::sm_count(), rest_cols);
+}
+
 extern "C" int oz_lookahead_sms(int64_t m, int64_t ncols, int64_t nb, int npairs) {
   const int setting = oz::lookahead_sms();
   if (setting == 0) return 0;
-  return oz::lookahead_split(setting, m, nb, npairs, oz::sm_count(), ncols);
+  // ncols = this rank's trailing columns, the next panel's included; on one
+  // rank this is the single-GPU driver's panel_sms (bit-identical factors)
+  (void)ncols;
+  return oz::panel_sms(setting, m, nb, npairs, oz::sm_count());
 }
 
 extern "C" int oz_lu_panel(double* a, int64_t lda, int64_t m, int64_t jb, int64_t base,

@@ -208,10 +208,17 @@ class DeviceOps:
         self.side = t.cuda.Stream()   # look-ahead panel (+ its broadcast) beside the update
 
     def lookahead_sms(self, m: int, ncols: int) -> int:
-        """Look-ahead SMs for a panel of m rows beside this rank's update of
-        ncols trailing columns (the single-GPU driver's model)."""
+        """Look-ahead SMs for the panel of an m-row trailing matrix (the
+        single-GPU driver's value for the same panel: equal SM caps keep the
+        panel's factors bit-identical)."""
         return int(_lib.query("oz_lookahead_sms", m, ncols, self.nb,
                               len(self.pa) if self.emulated else 0))
+
+    def lookahead_cols1(self, m: int, rest_cols: int, sms: int) -> int:
+        """Two-phase look-ahead: how many of this rank's rest_cols columns to
+        update beside the panel on the other SMs (the rest after it, on all)."""
+        return int(_lib.query("oz_lookahead_cols1", m, rest_cols, self.nb,
+                              len(self.pa) if self.emulated else 0, sms))
 
     # -- streams
     def side_stream(self):
@@ -414,7 +421,14 @@ def factor_block_cyclic(ops, comm, n: int, nb: int, lookahead: bool = True,
                     with ops.side_stream():
                         factor_and_send(nxt, lstart, nxt % 2, Q > 1, S)
                     side_pending = True
-                    ops.schur_cols(j, jb, lstart, nt, jb2, nt, slot, S)
+                    # two-phase: the first cols1 columns beside the panel on
+                    # sms - S SMs, the rest on every SM once the panel is done
+                    c1 = jb2 + ops.lookahead_cols1(m_next, nt - jb2, S)
+                    ops.schur_cols(j, jb, lstart, nt, jb2, c1, slot, S)
+                    if c1 < nt:
+                        ops.join_side()
+                        side_pending = False
+                        ops.schur_cols(j, jb, lstart, nt, c1, nt, slot)
                 else:
                     ops.schur_cols(j, jb, lstart, nt, jb2, nt, slot)
                     factor_and_send(nxt, lstart, nxt % 2, False)

@@ -41,6 +41,10 @@ class NumpyOps:
     def lookahead_sms(self, m, ncols):
         return 16
 
+    def lookahead_cols1(self, m, rest_cols, sms):
+        # two-phase split point: exercise both phases of the driver
+        return rest_cols // 2
+
     # -- streams (the device ops run the look-ahead panel on a side stream)
     def side_stream(self):
         import contextlib
