@@ -122,10 +122,14 @@ class DeviceOps2D:
         dev = "cuda"
         self.slab = t.empty((max(self.ncl, 1), max(self.mloc, 1)), dtype=t.float64, device=dev)
         self.ld = max(self.mloc, 1)
-        self.pbuf = t.empty((max(self.mloc, 1) * nb,), dtype=t.float64, device=dev)
+        # two slots: the look-ahead panel (side stream) fills one while the
+        # current step's trsm / Schur update read the other
+        self.pbufs = [t.empty((max(self.mloc, 1) * nb,), dtype=t.float64, device=dev)
+                      for _ in range(2)]
         self.ubuf = t.empty((nb * max(self.ncl, 1),), dtype=t.float64, device=dev)
         self.rec = t.empty((REC_HDR + 2 * nb,), dtype=t.float64, device=dev)
-        self.ipiv_buf = t.empty((nb,), dtype=t.int32, device=dev)
+        self.ipiv_bufs = [t.empty((nb,), dtype=t.int32, device=dev) for _ in range(2)]
+        self.side = t.cuda.Stream()   # look-ahead panel beside the update
         self.ipiv = t.empty((n,), dtype=t.int32, device=dev)
         self.info = t.zeros((1,), dtype=t.int32, device=dev)
         self.bits = t.zeros((2,), dtype=t.int64, device=dev)   # [seen, max|A|] IEEE bits
@@ -142,6 +146,22 @@ class DeviceOps2D:
 
     def _st(self):
         return _dev.stream()
+
+    # -- look-ahead (the 1 x Q driver's: hpl.DeviceOps)
+    def lookahead_sms(self, m: int, ncols: int) -> int:
+        return int(_lib.query("oz_lookahead_sms", m, ncols, self.nb,
+                              len(self.pa) if self.code != 0 else 0))
+
+    def lookahead_cols1(self, m: int, rest_cols: int, sms: int) -> int:
+        return int(_lib.query("oz_lookahead_cols1", m, rest_cols, self.nb,
+                              len(self.pa) if self.code != 0 else 0, sms))
+
+    def side_stream(self):
+        self.side.wait_stream(self.t.cuda.current_stream())
+        return self.t.cuda.stream(self.side)
+
+    def join_side(self) -> None:
+        self.t.cuda.current_stream().wait_stream(self.side)
 
     # -- matrix
     def generate(self, kind: int, seed, depth=1, block=1, alpha=1.0) -> None:
@@ -196,7 +216,8 @@ class DeviceOps2D:
 
     def dpanel_apply(self, lc: int, lr0: int, t: int, jb: int, g: int, owns_g: bool, recs):
         _lib.call("oz_dpanel_apply", self._a(lc, 0), self.ld, lr0, self.mloc, t, jb, g,
-                  int(owns_g), self.nb, self.P, self.p, recs.data_ptr(), self.ipiv_buf.data_ptr(),
+                  int(owns_g), self.nb, self.P, self.p, recs.data_ptr(),
+                  self.ipiv_bufs[0].data_ptr(),
                   self.info.data_ptr(), self.bits.data_ptr(), self._st())
 
     # -- gathered panel (default): one all-gather per panel, then the
@@ -212,7 +233,8 @@ class DeviceOps2D:
                       self._st())
         return buf
 
-    def panel_from_gathered(self, allp, lc: int, lr_j: int, j: int, jb: int, R: int) -> None:
+    def panel_from_gathered(self, allp, lc: int, lr_j: int, j: int, jb: int, R: int,
+                            slot: int = 0, max_ctas: int = 0) -> None:
         """Assemble the global m x jb panel (rows j..n) from the P gathered
         blocks, factor it with the single-GPU panel kernels (oz_lu_panel:
         recursive leaves, partial pivoting, interchanges inside the panel),
@@ -229,16 +251,16 @@ class DeviceOps2D:
         apan = t.empty((m * jb,), dtype=t.float64, device="cuda")
         _lib.call("oz_assemble_rows", allp.data_ptr(), R, R * jb, blk_d.data_ptr(),
                   row_d.data_ptr(), m, jb, apan.data_ptr(), m, self._st())
-        _lib.call("oz_lu_panel", apan.data_ptr(), m, m, jb, j, self.ipiv_buf.data_ptr(),
+        _lib.call("oz_lu_panel", apan.data_ptr(), m, m, jb, j, self.ipiv_bufs[slot].data_ptr(),
                   self.info.data_ptr(), self.bits.data_ptr(), self.ws.data_ptr(), self.wsb,
-                  self.n, self.nb, self.planes, 0, self._st())
+                  self.n, self.nb, self.planes, max_ctas, self._st())
         mine = self.mloc - lr_j
         if mine > 0:
             back = self._rows_dev(global_rows(n, nb, P, self.p)[lr_j:] - j)
             _lib.call("oz_assemble_rows", apan.data_ptr(), m, 0, None, back.data_ptr(), mine,
                       jb, self._a(lc, lr_j), self.ld, self._st())
 
-    def panel_finish(self, lc: int, lr_j: int, jb: int, diag: bool) -> None:
+    def panel_finish(self, lc: int, lr_j: int, jb: int, diag: bool, slot: int = 0) -> None:
         """Growth over the finalized U rows of the diagonal block; pack the
         local panel rows lr_j.. into the broadcast buffer (F-order)."""
         if diag:
@@ -246,15 +268,15 @@ class DeviceOps2D:
                       self.bits.data_ptr(), self._st())
         m = self.mloc - lr_j
         if m > 0:
-            _lib.call("oz_copy2d", self._a(lc, lr_j), m, jb, 1, self.ld, self.pbuf.data_ptr(), 1,
-                      m, self._st())
+            _lib.call("oz_copy2d", self._a(lc, lr_j), m, jb, 1, self.ld,
+                      self.pbufs[slot].data_ptr(), 1, m, self._st())
 
-    def panel_buffers(self, lr_j: int, jb: int):
-        return self.pbuf[:(self.mloc - lr_j) * jb], self.ipiv_buf[:jb]
+    def panel_buffers(self, lr_j: int, jb: int, slot: int = 0):
+        return self.pbufs[slot][:(self.mloc - lr_j) * jb], self.ipiv_bufs[slot][:jb]
 
-    def record_pivots(self, j: int, jb: int) -> np.ndarray:
-        self.ipiv[j:j + jb].copy_(self.ipiv_buf[:jb])
-        return self.ipiv_buf[:jb].cpu().numpy()
+    def record_pivots(self, j: int, jb: int, slot: int = 0) -> np.ndarray:
+        self.ipiv[j:j + jb].copy_(self.ipiv_bufs[slot][:jb])
+        return self.ipiv_bufs[slot][:jb].cpu().numpy()
 
     def _cols(self, ranges):
         (c0a, c1a), (c0b, c1b) = ranges
@@ -283,12 +305,13 @@ class DeviceOps2D:
         _lib.call("oz_scatter_rows", self.slab.data_ptr(), self.ld, rows.data_ptr(), len(lrows),
                   c0a, c1a, c0b, c1b, buf.data_ptr(), brow.data_ptr(), ldb, self._st())
 
-    def trsm(self, lr_j: int, jb: int, lstart: int, nt: int):
+    def trsm(self, lr_j: int, jb: int, lstart: int, nt: int, slot: int = 0):
         """U12 <- L11^-1 A12 in place (block row of this process row), copied
         into the U12 broadcast buffer."""
         m = self.mloc - lr_j
         u12 = self._a(lstart, lr_j)
-        _lib.call("oz_trsm_lunit", self.pbuf.data_ptr(), m, jb, u12, self.ld, nt, self._st())
+        _lib.call("oz_trsm_lunit", self.pbufs[slot].data_ptr(), m, jb, u12, self.ld, nt,
+                  self._st())
         _lib.call("oz_max_abs_bits", u12, jb, nt, 1, self.ld, 0, self.bits.data_ptr(),
                   self._st())
         _lib.call("oz_copy2d", u12, jb, nt, 1, self.ld, self.ubuf.data_ptr(), 1, jb, self._st())
@@ -296,21 +319,28 @@ class DeviceOps2D:
     def ubuf_view(self, jb: int, nt: int):
         return self.ubuf[:jb * nt]
 
-    def schur(self, lr_j: int, jb: int, skip: int, lstart: int, nt: int) -> None:
-        """A22 (local rows lr_j+skip.., columns lstart..) -= L21 U12."""
+    def schur(self, lr_j: int, jb: int, skip: int, lstart: int, nt: int, slot: int = 0,
+              c0: int = 0, c1: int | None = None, reserve_sms: int = 0) -> None:
+        """A22 (local rows lr_j+skip.., columns lstart+c0 .. lstart+c1) -= L21 U12.
+        The split of L21 and of all of U12 happens with the first column range
+        (c0 == 0); later ranges reuse it (per-vector exponents: the product of
+        an element does not depend on the column partition)."""
+        c1 = nt if c1 is None else c1
         mrem = self.mloc - lr_j
         mr = mrem - skip
-        if mr <= 0 or nt <= 0:
+        if mr <= 0 or nt <= 0 or c1 <= c0:
             return
-        l21 = self.pbuf.data_ptr() + 8 * skip
+        l21 = self.pbufs[slot].data_ptr() + 8 * skip
         u12 = self.ubuf.data_ptr()
         a22 = self._a(lstart, lr_j + skip)
-        _lib.call("oz_schur_split", self.code, mr, nt, jb, l21, mrem, u12, jb, self.k, self.qbits,
-                  self.ws.data_ptr(), self.wsb, self.n, self.nb, self._st())
+        if c0 == 0:
+            _lib.call("oz_schur_split", self.code, mr, nt, jb, l21, mrem, u12, jb, self.k,
+                      self.qbits, self.ws.data_ptr(), self.wsb, self.n, self.nb, self._st())
+        max_ctas = self.sms - reserve_sms if reserve_sms > 0 else 0
         _lib.call("oz_schur_cols", self.code, mr, nt, jb, l21, mrem, u12, jb, a22, self.ld,
                   self.k, self.qbits, len(self.pa), self.pa.ctypes.data, self.pb.ctypes.data,
-                  self.ps.ctypes.data, self.bits.data_ptr(), 0, nt, 0, self.ws.data_ptr(),
-                  self.wsb, self.n, self.nb, self._st())
+                  self.ps.ctypes.data, self.bits.data_ptr(), c0, c1, max_ctas,
+                  self.ws.data_ptr(), self.wsb, self.n, self.nb, self._st())
 
     def finish(self):
         b = self.bits.cpu().numpy().view(np.float64)
@@ -347,7 +377,8 @@ def panel_mode() -> str:
     return m
 
 
-def factor_2d(ops, grid: Grid, n: int, nb: int, mode: str | None = None):
+def factor_2d(ops, grid: Grid, n: int, nb: int, mode: str | None = None,
+              lookahead: bool = True):
     """Blocked right-looking LU (solve.py:94-140) on the P x Q grid.
     Returns (ipiv int32[n] global LAPACK-style, growth).
 
@@ -359,23 +390,49 @@ def factor_2d(ops, grid: Grid, n: int, nb: int, mode: str | None = None):
       round trip per panel instead of jb, and the blocked panel instead of
       the level-2 column loop;
     * 'column': one all-gather of small candidate records per panel column,
-      the reference's unblocked loop (solve.py:75-90) distributed."""
+      the reference's unblocked loop (solve.py:75-90) distributed.
+
+    Look-ahead (gather mode, depth 1, as hpl.py's 1 x Q driver): the process
+    column owning panel b+1 updates that panel's columns first, then gathers
+    and factors it on a side stream capped to S SMs (the single-GPU panel_sms
+    of the panel's height, so its factors do not depend on the grid), while
+    the compute stream updates the rest of its columns: the first cols1 on
+    sms - S SMs, the remainder on every SM once the panel is done.  Panel
+    buffers alternate between two slots so the look-ahead panel never
+    overwrites the L21 the current step is still reading."""
     P, Q, p, q = grid.P, grid.Q, grid.p, grid.q
     ncl = ops.ncl
     nblk = -(-n // nb)
     mode = mode or panel_mode()
+    lookahead = lookahead and mode == "gather"
     ops.begin()
+    early = set()                                 # panels factored on the side stream
+    side_pending = False
+
+    def factor_gathered(jblk, slot, max_ctas):
+        j = jblk * nb
+        jb = min(nb, n - j)
+        lc = (jblk // Q) * nb
+        lr_j = local_cols_before(j, nb, P, p)
+        R = max(local_ncols(n, nb, P, o) - local_cols_before(j, nb, P, o) for o in range(P))
+        allp = grid.col.allgather(ops.panel_pack(lc, lr_j, jb, R))
+        ops.panel_from_gathered(allp, lc, lr_j, j, jb, R, slot, max_ctas)
+        ops.panel_finish(lc, lr_j, jb, p == jblk % P, slot)
+
     for jblk in range(nblk):
         j = jblk * nb
         jb = min(nb, n - j)
         pr, pc = jblk % P, jblk % Q
         lc = (jblk // Q) * nb
         lr_j = local_cols_before(j, nb, P, p)
-        if q == pc and mode == "gather":              # panel: one exchange
-            R = max(local_ncols(n, nb, P, o) - local_cols_before(j, nb, P, o) for o in range(P))
-            allp = grid.col.allgather(ops.panel_pack(lc, lr_j, jb, R))
-            ops.panel_from_gathered(allp, lc, lr_j, j, jb, R)
-            ops.panel_finish(lc, lr_j, jb, p == pr)
+        slot = jblk % 2 if mode == "gather" else 0
+        if q == pc and mode == "gather":
+            if jblk in early:                         # factored during the previous step
+                if side_pending:
+                    ops.join_side()
+                    side_pending = False
+            else:
+                factor_gathered(jblk, slot, 0)
         elif q == pc:                                 # panel, one column at a time
             for t in range(jb):
                 g = j + t
@@ -385,10 +442,10 @@ def factor_2d(ops, grid: Grid, n: int, nb: int, mode: str | None = None):
                 recs = grid.col.allgather(rec)
                 ops.dpanel_apply(lc, lr0, t, jb, g, owns_g, recs)
             ops.panel_finish(lc, lr_j, jb, p == pr)
-        pbuf, ipiv = ops.panel_buffers(lr_j, jb)
+        pbuf, ipiv = ops.panel_buffers(lr_j, jb, slot)
         grid.row.bcast(pbuf, pc)                      # L of the panel, local rows
         grid.row.bcast(ipiv, pc)
-        piv = ops.record_pivots(j, jb)
+        piv = ops.record_pivots(j, jb, slot)
         # interchanges on every column outside the panel
         ranges = ((0, lc), (lc + jb, ncl)) if q == pc else ((0, ncl), (ncl, ncl))
         dst, src = compose_interchanges(piv, j)
@@ -418,9 +475,31 @@ def factor_2d(ops, grid: Grid, n: int, nb: int, mode: str | None = None):
         nt = ncl - lstart
         if j + jb < n and nt > 0:
             if p == pr:
-                ops.trsm(lr_j, jb, lstart, nt)
+                ops.trsm(lr_j, jb, lstart, nt, slot)
             grid.col.bcast(ops.ubuf_view(jb, nt), pr)
-            ops.schur(lr_j, jb, jb if p == pr else 0, lstart, nt)
+            skip = jb if p == pr else 0
+            nxt = jblk + 1
+            m_next = n - nxt * nb
+            jb2 = min(nb, m_next) if nxt < nblk else 0
+            S = 0
+            if lookahead and nxt < nblk and nxt % Q == q and m_next > jb2:
+                S = ops.lookahead_sms(m_next, nt)
+            if S > 0:
+                ops.schur(lr_j, jb, skip, lstart, nt, slot, 0, jb2)   # the next panel's columns
+                with ops.side_stream():
+                    factor_gathered(nxt, nxt % 2, S)
+                early.add(nxt)
+                side_pending = True
+                c1 = jb2 + ops.lookahead_cols1(m_next, nt - jb2, S)
+                ops.schur(lr_j, jb, skip, lstart, nt, slot, jb2, c1, S)
+                if c1 < nt:
+                    ops.join_side()
+                    side_pending = False
+                    ops.schur(lr_j, jb, skip, lstart, nt, slot, c1, nt)
+            else:
+                ops.schur(lr_j, jb, skip, lstart, nt, slot)
+    if side_pending:
+        ops.join_side()
     ipiv, info, seen, top = ops.finish()
     info, seen, top = grid.world.allreduce_values([info, seen, top], "max")
     info = int(info)

@@ -161,14 +161,29 @@ class NumpyOps2D:
         self.gcols = global_rows(self.n, nb, Q, q)
         self.mloc, self.ncl = len(self.grows), len(self.gcols)
         self.slab = np.asfortranarray(a_full[np.ix_(self.grows, self.gcols)])
-        self.pbuf = torch.zeros(max(self.mloc, 1) * nb, dtype=torch.float64)
+        self.pbufs = [torch.zeros(max(self.mloc, 1) * nb, dtype=torch.float64)
+                      for _ in range(2)]
         self.ubuf = torch.zeros(nb * max(self.ncl, 1), dtype=torch.float64)
-        self.ipiv_buf = torch.zeros(nb, dtype=torch.int32)
+        self.ipiv_bufs = [torch.zeros(nb, dtype=torch.int32) for _ in range(2)]
         self.ipiv = np.zeros(self.n, dtype=np.int32)
         self.flag = 0
 
     def generate(self, *args, **kw):
         self.slab = np.asfortranarray(self.full[np.ix_(self.grows, self.gcols)])
+
+    # -- look-ahead (hpl2d.factor_2d): sizes only matter on the device
+    def lookahead_sms(self, m, ncols):
+        return 16
+
+    def lookahead_cols1(self, m, rest_cols, sms):
+        return rest_cols // 2            # exercise both phases
+
+    def side_stream(self):
+        import contextlib
+        return contextlib.nullcontext()
+
+    def join_side(self):
+        pass
 
     def vector(self, host=None, n=None):
         if host is None:
@@ -210,7 +225,7 @@ class NumpyOps2D:
         rw = r[w]
         rg = r[int(np.nonzero(r[:, 2])[0][0])]
         piv = int(rw[1])
-        self.ipiv_buf[t] = piv
+        self.ipiv_bufs[0][t] = piv
         if rw[3 + t] == 0.0 and not self.info:
             self.info = g + 1
         a = self.slab
@@ -235,7 +250,7 @@ class NumpyOps2D:
             buf[:, :mine] = self.slab[lr_j:, lc:lc + jb].T
         return torch.from_numpy(buf.ravel().copy())
 
-    def panel_from_gathered(self, allp, lc, lr_j, j, jb, R):
+    def panel_from_gathered(self, allp, lc, lr_j, j, jb, R, slot=0, max_ctas=0):
         """The gathered panel factored by the reference's unblocked loop
         (solve.py:75-90) on the global m x jb panel; own rows written back."""
         from paper_2509_23565_b200.hpl import local_cols_before
@@ -249,7 +264,7 @@ class NumpyOps2D:
         m = n - j
         for t in range(jb):
             pr = t + int(np.argmax(np.abs(pan[t:, t])))
-            self.ipiv_buf[t] = j + pr
+            self.ipiv_bufs[slot][t] = j + pr
             if pan[pr, t] == 0.0:
                 if not self.info:
                     self.info = j + t + 1
@@ -265,20 +280,20 @@ class NumpyOps2D:
         if mine > 0:
             self.slab[lr_j:, lc:lc + jb] = pan[self.grows[lr_j:] - j, :]
 
-    def panel_finish(self, lc, lr_j, jb, diag):
+    def panel_finish(self, lc, lr_j, jb, diag, slot=0):
         if diag:
             self.seen = max(self.seen, float(np.abs(np.triu(
                 self.slab[lr_j:lr_j + jb, lc:lc + jb])).max()))
         m = self.mloc - lr_j
         if m > 0:
-            self.pbuf[:m * jb] = torch.from_numpy(
+            self.pbufs[slot][:m * jb] = torch.from_numpy(
                 self.slab[lr_j:, lc:lc + jb].ravel(order="F").copy())
 
-    def panel_buffers(self, lr_j, jb):
-        return self.pbuf[:(self.mloc - lr_j) * jb], self.ipiv_buf[:jb]
+    def panel_buffers(self, lr_j, jb, slot=0):
+        return self.pbufs[slot][:(self.mloc - lr_j) * jb], self.ipiv_bufs[slot][:jb]
 
-    def record_pivots(self, j, jb):
-        self.ipiv[j:j + jb] = self.ipiv_buf[:jb].numpy()
+    def record_pivots(self, j, jb, slot=0):
+        self.ipiv[j:j + jb] = self.ipiv_bufs[slot][:jb].numpy()
         return self.ipiv[j:j + jb].copy()
 
     @staticmethod
@@ -299,12 +314,12 @@ class NumpyOps2D:
         b = buf.numpy().reshape((len(cols), ldb)).T
         self.slab[np.ix_(np.asarray(lrows), cols)] = b[np.asarray(brows), :]
 
-    def _pan(self, lr_j, jb):
+    def _pan(self, lr_j, jb, slot=0):
         m = self.mloc - lr_j
-        return self.pbuf[:m * jb].numpy().reshape((jb, m)).T
+        return self.pbufs[slot][:m * jb].numpy().reshape((jb, m)).T
 
-    def trsm(self, lr_j, jb, lstart, nt):
-        pan = self._pan(lr_j, jb)
+    def trsm(self, lr_j, jb, lstart, nt, slot=0):
+        pan = self._pan(lr_j, jb, slot)
         u12 = solve_triangular(pan[:jb, :jb], self.slab[lr_j:lr_j + jb, lstart:lstart + nt],
                                lower=True, unit_diagonal=True, check_finite=False)
         self.slab[lr_j:lr_j + jb, lstart:lstart + nt] = u12
@@ -314,13 +329,14 @@ class NumpyOps2D:
     def ubuf_view(self, jb, nt):
         return self.ubuf[:jb * nt]
 
-    def schur(self, lr_j, jb, skip, lstart, nt):
+    def schur(self, lr_j, jb, skip, lstart, nt, slot=0, c0=0, c1=None, reserve_sms=0):
+        c1 = nt if c1 is None else c1
         mr = self.mloc - lr_j - skip
-        if mr <= 0 or nt <= 0:
+        if mr <= 0 or nt <= 0 or c1 <= c0:
             return
-        l21 = self._pan(lr_j, jb)[skip:, :]
-        u12 = self.ubuf[:jb * nt].numpy().reshape((nt, jb)).T
-        cols = slice(lstart, lstart + nt)
+        l21 = self._pan(lr_j, jb, slot)[skip:, :]
+        u12 = self.ubuf[:jb * nt].numpy().reshape((nt, jb)).T[:, c0:c1]
+        cols = slice(lstart + c0, lstart + c1)
         rows = slice(lr_j + skip, self.mloc)
         self.slab[rows, cols] = orc.gemm(-1.0, l21, u12, 1.0, self.slab[rows, cols], k=self.k)
         self.seen = max(self.seen, float(np.abs(self.slab[rows, cols]).max()))

@@ -136,9 +136,10 @@ np.savez(out, lu=a.cpu().numpy(), ipiv=ipiv.cpu().numpy())
 def test_pxq_gathered_panel_equals_single_gpu_lu(tmp_path):
     """The gathered-panel 2-D driver (one all-gather per panel, the whole
     panel factored by the single-GPU recursive kernels on every rank of the
-    column) reproduces the single-GPU LU bit for bit when that one factors
-    every panel on all SMs (no look-ahead): the distribution changes nothing
-    in the arithmetic (nb = 128: two 64-column leaves and a DGEMM per panel)."""
+    column, the next panel on a side stream) reproduces the single-GPU LU bit
+    for bit: both drivers give each panel the same look-ahead SM cap (a
+    function of its height only), so the distribution changes nothing in the
+    arithmetic (nb = 128: two 64-column leaves and a DGEMM per panel)."""
     import subprocess
     import sys
     n, nb, k = 640, 128, 7
@@ -146,7 +147,7 @@ def test_pxq_gathered_panel_equals_single_gpu_lu(tmp_path):
     script = tmp_path / "single.py"
     script.write_text(_SINGLE)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PYTHONPATH=root, OZ_LOOKAHEAD_SMS="0")
+    env = dict(os.environ, PYTHONPATH=root)
     r = subprocess.run([sys.executable, str(script), str(n), str(nb), str(k),
                         str(tmp_path / "s.npz")], env=env, capture_output=True, text=True,
                        timeout=300)

@@ -37,7 +37,7 @@ def test_compose_interchanges_matches_sequential_swaps():
         assert np.array_equal(moved, rows)
 
 
-def _worker(rank, world, P, Q, port, n, nb, k, seed, out, mode="gather"):
+def _worker(rank, world, P, Q, port, n, nb, k, seed, out, mode="gather", lookahead=True):
     import torch.distributed as dist
 
     from hpl_numpy_ops import NumpyOps2D
@@ -52,7 +52,7 @@ def _worker(rank, world, P, Q, port, n, nb, k, seed, out, mode="gather"):
         grid = hpl2d.Grid(P, Q, hpl.Comm())
         ops = NumpyOps2D(a, nb, P, Q, grid.p, grid.q, k)
         b = hpl2d.rhs_2d(ops, grid).numpy().copy()
-        ipiv, growth = hpl2d.factor_2d(ops, grid, n, nb, mode=mode)
+        ipiv, growth = hpl2d.factor_2d(ops, grid, n, nb, mode=mode, lookahead=lookahead)
         factored = ops.slab.copy()
         x = hpl2d.solve_2d(ops, grid, n, nb, ipiv_to_perm(ipiv), b)
         out.put((rank, factored, ops.grows, ops.gcols, ipiv, growth, x.numpy().copy(), b))
@@ -60,13 +60,14 @@ def _worker(rank, world, P, Q, port, n, nb, k, seed, out, mode="gather"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["gather", "column"])
+@pytest.mark.parametrize("mode,lookahead", [("gather", True), ("column", False)])
 @pytest.mark.parametrize("n,nb,P,Q,k", [(96, 16, 2, 1, 7), (100, 16, 2, 2, 7), (70, 8, 3, 1, 3),
-                                        (90, 12, 2, 2, None)])
-def test_pxq_lu_matches_oracle(n, nb, P, Q, k, mode):
+                                        (90, 12, 2, 2, None), (130, 16, 2, 3, 7)])
+def test_pxq_lu_matches_oracle(n, nb, P, Q, k, mode, lookahead):
     """Both panel modes (one all-gather per panel + the whole panel factored
-    on every rank of the column; or one exchange per panel column) give the
-    oracle's factors, pivots and growth bit for bit."""
+    on every rank of the column, with the side-stream look-ahead of the next
+    panel and the two-phase trailing update; or one exchange per panel
+    column) give the oracle's factors, pivots and growth bit for bit."""
     from oracle import ozaki_oracle as orc
     from paper_2509_23565_b200.solve import ipiv_to_perm
     here = os.path.dirname(os.path.abspath(__file__))
@@ -77,7 +78,8 @@ def test_pxq_lu_matches_oracle(n, nb, P, Q, k, mode):
     ctx = mp.get_context("spawn")
     out = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, P, Q, port, n, nb, k, 5, out, mode))
+    procs = [ctx.Process(target=_worker,
+                         args=(r, world, P, Q, port, n, nb, k, 5, out, mode, lookahead))
              for r in range(world)]
     for p in procs:
         p.start()
