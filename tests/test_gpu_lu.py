@@ -207,11 +207,13 @@ np.savez(out, lu=a.cpu().numpy(), ipiv=ipiv.cpu().numpy(), info=int(info.item())
 
 @pytest.mark.parametrize("n,nb,k", [(3000, 512, 7), (2304, 1024, 0)])
 def test_panel_exchange_variants(n, nb, k, tmp_path):
-    """The panel leaf's two exchange variants (grid-wide records + counter,
-    cluster DSMEM + cluster barrier) compute the same arithmetic: factors,
-    pivots and growth are bit-identical.  Without look-ahead the trsm of the
-    next panel's columns runs in the wide-trsm kernel (different FP64
-    summation order): same pivots, factors equal to rounding."""
+    """The panel leaf's three variants (shared-memory slab with grid-wide
+    records + counter, shared-memory slab with cluster DSMEM + cluster
+    barrier, register-resident rows with the cluster push exchange) compute
+    the same arithmetic: factors, pivots and growth are bit-identical.
+    Without look-ahead the trsm of the next panel's columns runs in the
+    wide-trsm kernel (different FP64 summation order): same pivots, factors
+    equal to rounding."""
     import os
     import subprocess
     import sys
@@ -219,18 +221,20 @@ def test_panel_exchange_variants(n, nb, k, tmp_path):
     script.write_text(_VARIANT_SCRIPT)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = []
-    for i, env_extra in enumerate(({"OZ_PANEL_CLUSTER": "0"}, {"OZ_PANEL_CLUSTER": "16"},
-                                   {"OZ_LOOKAHEAD_SMS": "0"})):
+    for i, env_extra in enumerate(({"OZ_PANEL_LEAF": "0", "OZ_PANEL_CLUSTER": "0"},
+                                   {"OZ_PANEL_LEAF": "0", "OZ_PANEL_CLUSTER": "16"},
+                                   {"OZ_LOOKAHEAD_SMS": "0"}, {})):
         env = dict(os.environ, PYTHONPATH=root, **env_extra)
         out = tmp_path / f"r{i}.npz"
         r = subprocess.run([sys.executable, str(script), str(n), str(nb), str(k), str(out)],
                            env=env, capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stderr[-2000:]
         res.append(np.load(out))
-    grid, cluster, nola = res
-    assert np.array_equal(grid["lu"], cluster["lu"])
-    assert np.array_equal(grid["ipiv"], cluster["ipiv"])
-    assert float(grid["growth"]) == float(cluster["growth"])
+    grid, cluster, nola, reg = res
+    for other in (cluster, reg):
+        assert np.array_equal(grid["lu"], other["lu"])
+        assert np.array_equal(grid["ipiv"], other["ipiv"])
+        assert float(grid["growth"]) == float(other["growth"])
     assert np.array_equal(grid["ipiv"], nola["ipiv"])
     np.testing.assert_allclose(nola["lu"], grid["lu"], rtol=0,
                                atol=1e-9 * np.abs(grid["lu"]).max())
