@@ -24,6 +24,7 @@
 // (native comparator) or the Ozaki-INT8 tcgen05 GEMM (gemm_emu.cu).
 #include <stdlib.h>
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -129,18 +130,21 @@ struct PanelArgs {
   int32_t* list_src;  // the window columns): new_row[dst] = old_row[src]
   int32_t* list_cnt;
   unsigned long long* dbg;  // optional per-phase cycle counters (OZ_PANEL_TIMING)
+  unsigned epoch;           // grid variant: record tags of this launch are epoch + t + 1
 };
 
-__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_release_u64(long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 // candidate record: [0] |v| (double), [1] pos (low 32) | tag (high 32), [2] physical
-// row, [4..4+w) row values.  Data first, tag last (release store).
+// row, [4..4+w) row values.  Grid variant: data first, then the tag word by
+// one release store; readers poll the tag word itself with acquire loads (no
+// separate arrival counter: one round trip less per column).
 
 constexpr int STAGE_G = 16;  // grids up to this size read every record in one round trip
 
@@ -267,15 +271,18 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
           rec[4 + c] = v;
         }
       }
+      const unsigned posw = br >= 0 ? (unsigned)pos[br] : 0x7fffffffu;
       if (lane == 0) {
         rec[0] = br >= 0 ? fabs(sm[t * R + br]) : -1.0;
-        irec[1] = br >= 0 ? pos[br] : 0x7fffffff;
+        if (kCluster) irec[1] = posw;
         irec[2] = br >= 0 ? row_lo + br : -1;
       }
-      // the warp's record stores are ordered before lane 0's release-add by
-      // the warp barrier (one release instead of a GPU-scope fence per lane)
+      // the warp's record stores are ordered before lane 0's release store of
+      // the tag word by the warp barrier (one release instead of a GPU-scope
+      // fence per lane)
       __syncwarp();
-      if (!kCluster && lane == 0) red_release_add(&p.bar->count, 1u);
+      if (!kCluster && lane == 0)
+        st_release_u64(&irec[1], ((unsigned long long)(p.epoch + (unsigned)t + 1u) << 32) | posw);
       if (p.dbg && lane == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 0, (unsigned long long)(_n - _tp)); _tp = _n; }
     }
     __syncthreads();  // the publish above read row br before the deferred update below
@@ -314,19 +321,21 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
       }
     }
     if (p.dbg && tid == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 4, (unsigned long long)(_n - _tp)); _tp = _n; }
-    // ---- wait for all CTAs (counter reaches G*(t+1) / the cluster barrier)
+    // ---- wait for all CTAs: the cluster barrier, or (grid) every record's
+    //      tag word of this step, polled by warp 0 (lane l: CTAs l, l+32, ..)
+    const unsigned tag = p.epoch + (unsigned)t + 1u;
+    const double* recs = p.cand + (size_t)buf * gridDim.x * CAND_STRIDE;
     if (kCluster) {
       cluster_wait_acquire();
-    } else {
-      if (tid == 0) {
-        const unsigned target = gridDim.x * (unsigned)(t + 1);
-        while (ld_acquire_u32(&p.bar->count) < target) {
+    } else if (staged) {
+      if (wid == 0 && lane < (int)gridDim.x) {
+        const long long* tw = reinterpret_cast<const long long*>(recs + (size_t)lane * CAND_STRIDE) + 1;
+        while ((unsigned)(ld_acquire_u64(tw) >> 32) != tag) {
         }
       }
       __syncthreads();
     }
     if (p.dbg && tid == 0) { const long long _n = clock64(); atomicAdd(p.dbg + 1, (unsigned long long)(_n - _tp)); _tp = _n; }
-    const double* recs = p.cand + (size_t)buf * gridDim.x * CAND_STRIDE;
     if (staged) {
       // small grids: the whole record array in one round trip, all threads
       constexpr int LOADS = (STAGE_G * CAND_STRIDE + PANEL_THREADS - 1) / PANEL_THREADS;
@@ -367,10 +376,18 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
         for (int i = 0; i < PER; ++i) {
           const int g = lane + 32 * i;
           const double* cr_ = recs + (size_t)g * CAND_STRIDE;
+          unsigned long long w = 0x7fffffffull;
+          if (g < (int)gridDim.x) {
+            const long long* tw = reinterpret_cast<const long long*>(cr_) + 1;
+            do {
+              w = ld_acquire_u64(tw);
+            } while ((unsigned)(w >> 32) != tag);
+          }
+          pk[i] = (long long)(w & 0xffffffffull);
           av[i] = g < (int)gridDim.x ? __ldcg(cr_) : -2.0;
-          pk[i] = g < (int)gridDim.x ? __ldcg(reinterpret_cast<const long long*>(cr_) + 1)
-                                     : 0x7fffffffll;
         }
+        // every lane's acquire precedes the warp's reads of the winner's row
+        __syncwarp();
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
           if (lane + 32 * i >= (int)gridDim.x) continue;
@@ -388,7 +405,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_window_kernel(PanelArg
       for (int c = t + lane; c < w; c += 32) urow[c] = staged ? win[4 + c] : __ldcg(win + 4 + c);
       if (lane == 0) {
         const int ppos = staged ? (int)reinterpret_cast<const long long*>(win)[1]
-                                : (int)__ldcg(reinterpret_cast<const long long*>(win) + 1);
+                                : (int)(unsigned)__ldcg(reinterpret_cast<const long long*>(win) + 1);
         const int64_t prow = staged ? reinterpret_cast<const long long*>(win)[2]
                                     : __ldcg(reinterpret_cast<const long long*>(win) + 2);
         const double pv = staged ? win[4 + t] : __ldcg(win + 4 + t);
@@ -1185,6 +1202,14 @@ bool cluster_fits(int G, size_t smem) {
   return ok;
 }
 
+// Record tags of the grid-exchange leaves: epoch + t + 1 (t < 128), unique per
+// launch for 2^25 launches, so a record left in the candidate buffer by an
+// earlier launch never matches the current step.
+unsigned next_record_epoch() {
+  static std::atomic<unsigned> seq{1};
+  return (seq.fetch_add(1u) & 0x1ffffffu) << 7;
+}
+
 // Register-resident leaf (panel_leaf.cuh) for short panels: OZ_PANEL_LEAF=0
 // disables it (tuning / A-B).  Variant = W*10 + RPT: rows per CTA 256*RPT,
 // at most LEAF_MAXG CTAs in the cluster, W*RPT <= 64 doubles per thread.
@@ -1209,9 +1234,21 @@ int leaf_max_rpt() {
   }();
   return v;
 }
+// OZ_PANEL_LEAF_GRID=0 keeps taller panels on the shared-memory grid leaf
+// (tuning A/B): otherwise the register leaf with the global-memory exchange
+// takes panels whose rows fit 256 (W = 64) or 512 (W = 32) per CTA on the
+// SMs the caller may use.
+bool leaf_grid_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("OZ_PANEL_LEAF_GRID");
+    return e == nullptr || atoi(e) != 0;
+  }();
+  return v;
+}
 int leaf_variant(int64_t m, int w, int max_ctas) {
   if (!leaf_enabled() || m < 1) return 0;
   const int rpt = leaf_max_rpt();
+  const int cap = max_ctas > 0 && max_ctas < sm_count() ? max_ctas : sm_count();
   int v = 0, rows = 0;
   if (w <= 64 && m <= (int64_t)LEAF_MAXG * 128) {
     v = 6411;  // 128 threads x 1 row
@@ -1227,32 +1264,49 @@ int leaf_variant(int64_t m, int w, int max_ctas) {
     rows = 1024;
   }
   // the cluster must fit in the SMs the caller may use (look-ahead side stream)
-  if (v != 0 && max_ctas > 0 && ceil_div(m, (int64_t)rows) > max_ctas) return 0;
-  return v;
+  if (v != 0 && ceil_div(m, (int64_t)rows) <= cap) return v;
+  if (!leaf_grid_enabled()) return 0;
+  // taller: one co-resident grid, records exchanged through global memory
+  if (w <= 64 && ceil_div(m, (int64_t)256) <= cap) return 64120;
+  if (w <= 32 && ceil_div(m, (int64_t)512) <= cap) return 32220;
+  return 0;
 }
-// widest leaf the register variant takes at this height (0: none)
+// widest leaf the register variants take at this height (0: none)
 int leaf_width_for(int64_t m, int max_ctas) {
   const int rpt = leaf_max_rpt();
   if (!leaf_enabled()) return 0;
-  if (m <= (int64_t)LEAF_MAXG * 256)
-    return ceil_div(m, (int64_t)(m <= (int64_t)LEAF_MAXG * 128 ? 128 : 256)) <= max_ctas ? 64 : 0;
-  if (rpt >= 2 && m <= (int64_t)LEAF_MAXG * 512) return ceil_div(m, (int64_t)512) <= max_ctas ? 32 : 0;
-  if (rpt >= 4 && m <= (int64_t)LEAF_MAXG * 1024) return ceil_div(m, (int64_t)1024) <= max_ctas ? 16 : 0;
+  const int cap = max_ctas > 0 && max_ctas < sm_count() ? max_ctas : sm_count();
+  if (m <= (int64_t)LEAF_MAXG * 256 &&
+      ceil_div(m, (int64_t)(m <= (int64_t)LEAF_MAXG * 128 ? 128 : 256)) <= cap)
+    return 64;
+  if (rpt >= 2 && m <= (int64_t)LEAF_MAXG * 512 && ceil_div(m, (int64_t)512) <= cap) return 32;
+  if (leaf_grid_enabled()) {
+    if (ceil_div(m, (int64_t)256) <= cap) return 64;
+    if (ceil_div(m, (int64_t)512) <= cap) return 32;
+  }
+  if (rpt >= 4 && m <= (int64_t)LEAF_MAXG * 1024 && ceil_div(m, (int64_t)1024) <= cap) return 16;
   return 0;
 }
 
-template <int W, int RPT, int NT>
-int panel_leaf_launch(const PanelArgs& pa, cudaStream_t st) {
+template <int W, int RPT, int NT, bool kGrid = false>
+int panel_leaf_launch(PanelArgs pa, cudaStream_t st) {
   constexpr size_t smem = leaf_smem_bytes<W, RPT, NT>();
   OZ_ONCE([] {
-    cudaError_t e = cudaFuncSetAttribute(panel_leaf_kernel<W, RPT, NT>,
+    cudaError_t e = cudaFuncSetAttribute(panel_leaf_kernel<W, RPT, NT, kGrid>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(panel_leaf_kernel<W, RPT, NT>,
+    if (e == cudaSuccess && !kGrid)
+      e = cudaFuncSetAttribute(panel_leaf_kernel<W, RPT, NT, kGrid>,
                                cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     return e;
   }());
   const int G = (int)ceil_div(pa.m, (int64_t)NT * RPT);
+  if constexpr (kGrid) {
+    pa.epoch = next_record_epoch();
+    void* args[] = {&pa};
+    OZ_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)panel_leaf_kernel<W, RPT, NT, kGrid>,
+                                              dim3(G), dim3(NT), args, smem, st));
+    return OZ_OK;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(G);
   cfg.blockDim = dim3(NT);
@@ -1265,7 +1319,7 @@ int panel_leaf_launch(const PanelArgs& pa, cudaStream_t st) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  OZ_CHECK_CUDA(cudaLaunchKernelEx(&cfg, panel_leaf_kernel<W, RPT, NT>, pa));
+  OZ_CHECK_CUDA(cudaLaunchKernelEx(&cfg, panel_leaf_kernel<W, RPT, NT, kGrid>, pa));
   return OZ_OK;
 }
 
@@ -1289,6 +1343,7 @@ int panel_leaf(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t bas
   pa.list_src = ws.swap_src;
   pa.list_cnt = ws.swap_cnt;
   pa.dbg = panel_dbg();
+  pa.epoch = 0;
   OZ_CHECK_CUDA(cudaMemsetAsync(ws.swap_cnt, 0, sizeof(int32_t), st));
   const int tag = prof_start(st);
   count_launch();
@@ -1299,6 +1354,8 @@ int panel_leaf(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t bas
     case 3212: s = panel_leaf_launch<32, 1, 256>(pa, st); break;
     case 3222: s = panel_leaf_launch<32, 2, 256>(pa, st); break;
     case 1642: s = panel_leaf_launch<16, 4, 256>(pa, st); break;
+    case 64120: s = panel_leaf_launch<64, 1, 256, true>(pa, st); break;
+    case 32220: s = panel_leaf_launch<32, 2, 256, true>(pa, st); break;
     default: s = OZ_UNSUPPORTED;
   }
   prof_stop(tag, st, PROF_PANEL, (double)m * w);
@@ -1377,6 +1434,7 @@ int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t b
   pa.list_src = ws.swap_src;
   pa.list_cnt = ws.swap_cnt;
   pa.dbg = panel_dbg();
+  pa.epoch = next_record_epoch();
   OZ_CHECK_CUDA(cudaMemsetAsync(ws.swap_cnt, 0, sizeof(int32_t), st));
   const int tag = prof_start(st);
   count_launch();
@@ -1395,7 +1453,6 @@ int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t b
     cfg.numAttrs = 1;
     OZ_CHECK_CUDA(cudaLaunchKernelEx(&cfg, panel_window_kernel<true>, pa));
   } else {
-    OZ_CHECK_CUDA(cudaMemsetAsync(ws.bar, 0, sizeof(GridBar), st));
     void* args[] = {&pa};
     OZ_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)panel_window_kernel<false>, dim3(G),
                                               dim3(PANEL_THREADS), args,

@@ -29,9 +29,11 @@
 
 constexpr int LEAF_MAXG = 16;
 
-template <int W, int NT>
+template <int W, int NT, bool kGrid>
 struct LeafShared {
-  double rec[3][LEAF_MAXG][4 + W];  // received records: [0] |v|, [1] pos, [2] row, [4..) values
+  // received records: [0] |v|, [1] pos, [2] row, [4..) values.  Cluster
+  // variant: every CTA's; grid variant: the winner's, copied from global
+  double rec[3][kGrid ? 1 : LEAF_MAXG][4 + W];
   double mine[3][4 + W];            // this CTA's record (source of the bulk copies)
   double raw[W];                    // the owner row's registers, before step t-1's update
   unsigned long long bar[3];
@@ -90,13 +92,20 @@ __device__ __forceinline__ void leaf_push(uint32_t dst, uint32_t src, uint32_t b
     _tp = _n;                                                          \
   }
 
-template <int W, int RPT, int NT>
+// kGrid = false: the G <= 16 CTAs form one cluster and push records through
+// DSMEM (above).  kGrid = true: G co-resident CTAs (cooperative launch, G up
+// to the SM count) publish records to global memory (triple-buffered slots of
+// p.cand), each with a tag word written last by a release store; warp 0 of
+// every CTA polls the G tags with acquire loads, reduces, and copies the
+// winner's record to shared memory.  Same arithmetic, same bits.
+template <int W, int RPT, int NT, bool kGrid>
 __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(PanelArgs p) {
   constexpr int R = NT * RPT;
+  static_assert(4 + W <= CAND_STRIDE, "grid record must fit a candidate slot");
   extern __shared__ double lbuf[];  // [W][R]: L (and, for pivot rows, U) values by window row
-  __shared__ LeafShared<W, NT> sh;
+  __shared__ LeafShared<W, NT, kGrid> sh;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int G = (int)gridDim.x;  // one cluster of G CTAs
+  const int G = (int)gridDim.x;  // CTAs of the window (one cluster unless kGrid)
   const int g = (int)blockIdx.x;
   const int w = p.w;
   const int64_t m = p.m;
@@ -117,13 +126,15 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(PanelArgs p) {
     }
   }
   if (tid < W) sh.occ[tid] = tid;
-  if (tid == 0) {
+  if (!kGrid && tid == 0) {
     for (int b = 0; b < 3; ++b) leaf_mbar_init(smem_u32(&sh.bar[b]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if constexpr (!kGrid) {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
 
   // candidate for column 0
   double ca = -1.0;
@@ -151,7 +162,8 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(PanelArgs p) {
     // full records every step: columns >= w are zero in every row and stay
     // zero (0 - l*0), so the update below needs no per-column predicates
     constexpr uint32_t bytes = (uint32_t)((4 + W) * 8);
-    if (tid == 0) leaf_mbar_expect(smem_u32(&sh.bar[b]), (uint32_t)G * bytes);
+    const unsigned tag = p.epoch + (unsigned)t + 1u;  // kGrid record tag of this step
+    if (!kGrid && tid == 0) leaf_mbar_expect(smem_u32(&sh.bar[b]), (uint32_t)G * bytes);
     // ---- CTA argmax of the thread candidates (np.argmax order)
     warp_argmax(ca, cp, cr);
     if (lane == 0) {
@@ -209,14 +221,27 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(PanelArgs p) {
           rec[4 + c] = v;
         }
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      // one bulk copy per destination CTA, issued by lane d (a single thread
-      // issuing G copies serialises them, ~150 cycles each)
-      if (lane < G) {
-        const uint32_t dst = leaf_mapa(smem_u32(&sh.rec[b][g][0]), (uint32_t)lane);
-        const uint32_t mb = leaf_mapa(smem_u32(&sh.bar[b]), (uint32_t)lane);
-        leaf_push(dst, smem_u32(rec), bytes, mb);
+      if constexpr (kGrid) {
+        // the record to this CTA's global slot; the tag word last (release)
+        __syncwarp();
+        double* gs = p.cand + ((size_t)b * G + g) * CAND_STRIDE;
+        for (int c = lane; c < 4 + W; c += 32)
+          if (c != 1) gs[c] = rec[c];
+        __syncwarp();
+        if (lane == 0)
+          st_release_u64(reinterpret_cast<long long*>(gs) + 1,
+                         ((unsigned long long)tag << 32) |
+                             (unsigned)reinterpret_cast<const long long*>(rec)[1]);
+      } else {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        // one bulk copy per destination CTA, issued by lane d (a single thread
+        // issuing G copies serialises them, ~150 cycles each)
+        if (lane < G) {
+          const uint32_t dst = leaf_mapa(smem_u32(&sh.rec[b][g][0]), (uint32_t)lane);
+          const uint32_t mb = leaf_mapa(smem_u32(&sh.bar[b]), (uint32_t)lane);
+          leaf_push(dst, smem_u32(rec), bytes, mb);
+        }
       }
       if (p.dbg != nullptr && g == 0 && lane == ol) _own += (unsigned long long)(clock64() - _o);
     }
@@ -240,15 +265,53 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(PanelArgs p) {
     }
     LEAF_MARK(3)
     // ---- every CTA's record of step t has arrived
-    leaf_mbar_wait(smem_u32(&sh.bar[b]), (uint32_t)((t / 3) & 1));
+    double ra;
+    int rp, rg;
+    if constexpr (kGrid) {
+      if (wid == 0) {
+        // lane l polls CTAs l, l+32, ... (tag word, acquire), then the warp
+        // reduces and copies the winner's record into shared memory
+        const double* slots = p.cand + (size_t)b * G * CAND_STRIDE;
+        double a1 = -2.0;
+        int p1 = 0x7fffffff, g1 = -1;
+        for (int gg = lane; gg < G; gg += 32) {
+          const long long* tw = reinterpret_cast<const long long*>(slots + (size_t)gg * CAND_STRIDE) + 1;
+          unsigned long long wv;
+          do {
+            wv = ld_acquire_u64(tw);
+          } while ((unsigned)(wv >> 32) != tag);
+          const double av = __ldcg(slots + (size_t)gg * CAND_STRIDE);
+          const int pv = (int)(unsigned)(wv & 0xffffffffull);
+          if (better(av, pv, a1, p1)) {
+            a1 = av;
+            p1 = pv;
+            g1 = gg;
+          }
+        }
+        warp_argmax(a1, p1, g1);
+        __syncwarp();  // every lane's acquire precedes the reads of the winner
+        const double* win = slots + (size_t)g1 * CAND_STRIDE;
+        for (int c = lane; c < 4 + W; c += 32) sh.rec[b][0][c] = c == 1 ? 0.0 : __ldcg(win + c);
+        if (lane == 0) {
+          reinterpret_cast<long long*>(sh.rec[b][0])[1] = p1;
+        }
+      }
+      __syncthreads();
+      ra = sh.rec[b][0][0];
+      rp = (int)reinterpret_cast<const long long*>(sh.rec[b][0])[1];
+      rg = 0;
+    } else {
+      leaf_mbar_wait(smem_u32(&sh.bar[b]), (uint32_t)((t / 3) & 1));
+      const double(*recs)[4 + W] = sh.rec[b];
+      ra = lane < G ? recs[lane][0] : -2.0;
+      rp = lane < G ? (int)reinterpret_cast<const long long*>(recs[lane])[1] : 0x7fffffff;
+      rg = lane < G ? lane : -1;
+      warp_argmax(ra, rp, rg);
+    }
     LEAF_MARK(4)
-    const double(*recs)[4 + W] = sh.rec[b];
-    double ra = lane < G ? recs[lane][0] : -2.0;
-    int rp = lane < G ? (int)reinterpret_cast<const long long*>(recs[lane])[1] : 0x7fffffff;
-    int rg = lane < G ? lane : -1;
-    warp_argmax(ra, rp, rg);
-    const double* urow = recs[rg] + 4;  // winner row: urow[c] = column t + c
-    const int prow = (int)reinterpret_cast<const long long*>(recs[rg])[2];
+    (void)ra;
+    const double* urow = sh.rec[b][rg] + 4;  // winner row: urow[c] = column t + c
+    const int prow = (int)reinterpret_cast<const long long*>(sh.rec[b][rg])[2];
     const double piv = urow[0];
     const int rt = sh.occ[t];  // physical row at logical position t
     if (g == 0 && tid == 0) {
@@ -319,7 +382,9 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(PanelArgs p) {
     const double gm = warp_max(__longlong_as_double((long long)gmax));
     if (lane == 0 && gm > 0.0) atomic_max_abs(p.growth, gm);
   }
-  // no CTA exits while its last record may still be copied out of its smem
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if constexpr (!kGrid) {
+    // no CTA exits while its last record may still be copied out of its smem
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
 }

@@ -66,6 +66,10 @@ for m in ms:
         if dbg[7] > 0:  # OZ_PANEL_TIMING=1 with the register leaf: cycles per column step
             names = ["argmax", "reduce", "push", "deferred", "wait", "tail", "owner_push"]
             phases = {nm: round(float(dbg[i]) / float(dbg[7]), 1) for i, nm in enumerate(names)}
+        elif dbg[:6].sum() > 0:  # shared-memory leaf: cycles summed over CTAs and columns
+            names = ["publish", "wait", "reduce", "urow", "deferred", "update"]
+            phases = {nm + "_Mcyc_all_ctas": round(float(dbg[i]) / reps / 1e6, 2)
+                      for i, nm in enumerate(names)}
         rec = {"m": m, "jb": jb, "S": S, "ms": round(t, 3), "us_per_col": round(t * 1e3 / jb, 2),
                "leaf_cycles_per_step": phases,
                "pivots_same_as_first_S": same, "info": int(info.item()), "kinds": kinds}

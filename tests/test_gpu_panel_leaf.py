@@ -4,9 +4,10 @@ order, ties to the first row), factors and the zero-pivot report bit for bit.
 
 Small-integer entries make ties between candidate rows frequent, which is
 where a distributed argmax can go wrong.  Heights cover every leaf variant:
-register leaf with 128-row CTAs (m <= 2048), 256-row CTAs (m <= 4096), two
-rows per thread (m <= 8192, 32-column windows), and the shared-memory grid
-leaf beyond."""
+register leaf with one cluster of 128-row CTAs (m <= 2048), 256-row CTAs
+(m <= 4096), two rows per thread (m <= 8192, 32-column windows), and the
+register leaf with the global-memory exchange beyond (256 rows per CTA up to
+the SM count, then 512 with 32-column windows)."""
 
 import numpy as np
 import pytest
@@ -54,7 +55,8 @@ def _device_panel(a):
 
 
 @pytest.mark.parametrize("m,jb", [(70, 64), (300, 64), (2048, 64), (2049, 64), (4096, 64),
-                                  (5000, 32), (8192, 32), (12000, 16)])
+                                  (5000, 32), (8192, 32), (12000, 16), (12000, 64),
+                                  (40000, 32)])
 def test_leaf_ties_match_reference(m, jb):
     rng = np.random.default_rng(m)
     a = rng.integers(-4, 5, size=(m, jb)).astype(np.float64)
