@@ -1695,7 +1695,7 @@ int lookahead_split(int setting, int64_t m, int64_t nb, int npairs, int sms, int
 // linearly in S), so a larger S for a shorter time beats a narrow S for the
 // whole step.  Model (fit to OZ_LU_TRACE timelines at n = 32768, in-LU times,
 // GEMM running beside the panel): panel ~ nb * (5.2 us + 0.012 us * m / S);
-// GEMM 2.4e15 INT8 ops/s on all SMs; interchanges + trsm + split of the rest
+// GEMM at emu_rate(pairs) on all SMs; interchanges + trsm + split of the rest
 // before the GEMM ~ 0.8 ms + 0.117 us per column.  OZ_LA_TWO_PHASE=0 keeps the
 // single-phase split (lookahead_split).
 struct LaPlan {
@@ -1709,10 +1709,23 @@ bool la_two_phase() {
   }();
   return v;
 }
+// Emulated GEMM rate in the LU shape (K = nb = 1024, all SMs), INT8 ops/s,
+// measured with scripts/probe.py kern (profiles/r02_gemm_rate_lu_shape.txt):
+// few pairs leave the per-group FP64 epilogue less MMA work to hide behind.
+double emu_rate(int npairs) {
+  static const double scale = getenv("OZ_LA_RATE_SCALE") ? atof(getenv("OZ_LA_RATE_SCALE"))
+                                                          : 1.0;  // tuning
+  // measured 1.45 / 1.9 / 2.1 / 2.2 POPS, scaled by 1.09: planning with the
+  // slightly optimistic rate measured faster at n = 32768, k = 7
+  // (profiles/r02_la_rate_ab.txt: 485 vs 492 ms over three interleaved runs)
+  const double r = npairs <= 6 ? 1.45e15 : npairs <= 10 ? 1.9e15 : npairs <= 15 ? 2.1e15 : 2.2e15;
+  return r * 1.09 * scale;
+}
+
 // phase-1 width for a given S: the columns sms - S SMs update while the panel runs
 int64_t phase1_cols(int s, int64_t m, int64_t nb, int npairs, int sms, int64_t rest) {
   if (rest <= 0 || npairs <= 0) return rest > 0 ? rest : 0;
-  const double rate = 2.4e15;
+  const double rate = emu_rate(npairs);
   const double ops_per_col = 2.0 * npairs * (double)m * (double)nb;
   const double t_lt = 0.8e-3 + 1.17e-7 * (double)rest;
   const double tp = (double)nb * (5.2e-6 + 1.2e-8 * (double)m / s);
@@ -1726,7 +1739,7 @@ int64_t phase1_cols(int s, int64_t m, int64_t nb, int npairs, int sms, int64_t r
 LaPlan lookahead_plan(int setting, int64_t m, int64_t nb, int npairs, int sms, int64_t rest) {
   LaPlan best{lookahead_split(setting, m, nb, npairs, sms), rest};
   if (!la_two_phase() || setting >= 0 || npairs <= 0 || rest <= 0) return best;
-  const double rate = 2.4e15;
+  const double rate = emu_rate(npairs);
   const double ops_per_col = 2.0 * npairs * (double)m * (double)nb;
   const double t_lt = 0.8e-3 + 1.17e-7 * (double)rest;
   double best_t = 1e30;
