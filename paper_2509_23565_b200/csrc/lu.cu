@@ -829,6 +829,28 @@ constexpr size_t trsmf_smem(int jb) {
 }
 
 // --------------------------------------------------------------- reductions
+// max |a| over a contiguous block of `count` doubles (16-byte aligned):
+// 128-bit loads, four in flight per thread, no index arithmetic per element
+__global__ void max_abs_flat_kernel(const double2* __restrict__ a, int64_t count2,
+                                    unsigned long long* out) {
+  double mx[4] = {0.0, 0.0, 0.0, 0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < count2; i += 4 * stride) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldcs(a + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) mx[u] = fmax(mx[u], fmax(fabs(v[u].x), fabs(v[u].y)));
+  }
+  for (; i < count2; i += stride) {
+    const double2 v = __ldcs(a + i);
+    mx[0] = fmax(mx[0], fmax(fabs(v.x), fabs(v.y)));
+  }
+  double m = warp_max(fmax(fmax(mx[0], mx[1]), fmax(mx[2], mx[3])));
+  if ((threadIdx.x & 31) == 0 && m > 0.0) atomic_max_abs(out, m);
+}
+
 __global__ void max_abs_kernel(const double* __restrict__ a, int64_t m, int64_t n, int64_t rs,
                                int64_t cs, int upper_only, int64_t diag_off,
                                unsigned long long* out) {
@@ -976,6 +998,20 @@ __global__ void gather_kernel(const double* __restrict__ b, const int64_t* __res
   if (i < n) x[i] = b[perm[i]];
 }
 
+__global__ void copy_flat_kernel(const double2* __restrict__ src, double2* __restrict__ dst,
+                                 int64_t count2) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < count2; i += 4 * stride) {  // four 16-byte loads in flight
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldcs(src + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) __stcs(dst + i + u * stride, v[u]);
+  }
+  for (; i < count2; i += stride) __stcs(dst + i, __ldcs(src + i));
+}
+
 __global__ void copy2d_kernel(const double* __restrict__ src, int64_t rows, int64_t cols,
                               int64_t srs, int64_t scs, double* __restrict__ dst, int64_t drs,
                               int64_t dcs) {
@@ -1061,6 +1097,17 @@ size_t lu_ws_layout(int64_t n, int64_t nb, int k, uint8_t* base, LuWs* ws) {
 int max_abs(const double* a, int64_t m, int64_t n, int64_t rs, int64_t cs, int upper,
             int64_t diag_off, unsigned long long* out, cudaStream_t st) {
   if (m <= 0 || n <= 0) return OZ_OK;
+  const int64_t count = m * n;
+  if (!upper && rs == 1 && (cs == m || n == 1) && count % 2 == 0 &&
+      (reinterpret_cast<uintptr_t>(a) & 15) == 0 && count >= (1 << 20)) {
+    // one contiguous block (the LU's working copy, lda = n): flat 128-bit scan
+    int64_t blocks = ceil_div(count / 2, 256);
+    if (blocks > sm_count() * 8) blocks = sm_count() * 8;
+    max_abs_flat_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const double2*>(a),
+                                                            count / 2, out);
+    OZ_CHECK_LAUNCH();
+    return OZ_OK;
+  }
   int64_t blocks = ceil_div(m * n, 256);
   if (blocks > sm_count() * 8) blocks = sm_count() * 8;
   max_abs_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, m, n, rs, cs, upper, diag_off, out);
@@ -2243,6 +2290,20 @@ extern "C" int oz_copy2d(const double* src, int64_t rows, int64_t cols, int64_t 
                          void* stream) {
   using namespace oz;
   if (rows <= 0 || cols <= 0) return OZ_OK;
+  const int64_t count = rows * cols;
+  const bool same_dense = (src_rs == 1 && dst_rs == 1 && src_cs == rows && dst_cs == rows) ||
+                          (src_cs == 1 && dst_cs == 1 && src_rs == cols && dst_rs == cols);
+  if (same_dense && count % 2 == 0 && ((reinterpret_cast<uintptr_t>(src) |
+                                        reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    // one dense block in the same layout (the LU's working copy): a flat
+    // 128-bit copy, four loads in flight, instead of the transposing tiles
+    int64_t blocks = ceil_div(count / 2, 256);
+    if (blocks > sm_count() * 8) blocks = sm_count() * 8;
+    copy_flat_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
+        reinterpret_cast<const double2*>(src), reinterpret_cast<double2*>(dst), count / 2);
+    OZ_CHECK_LAUNCH();
+    return OZ_OK;
+  }
   dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32));
   copy2d_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(src, rows, cols, src_rs, src_cs, dst,
                                                             dst_rs, dst_cs);
