@@ -30,16 +30,19 @@
 constexpr int LEAF_MAXG = 16;
 
 template <int W, int NT, bool kGrid>
-struct LeafShared {
+struct alignas(128) LeafShared {  // bulk-copy sources/destinations need 16-byte alignment
   // received records: [0] |v|, [1] pos, [2] row, [4..) values.  Cluster
   // variant: every CTA's; grid variant: the winner's, copied from global
   double rec[3][kGrid ? 1 : LEAF_MAXG][4 + W];
   double mine[3][4 + W];            // this CTA's record (source of the bulk copies)
   double raw[W];                    // the owner row's registers, before step t-1's update
   unsigned long long bar[3];
-  double wa[NT / 32];  // per-warp candidate |v|, position, row
-  int wp[NT / 32];
-  int wr[NT / 32];
+  // per-warp candidate |v|, position, row; two buffers by step parity: a warp
+  // may write step t+1's candidate while another still reads step t's (the
+  // cluster variant has no CTA barrier between those points)
+  double wa[2][NT / 32];
+  int wp[2][NT / 32];
+  int wr[2][NT / 32];
   int occ[W];  // physical window row at logical position c (< W)
 };
 
@@ -166,16 +169,17 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(PanelArgs p) {
     if (!kGrid && tid == 0) leaf_mbar_expect(smem_u32(&sh.bar[b]), (uint32_t)G * bytes);
     // ---- CTA argmax of the thread candidates (np.argmax order)
     warp_argmax(ca, cp, cr);
+    const int wb = t & 1;
     if (lane == 0) {
-      sh.wa[wid] = ca;
-      sh.wp[wid] = cp;
-      sh.wr[wid] = cr;
+      sh.wa[wb][wid] = ca;
+      sh.wp[wb][wid] = cp;
+      sh.wr[wb][wid] = cr;
     }
     __syncthreads();
     LEAF_MARK(0)
-    double ba = lane < NT / 32 ? sh.wa[lane] : -2.0;
-    int bp = lane < NT / 32 ? sh.wp[lane] : 0x7fffffff;
-    int br = lane < NT / 32 ? sh.wr[lane] : -1;
+    double ba = lane < NT / 32 ? sh.wa[wb][lane] : -2.0;
+    int bp = lane < NT / 32 ? sh.wp[wb][lane] : 0x7fffffff;
+    int br = lane < NT / 32 ? sh.wr[wb][lane] : -1;
     warp_argmax(ba, bp, br);  // every warp computes the same winner
     const bool none = br < 0;
     const int owner = none ? 0 : (br % NT);
@@ -291,10 +295,9 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(PanelArgs p) {
         warp_argmax(a1, p1, g1);
         __syncwarp();  // every lane's acquire precedes the reads of the winner
         const double* win = slots + (size_t)g1 * CAND_STRIDE;
-        for (int c = lane; c < 4 + W; c += 32) sh.rec[b][0][c] = c == 1 ? 0.0 : __ldcg(win + c);
-        if (lane == 0) {
-          reinterpret_cast<long long*>(sh.rec[b][0])[1] = p1;
-        }
+        for (int c = lane; c < 4 + W; c += 32)
+          if (c != 1) sh.rec[b][0][c] = __ldcg(win + c);
+        if (lane == 0) reinterpret_cast<long long*>(sh.rec[b][0])[1] = p1;
       }
       __syncthreads();
       ra = sh.rec[b][0][0];

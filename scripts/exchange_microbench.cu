@@ -8,6 +8,7 @@
 //     winner row read through DSMEM.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o exch scripts/exchange_microbench.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -202,7 +203,7 @@ float run(int G, int steps) {
 }
 
 int main() {
-  const int steps = 20000;
+  const int steps = getenv("EXCH_STEPS") ? atoi(getenv("EXCH_STEPS")) : 20000;
   for (int G : {2, 4, 8, 16}) {
     printf("G=%2d  barrier+DSMEM reads %.3f us  bulk push of records %.3f us  "
            "st.async headers + DSMEM row %.3f us  st.async records %.3f us  no exchange %.3f us\n",
