@@ -1549,6 +1549,34 @@ int laswp_ipiv(double* a, int64_t lda, int64_t c0a, int64_t c1a, int64_t c0b, in
   return OZ_OK;
 }
 
+// laswp_ipiv in two parts: compose the gather list once, then apply it to
+// column ranges (possibly on two streams at once; the list stays valid until
+// the next compose, which the caller orders after every apply).
+int compose_list(int64_t k1, const int32_t* ipiv, int npiv, const LuWs& ws, cudaStream_t st) {
+  OZ_REQUIRE(npiv >= 0 && npiv <= COMPOSE_MAX, OZ_INVALID_PARAMS, "bad interchange count");
+  if (npiv == 0) return OZ_OK;
+  compose_ipiv_kernel<<<1, 256, 0, st>>>(ipiv, npiv, k1, ws.cdst, ws.csrc, ws.ccnt);
+  OZ_CHECK_LAUNCH();
+  return OZ_OK;
+}
+int apply_composed(double* a, int64_t lda, int64_t c0a, int64_t c1a, int64_t c0b, int64_t c1b,
+                   int npiv, const LuWs& ws, cudaStream_t st, int max_ctas = 0) {
+  const int64_t ncols = (c1a - c0a) + (c1b - c0b);
+  if (npiv == 0 || ncols <= 0) return OZ_OK;
+  struct Stop {
+    int tag;
+    cudaStream_t st;
+    ~Stop() { prof_stop(tag, st, PROF_LASWP, 0.0); }
+  } stop{prof_start(st), st};
+  int64_t blocks = ceil_div(ncols, LSWR_WARPS);
+  if (blocks > sm_count()) blocks = sm_count();
+  if (max_ctas > 0 && blocks > max_ctas) blocks = max_ctas;
+  laswp_list_reg_kernel<<<(unsigned)blocks, LSWR_WARPS * 32, 0, st>>>(
+      a, lda, ws.cdst, ws.csrc, ws.ccnt, c0a, c1a, c0b, c1b);
+  OZ_CHECK_LAUNCH();
+  return OZ_OK;
+}
+
 // Factor one m x jb column panel in place (solve.py:66-91 for columns
 // j..j+jb of the global matrix): `a` points at the panel's diagonal corner,
 // rows keep the global numbering through `base` (= j).  Interchanges are
@@ -1844,6 +1872,8 @@ struct LuTrace {
 struct SideStream {
   cudaStream_t st = nullptr;
   cudaEvent_t ready = nullptr, done = nullptr;
+  cudaStream_t aux = nullptr;  // early steps: the rest's row interchanges
+  cudaEvent_t aux_ready = nullptr, aux_done = nullptr;
 };
 int side_stream(SideStream** out) {
   static thread_local std::vector<SideStream> per_dev;
@@ -1859,6 +1889,9 @@ int side_stream(SideStream** out) {
                                                pr && atoi(pr) ? hi : lo));
     OZ_CHECK_CUDA(cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming));
     OZ_CHECK_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+    OZ_CHECK_CUDA(cudaStreamCreateWithPriority(&s.aux, cudaStreamNonBlocking, lo));
+    OZ_CHECK_CUDA(cudaEventCreateWithFlags(&s.aux_ready, cudaEventDisableTiming));
+    OZ_CHECK_CUDA(cudaEventCreateWithFlags(&s.aux_done, cudaEventDisableTiming));
   }
   *out = &s;
   return OZ_OK;
@@ -2043,10 +2076,32 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
     // columns, trsm, split and update of the remaining columns) runs beside it.
     // GLOBAL scaling needs all of U12 for its one exponent: no column split.
     const bool la = side != nullptr && rest > jb2 && backend != 2;
+    // Early (GEMM-bound) steps: the interchanges of every column but the next
+    // panel's run on an aux stream with aux_ctas CTAs beside the serial chain
+    // (the next panel's columns: interchanges, trsm, split, update on
+    // sms - aux_ctas SMs).  Row swaps are DRAM-latency-bound, so a few CTAs
+    // keep most of their throughput.  OZ_AUX_SWAPS_CTAS=0 disables.
+    // Measured at n = 32768, k = 7 (profiles/r02_aux_swaps_ab.txt, three
+    // interleaved runs each): off 488.7 ms, 16 CTAs 486.5, 24 481.8, 32 481.5,
+    // 48 486.7; 32 CTAs from m >= 8192 480.6.
+    static const int aux_ctas = getenv("OZ_AUX_SWAPS_CTAS") ? atoi(getenv("OZ_AUX_SWAPS_CTAS"))
+                                                           : 32;
+    static const int64_t aux_min_m = getenv("OZ_AUX_SWAPS_MIN_M")
+                                         ? atoll(getenv("OZ_AUX_SWAPS_MIN_M"))
+                                         : 8192;
+    const bool aux = la && ready_cols >= n && aux_ctas > 0 && jb <= COMPOSE_MAX &&
+                     rest >= aux_min_m && side->aux != nullptr;
     tr.mark(st);  // 0 step start
     // ---- the panel's interchanges: whole-row swaps (solve.py:80-82)
     if (!la) OZ_TRY(wait_cols());
-    if (la)
+    if (aux) {
+      OZ_TRY(compose_list(j, ipiv + j, (int)jb, ws, st));
+      OZ_CHECK_CUDA(cudaEventRecord(side->aux_ready, st));
+      OZ_CHECK_CUDA(cudaStreamWaitEvent(side->aux, side->aux_ready, 0));
+      OZ_TRY(apply_composed(a, lda, 0, j, j + jb + jb2, n, (int)jb, ws, side->aux, aux_ctas));
+      OZ_CHECK_CUDA(cudaEventRecord(side->aux_done, side->aux));
+      OZ_TRY(apply_composed(a, lda, j + jb, j + jb + jb2, 0, 0, (int)jb, ws, st));
+    } else if (la)
       OZ_TRY(laswp_ipiv(a, lda, j + jb, j + jb + jb2, 0, 0, j, ipiv + j, (int)jb, ws, st));
     else
       OZ_TRY(laswp_ipiv(a, lda, 0, j, j + jb, n, j, ipiv + j, (int)jb, ws, st));
@@ -2057,7 +2112,7 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
       tr.mark(st);  // 2 after trsm
       OZ_TRY(schur_split_part(sc, true, 0, la ? jb2 : rest, ws, st));
       tr.mark(st);  // 3 after split
-      OZ_TRY(schur_cols(sc, 0, jb2, ws, st));
+      OZ_TRY(schur_cols(sc, 0, jb2, ws, st, aux ? sm_count() - aux_ctas : 0));
       tr.mark(st);  // 4 after the update of the next panel's columns
       double* p2 = a + (j + jb) * lda + (j + jb);
       if (la) {
@@ -2090,7 +2145,10 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
           tr.mark_sub(st);
           tr.mark_sub(st);
         } else {
-          OZ_TRY(laswp_ipiv(a, lda, 0, j, j + jb + jb2, n, j, ipiv + j, (int)jb, ws, st));
+          if (aux)
+            OZ_CHECK_CUDA(cudaStreamWaitEvent(st, side->aux_done, 0));
+          else
+            OZ_TRY(laswp_ipiv(a, lda, 0, j, j + jb + jb2, n, j, ipiv + j, (int)jb, ws, st));
           tr.mark_sub(st);
           OZ_TRY(trsm_blocked(a, lda, j, jb, a12 + jb2 * lda, lda, rest - jb2, st));
           tr.mark_sub(st);
