@@ -1179,6 +1179,13 @@ int trsm_blocked(double* a, int64_t lda, int64_t j, int64_t jb, double* b, int64
   // panel): one launch, latency-bound (~0.3 ms at jb = 1024 vs ~0.5 ms for the
   // 2*jb/64 launches below); wide updates: diagonal blocks + cuBLAS DGEMM,
   // FP64-throughput-bound (15 vs 5 TFLOP/s at 30720 columns)
+  static const bool narrow_cublas = getenv("OZ_TRSM_NARROW_CUBLAS") != nullptr;  // tuning A/B
+  if (narrow_cublas && ncols <= 2048) {
+    const int tag = prof_start(st);
+    const int s = dtrsm_lunit(jb, ncols, a + j * lda + j, lda, b, ldb, st, max_ctas);
+    prof_stop(tag, st, PROF_TRSM, (double)jb * jb * ncols);
+    return s;
+  }
   if (!legacy && jb <= TRSMF_MAXJB && ncols <= 2048) {
     const int tag = prof_start(st);
     const int s = trsm_fused<8>(a + j * lda + j, lda, jb, b, ldb, ncols, st, max_ctas);
