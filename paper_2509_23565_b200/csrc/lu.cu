@@ -728,18 +728,83 @@ constexpr int TRSMF_THREADS = 256;
 constexpr int TRSMF_MAXJB = 1024;
 constexpr int TRSMF_RPT = (TRSMF_MAXJB - 64 + TRSMF_THREADS - 1) / TRSMF_THREADS;  // rows/thread
 constexpr int TRSMF_KB = 16;  // L columns per load batch
+// Diagonal block at (r0, r0) of L into shared memory, column-major [64][64],
+// asynchronously (cp.async, 8-byte elements: no alignment assumption on L);
+// entries outside the matrix are zeroed (never read by the solve, which uses
+// the strictly lower part of valid rows only)
+__device__ __forceinline__ void trsmf_fetch_diag(const double* __restrict__ L, int64_t ldl, int jb,
+                                                 int r0, double* dst, int tid) {
+#pragma unroll 4
+  for (int i = tid; i < TRSM_W * TRSM_W; i += TRSMF_THREADS) {
+    const int c = i / TRSM_W, r = i - c * TRSM_W;
+    if (r0 + r < jb && r0 + c < jb) {
+      const double* src = L + (int64_t)(r0 + c) * ldl + r0 + r;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst + i)), "l"(src)
+                   : "memory");
+    } else {
+      dst[i] = 0.0;
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// Rows r0 + w .. jb - 1 of the CTA's block: b_r -= L[r, r0:r0+w] x[r0:r0+w]
+// in k order, NQ rows per thread (each thread issues the L loads of all its
+// rows per batch of TRSMF_KB columns: one L2 round trip per batch)
+template <int NQ, int NC>
+__device__ __forceinline__ void trsmf_rows_below(const double* __restrict__ L, int64_t ldl,
+                                                 int jb, int r0, int w, double* sB, int tid) {
+  double b[NQ][NC];
+  int rr[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    rr[q] = r0 + w + tid + q * TRSMF_THREADS;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) b[q][c] = rr[q] < jb ? sB[rr[q] * NC + c] : 0.0;
+  }
+  constexpr int KB = NQ <= 2 ? TRSM_W / NQ : TRSMF_KB;  // L loads in flight per thread: 64
+  for (int k0 = 0; k0 < w; k0 += KB) {
+    double l[NQ][KB];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int u = 0; u < KB; ++u)
+        l[q][u] = (rr[q] < jb && k0 + u < w) ? __ldg(L + (int64_t)(r0 + k0 + u) * ldl + rr[q])
+                                             : 0.0;
+#pragma unroll
+    for (int u = 0; u < KB; ++u) {
+      if (k0 + u < w) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const double x = sB[(r0 + k0 + u) * NC + c];
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) b[q][c] = fma(-l[q][u], x, b[q][c]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+    if (rr[q] < jb)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) sB[rr[q] * NC + c] = b[q][c];
+}
+
 template <int NC>
 __global__ void __launch_bounds__(TRSMF_THREADS) trsm_fused_kernel(
     const double* __restrict__ L, int64_t ldl, int jb, double* __restrict__ B, int64_t ldb,
     int64_t ncols) {
   extern __shared__ double dsm[];
   double* sB = dsm;                          // [jb][NC]
-  double* sD = dsm + (size_t)jb * NC;        // [64][65] diagonal block, row-major
+  // diagonal blocks, column-major [64][64], double-buffered: block b+1 is
+  // fetched (cp.async) while block b's rows below are updated
+  double* sDb = dsm + (size_t)jb * NC;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   // grid-stride over column groups: a capped grid (look-ahead side stream)
   // walks every group
   for (int64_t c0 = (int64_t)blockIdx.x * NC; c0 < ncols; c0 += (int64_t)gridDim.x * NC) {
   const int nc = (int)(ncols - c0 < NC ? ncols - c0 : NC);
+  trsmf_fetch_diag(L, ldl, jb, 0, sDb, tid);
   // loads batched (unrolled) so each thread keeps several L2/HBM requests in flight
 #pragma unroll 8
   for (int i = tid; i < jb * NC; i += TRSMF_THREADS) {
@@ -748,70 +813,54 @@ __global__ void __launch_bounds__(TRSMF_THREADS) trsm_fused_kernel(
   }
   for (int r0 = 0; r0 < jb; r0 += TRSM_W) {
     const int w = jb - r0 < TRSM_W ? jb - r0 : TRSM_W;
-    constexpr int DL = TRSM_W * TRSM_W / TRSMF_THREADS;
-    double dv[DL];
-#pragma unroll
-    for (int u = 0; u < DL; ++u) {
-      const int i = tid + u * TRSMF_THREADS;
-      const int c = i / TRSM_W, r = i - c * TRSM_W;
-      dv[u] = (r < w && c < w && r > c) ? L[(r0 + c) * ldl + r0 + r] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < DL; ++u) {
-      const int i = tid + u * TRSMF_THREADS;
-      const int c = i / TRSM_W, r = i - c * TRSM_W;
-      sD[r * (TRSM_W + 1) + c] = dv[u];
-    }
+    const double* sD = sDb + ((r0 / TRSM_W) & 1) * TRSM_W * TRSM_W;
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     for (int c = wid; c < NC; c += TRSMF_THREADS / 32) {
       double v0 = lane < w ? sB[(r0 + lane) * NC + c] : 0.0;
       double v1 = lane + 32 < w ? sB[(r0 + lane + 32) * NC + c] : 0.0;
-      for (int k = 0; k < w; ++k) {
-        const double xk = __shfl_sync(0xffffffffu, k < 32 ? v0 : v1, k & 31);
-        if (lane > k) v0 = fma(-sD[lane * (TRSM_W + 1) + k], xk, v0);
-        if (lane + 32 > k) v1 = fma(-sD[(lane + 32) * (TRSM_W + 1) + k], xk, v1);
+      if (w == TRSM_W) {
+        // full block: static indices, the L loads leave the dependency chain
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const double xk = __shfl_sync(0xffffffffu, v0, k);
+          if (lane > k) v0 = fma(-sD[k * TRSM_W + lane], xk, v0);
+          v1 = fma(-sD[k * TRSM_W + lane + 32], xk, v1);
+        }
+#pragma unroll
+        for (int k = 32; k < TRSM_W; ++k) {
+          const double xk = __shfl_sync(0xffffffffu, v1, k - 32);
+          if (lane + 32 > k) v1 = fma(-sD[k * TRSM_W + lane + 32], xk, v1);
+        }
+      } else {
+        for (int k = 0; k < w; ++k) {
+          const double xk = __shfl_sync(0xffffffffu, k < 32 ? v0 : v1, k & 31);
+          if (lane > k) v0 = fma(-sD[k * TRSM_W + lane], xk, v0);
+          if (lane + 32 > k) v1 = fma(-sD[k * TRSM_W + lane + 32], xk, v1);
+        }
       }
       if (lane < w) sB[(r0 + lane) * NC + c] = v0;
       if (lane + 32 < w) sB[(r0 + lane + 32) * NC + c] = v1;
     }
     __syncthreads();
-    // rows below the block: each thread owns up to TRSMF_RPT rows and issues
-    // the L loads of all of them per batch of TRSMF_KB columns (one L2 round
-    // trip per batch instead of one per row and batch)
+    // the next diagonal block into the other buffer (last read by block - 1)
+    if (r0 + TRSM_W < jb)
+      trsmf_fetch_diag(L, ldl, jb, r0 + TRSM_W, sDb + ((r0 / TRSM_W + 1) & 1) * TRSM_W * TRSM_W,
+                       tid);
+    // rows below the block: only as many rows per thread as there are rows
+    // left (a CTA-uniform count), so no predicated-off FMA issues
     {
-      double b[TRSMF_RPT][NC];
-      int rr[TRSMF_RPT];
-#pragma unroll
-      for (int q = 0; q < TRSMF_RPT; ++q) {
-        rr[q] = r0 + w + tid + q * TRSMF_THREADS;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) b[q][c] = rr[q] < jb ? sB[rr[q] * NC + c] : 0.0;
+      const int below = jb - r0 - w;
+      if (below > 2 * TRSMF_THREADS) {
+        if (below > 3 * TRSMF_THREADS)
+          trsmf_rows_below<4, NC>(L, ldl, jb, r0, w, sB, tid);
+        else
+          trsmf_rows_below<3, NC>(L, ldl, jb, r0, w, sB, tid);
+      } else if (below > TRSMF_THREADS) {
+        trsmf_rows_below<2, NC>(L, ldl, jb, r0, w, sB, tid);
+      } else if (below > 0) {
+        trsmf_rows_below<1, NC>(L, ldl, jb, r0, w, sB, tid);
       }
-      for (int k0 = 0; k0 < w; k0 += TRSMF_KB) {
-        double l[TRSMF_RPT][TRSMF_KB];
-#pragma unroll
-        for (int q = 0; q < TRSMF_RPT; ++q)
-#pragma unroll
-          for (int u = 0; u < TRSMF_KB; ++u)
-            l[q][u] = (rr[q] < jb && k0 + u < w) ? __ldg(L + (int64_t)(r0 + k0 + u) * ldl + rr[q])
-                                                 : 0.0;
-#pragma unroll
-        for (int u = 0; u < TRSMF_KB; ++u) {
-          if (k0 + u < w) {
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-              const double x = sB[(r0 + k0 + u) * NC + c];
-#pragma unroll
-              for (int q = 0; q < TRSMF_RPT; ++q) b[q][c] = fma(-l[q][u], x, b[q][c]);
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < TRSMF_RPT; ++q)
-        if (rr[q] < jb)
-#pragma unroll
-          for (int c = 0; c < NC; ++c) sB[rr[q] * NC + c] = b[q][c];
     }
     __syncthreads();
   }
@@ -825,7 +874,7 @@ __global__ void __launch_bounds__(TRSMF_THREADS) trsm_fused_kernel(
 }
 template <int NC>
 constexpr size_t trsmf_smem(int jb) {
-  return sizeof(double) * ((size_t)jb * NC + TRSM_W * (TRSM_W + 1));
+  return sizeof(double) * ((size_t)jb * NC + 2 * TRSM_W * TRSM_W);
 }
 
 // --------------------------------------------------------------- reductions
@@ -1188,6 +1237,8 @@ int trsm_blocked(double* a, int64_t lda, int64_t j, int64_t jb, double* b, int64
   }
   if (!legacy && jb <= TRSMF_MAXJB && ncols <= 2048) {
     const int tag = prof_start(st);
+    // 8 columns per CTA: measured faster than 4 or 2 (more CTAs) at every
+    // panel-recursion shape and inside the LU (profiles/r02bm_trsm_nc_ab.log)
     const int s = trsm_fused<8>(a + j * lda + j, lda, jb, b, ldb, ncols, st, max_ctas);
     prof_stop(tag, st, PROF_TRSM, (double)jb * jb * ncols);
     return s;
