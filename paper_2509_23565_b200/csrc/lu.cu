@@ -673,48 +673,63 @@ __global__ void __launch_bounds__(LSWR_WARPS * 32, 1) laswp_list_reg_kernel(
 // ---------------------------------------------------------------- small trsm
 // B[0:w, c] <- L^{-1} B[0:w, c], L the unit-lower w x w block (w <= TRSM_W).
 // One thread per right-hand-side column, the column held in registers, L in
-// shared memory (broadcast reads); the 64 x TRSM_COLS tile is staged through
-// shared memory so global loads/stores are coalesced along the columns.
+// shared memory column by column (sLt[i][r] = L[r][i], so the update of rows
+// i+1.. reads consecutive words: 16-byte broadcast loads, half the shared
+// wavefronts of a row-major copy).  The L block and the 64 x TRSM_COLS tile of
+// B arrive by cp.async (every load in flight at once; the tile is row-major
+// with a one-word pad so the column-wise writes and the per-thread row reads
+// are both conflict-free), and the result leaves through the same tile,
+// coalesced along the columns.  Per element the order is b_r = fma(-l_ri,
+// x_i, b_r) for i = 0, 1, ...: the sequential forward substitution.
 constexpr int TRSM_COLS = 128;
+constexpr int TRSM_LDX = TRSM_COLS + 1;
 __global__ void __launch_bounds__(TRSM_COLS) trsm_unit_lower_kernel(
     const double* __restrict__ L, int64_t ldl, int w, double* __restrict__ B, int64_t ldb,
     int64_t ncols) {
   extern __shared__ double dsm[];
-  double* sL = dsm;                         // [TRSM_W][TRSM_W], row-major sL[r*W+c]
-  double* sX = dsm + TRSM_W * TRSM_W;       // [TRSM_W][TRSM_COLS]
+  double* sL = dsm;                         // [TRSM_W][TRSM_W], sL[i*W + r] = L[r][i]
+  double* sX = dsm + TRSM_W * TRSM_W;       // [TRSM_W][TRSM_LDX]
   const int tid = threadIdx.x;
   const int64_t c0 = (int64_t)blockIdx.x * TRSM_COLS;
-#pragma unroll 8
-  for (int i = tid; i < TRSM_W * TRSM_W; i += TRSM_COLS) {
-    const int r = i % TRSM_W, c = i / TRSM_W;
-    sL[r * TRSM_W + c] = (r < w && c < w && r > c) ? __ldg(L + c * ldl + r) : 0.0;
+  for (int e = tid; e < TRSM_W * TRSM_W; e += TRSM_COLS) {
+    const int i = e / TRSM_W, r = e - i * TRSM_W;
+    if (r < w && i < w && r > i)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sL + e)),
+                   "l"(L + (int64_t)i * ldl + r)
+                   : "memory");
+    else
+      sL[e] = 0.0;
   }
-  const int lane = tid & 31, wid = tid >> 5;
-#pragma unroll 8
-  for (int c = wid; c < TRSM_COLS; c += TRSM_COLS / 32) {
-    const bool okc = c0 + c < ncols;
-#pragma unroll
-    for (int r = lane; r < TRSM_W; r += 32)
-      sX[r * TRSM_COLS + c] = (okc && r < w) ? B[(c0 + c) * ldb + r] : 0.0;
+  const int nc = (int)(ncols - c0 < TRSM_COLS ? ncols - c0 : TRSM_COLS);
+  for (int e = tid; e < TRSM_W * TRSM_COLS; e += TRSM_COLS) {
+    const int c = e / TRSM_W, r = e - c * TRSM_W;
+    if (c < nc && r < w)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sX + r * TRSM_LDX + c)),
+                   "l"(B + (c0 + c) * ldb + r)
+                   : "memory");
+    else
+      sX[r * TRSM_LDX + c] = 0.0;
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   double x[TRSM_W];
 #pragma unroll
-  for (int i = 0; i < TRSM_W; ++i) x[i] = sX[i * TRSM_COLS + tid];
+  for (int i = 0; i < TRSM_W; ++i) x[i] = sX[i * TRSM_LDX + tid];
 #pragma unroll
   for (int i = 0; i < TRSM_W - 1; ++i) {
 #pragma unroll
-    for (int r = i + 1; r < TRSM_W; ++r) x[r] = fma(-sL[r * TRSM_W + i], x[i], x[r]);
+    for (int r = i + 1; r < TRSM_W; ++r) x[r] = fma(-sL[i * TRSM_W + r], x[i], x[r]);
   }
 #pragma unroll
-  for (int i = 0; i < TRSM_W; ++i) sX[i * TRSM_COLS + tid] = x[i];
+  for (int i = 0; i < TRSM_W; ++i) sX[i * TRSM_LDX + tid] = x[i];
   __syncthreads();
-  for (int c = wid; c < TRSM_COLS; c += TRSM_COLS / 32) {
-    if (c0 + c >= ncols) continue;
-    for (int r = lane; r < w; r += 32) B[(c0 + c) * ldb + r] = sX[r * TRSM_COLS + c];
+  for (int e = tid; e < TRSM_W * TRSM_COLS; e += TRSM_COLS) {
+    const int c = e / TRSM_W, r = e - c * TRSM_W;
+    if (c < nc && r < w) B[(c0 + c) * ldb + r] = sX[r * TRSM_LDX + c];
   }
 }
-constexpr size_t TRSM_SMEM = sizeof(double) * (TRSM_W * TRSM_W + TRSM_W * TRSM_COLS);
+constexpr size_t TRSM_SMEM = sizeof(double) * (TRSM_W * TRSM_W + TRSM_W * TRSM_LDX);
 
 // Whole-panel forward substitution in one launch: B[0:jb, c] <- L^{-1} B[0:jb, c]
 // for NC columns per CTA, L unit lower jb x jb (jb <= 1024).  The CTA keeps its
@@ -1855,13 +1870,20 @@ double emu_rate(int npairs) {
   return r * 1.09 * scale;
 }
 
+// modelled in-LU panel time (s) of an m x nb panel on s SMs
+double panel_model(int64_t m, int64_t nb, int s) {
+  static const double a = getenv("OZ_LA_TP_A") ? atof(getenv("OZ_LA_TP_A")) : 5.2e-6;  // tuning
+  static const double b = getenv("OZ_LA_TP_B") ? atof(getenv("OZ_LA_TP_B")) : 1.2e-8;
+  return (double)nb * (a + b * (double)m / s);
+}
+
 // phase-1 width for a given S: the columns sms - S SMs update while the panel runs
 int64_t phase1_cols(int s, int64_t m, int64_t nb, int npairs, int sms, int64_t rest) {
   if (rest <= 0 || npairs <= 0) return rest > 0 ? rest : 0;
   const double rate = emu_rate(npairs);
   const double ops_per_col = 2.0 * npairs * (double)m * (double)nb;
   const double t_lt = 0.8e-3 + 1.17e-7 * (double)rest;
-  const double tp = (double)nb * (5.2e-6 + 1.2e-8 * (double)m / s);
+  const double tp = panel_model(m, nb, s);
   const double r1 = rate * (double)(sms - s) / sms;
   double x = (tp - t_lt) * r1 / ops_per_col;
   if (x < 0) x = 0;
@@ -1877,7 +1899,7 @@ LaPlan lookahead_plan(int setting, int64_t m, int64_t nb, int npairs, int sms, i
   const double t_lt = 0.8e-3 + 1.17e-7 * (double)rest;
   double best_t = 1e30;
   for (int s = 16; s <= sms - 16; s += 2) {
-    const double tp = (double)nb * (5.2e-6 + 1.2e-8 * (double)m / s);
+    const double tp = panel_model(m, nb, s);
     const double r1 = rate * (double)(sms - s) / sms;
     // phase-1 columns: what the reduced grid finishes while the panel runs
     double x = (tp - t_lt) * r1 / ops_per_col;

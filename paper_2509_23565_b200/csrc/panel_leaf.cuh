@@ -86,6 +86,44 @@ __device__ __forceinline__ void leaf_push(uint32_t dst, uint32_t src, uint32_t b
       : "memory");
 }
 
+// Grid variant records as tagged 8-byte words (LL protocol): each word holds
+// 32 payload bits and the step's 32-bit tag, so a reader that sees the tag
+// in a word has that word's payload — no fence on the writer, no ordering
+// between words.  A record is 2 + W pairs of words (16-byte stores).
+constexpr int LEAF_LL_STRIDE = 2 * (2 + 64);  // words per CTA slot (W <= 64)
+__device__ __forceinline__ void leaf_ll_store(unsigned long long* p, unsigned lo, unsigned hi,
+                                              unsigned tag) {
+  const unsigned long long t = (unsigned long long)tag << 32;
+  asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(t | lo), "l"(t | hi)
+               : "memory");
+}
+__device__ __forceinline__ void leaf_ll_load(const unsigned long long* p, unsigned tag,
+                                             unsigned& lo, unsigned& hi) {
+  unsigned long long x, y;
+  do {
+    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(p)
+                 : "memory");
+  } while ((unsigned)(x >> 32) != tag || (unsigned)(y >> 32) != tag);
+  lo = (unsigned)x;
+  hi = (unsigned)y;
+}
+__device__ __forceinline__ void leaf_ll_load2(const unsigned long long* p, unsigned tag,
+                                              unsigned& w0, unsigned& w1, unsigned& w2,
+                                              unsigned& w3) {
+  unsigned long long x, y, z, u;
+  do {
+    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(p)
+                 : "memory");
+    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(z), "=l"(u) : "l"(p + 2)
+                 : "memory");
+  } while ((unsigned)(x >> 32) != tag || (unsigned)(y >> 32) != tag ||
+           (unsigned)(z >> 32) != tag || (unsigned)(u >> 32) != tag);
+  w0 = (unsigned)x;
+  w1 = (unsigned)y;
+  w2 = (unsigned)z;
+  w3 = (unsigned)u;
+}
+
 // OZ_PANEL_TIMING (tuning): thread 0 of CTA 0 adds per-phase clock64 deltas to
 // p.dbg[0..5]; the owner thread of CTA 0 adds its record+push time to p.dbg[6]
 #define LEAF_MARK(i)                                                   \
@@ -105,6 +143,7 @@ template <int W, int RPT, int NT, bool kGrid>
 __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(PanelArgs p) {
   constexpr int R = NT * RPT;
   static_assert(4 + W <= CAND_STRIDE, "grid record must fit a candidate slot");
+  static_assert(2 * (2 + W) <= LEAF_LL_STRIDE, "grid record must fit a tagged slot");
   extern __shared__ double lbuf[];  // [W][R]: L (and, for pivot rows, U) values by window row
   __shared__ LeafShared<W, NT, kGrid> sh;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -226,16 +265,24 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(PanelArgs p) {
         }
       }
       if constexpr (kGrid) {
-        // the record to this CTA's global slot; the tag word last (release)
+        // the record to this CTA's global slot as tagged words (no fence):
+        // pair 0 = |v|, pair 1 = (pos, row), pair 2 + c = value c
         __syncwarp();
-        double* gs = p.cand + ((size_t)b * G + g) * CAND_STRIDE;
-        for (int c = lane; c < 4 + W; c += 32)
-          if (c != 1) gs[c] = rec[c];
-        __syncwarp();
-        if (lane == 0)
-          st_release_u64(reinterpret_cast<long long*>(gs) + 1,
-                         ((unsigned long long)tag << 32) |
-                             (unsigned)reinterpret_cast<const long long*>(rec)[1]);
+        unsigned long long* gs =
+            reinterpret_cast<unsigned long long*>(p.cand) + ((size_t)b * G + g) * LEAF_LL_STRIDE;
+        const long long* irec = reinterpret_cast<const long long*>(rec);
+        for (int c = lane; c < 2 + W; c += 32) {
+          unsigned lo, hi;
+          if (c == 1) {
+            lo = (unsigned)irec[1];
+            hi = (unsigned)irec[2];
+          } else {
+            const unsigned long long v = (unsigned long long)irec[c == 0 ? 0 : c + 2];
+            lo = (unsigned)v;
+            hi = (unsigned)(v >> 32);
+          }
+          leaf_ll_store(gs + 2 * c, lo, hi, tag);
+        }
       } else {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
@@ -273,31 +320,39 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(PanelArgs p) {
     int rp, rg;
     if constexpr (kGrid) {
       if (wid == 0) {
-        // lane l polls CTAs l, l+32, ... (tag word, acquire), then the warp
-        // reduces and copies the winner's record into shared memory
-        const double* slots = p.cand + (size_t)b * G * CAND_STRIDE;
+        // lane l polls the headers of CTAs l, l+32, ... until both pairs
+        // carry this step's tag, the warp reduces, then copies the winner's
+        // row (polling each pair's tags) into shared memory
+        const unsigned long long* slots =
+            reinterpret_cast<const unsigned long long*>(p.cand) + (size_t)b * G * LEAF_LL_STRIDE;
         double a1 = -2.0;
         int p1 = 0x7fffffff, g1 = -1;
         for (int gg = lane; gg < G; gg += 32) {
-          const long long* tw = reinterpret_cast<const long long*>(slots + (size_t)gg * CAND_STRIDE) + 1;
-          unsigned long long wv;
-          do {
-            wv = ld_acquire_u64(tw);
-          } while ((unsigned)(wv >> 32) != tag);
-          const double av = __ldcg(slots + (size_t)gg * CAND_STRIDE);
-          const int pv = (int)(unsigned)(wv & 0xffffffffull);
-          if (better(av, pv, a1, p1)) {
+          const unsigned long long* r = slots + (size_t)gg * LEAF_LL_STRIDE;
+          unsigned a_lo, a_hi, pv, rv;
+          leaf_ll_load2(r, tag, a_lo, a_hi, pv, rv);
+          const double av = __longlong_as_double((long long)(((unsigned long long)a_hi << 32) | a_lo));
+          if (better(av, (int)pv, a1, p1)) {
             a1 = av;
-            p1 = pv;
+            p1 = (int)pv;
             g1 = gg;
           }
         }
         warp_argmax(a1, p1, g1);
-        __syncwarp();  // every lane's acquire precedes the reads of the winner
-        const double* win = slots + (size_t)g1 * CAND_STRIDE;
-        for (int c = lane; c < 4 + W; c += 32)
-          if (c != 1) sh.rec[b][0][c] = __ldcg(win + c);
-        if (lane == 0) reinterpret_cast<long long*>(sh.rec[b][0])[1] = p1;
+        const unsigned long long* win = slots + (size_t)g1 * LEAF_LL_STRIDE;
+        long long* irw = reinterpret_cast<long long*>(sh.rec[b][0]);
+        for (int c = lane; c < 1 + W; c += 32) {
+          unsigned lo, hi;
+          leaf_ll_load(win + 2 * (c == 0 ? 1 : c + 1), tag, lo, hi);
+          if (c == 0)
+            irw[2] = (long long)(int)hi;
+          else
+            irw[3 + c] = (long long)(((unsigned long long)hi << 32) | lo);
+        }
+        if (lane == 0) {
+          sh.rec[b][0][0] = a1;
+          irw[1] = p1;
+        }
       }
       __syncthreads();
       ra = sh.rec[b][0][0];
