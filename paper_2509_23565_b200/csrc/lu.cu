@@ -1870,7 +1870,11 @@ double emu_rate(int npairs) {
   return r * 1.09 * scale;
 }
 
-// modelled in-LU panel time (s) of an m x nb panel on s SMs
+// Modelled in-LU panel time (s) of an m x nb panel on s SMs (the fit of the
+// two-phase comment above).  A model in which register-leaf panels do not
+// depend on s (true standalone) picked the fewest SMs that fit the leaf and
+// lost: beside a GEMM on more SMs the panel ran 1.2-1.5x slower
+// (profiles/r02bt_panel_model_ab.log); the 1/s term stands in for that.
 double panel_model(int64_t m, int64_t nb, int s) {
   static const double a = getenv("OZ_LA_TP_A") ? atof(getenv("OZ_LA_TP_A")) : 5.2e-6;  // tuning
   static const double b = getenv("OZ_LA_TP_B") ? atof(getenv("OZ_LA_TP_B")) : 1.2e-8;
