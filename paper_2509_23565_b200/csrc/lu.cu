@@ -1365,6 +1365,17 @@ bool leaf_grid_enabled() {
   }();
   return v;
 }
+// OZ_PANEL_LEAF_TALL=0: the tallest panels keep the shared-memory leaf (A/B).
+// 1024 rows per CTA with 16-column windows measured 465 -> 461 ms at n =
+// 32768; 2048 rows with 8-column windows (twice the recursion's inner nodes)
+// lost (484 ms, profiles/r02bw_tall_leaf_ab.log) and was dropped.
+bool leaf_tall_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("OZ_PANEL_LEAF_TALL");
+    return e == nullptr || atoi(e) != 0;
+  }();
+  return v;
+}
 int leaf_variant(int64_t m, int w, int max_ctas) {
   if (!leaf_enabled() || m < 1) return 0;
   const int rpt = leaf_max_rpt();
@@ -1389,6 +1400,9 @@ int leaf_variant(int64_t m, int w, int max_ctas) {
   // taller: one co-resident grid, records exchanged through global memory
   if (w <= 64 && ceil_div(m, (int64_t)256) <= cap) return 64120;
   if (w <= 32 && ceil_div(m, (int64_t)512) <= cap) return 32220;
+  // tallest (early look-ahead panels on few SMs): narrower windows, more rows
+  // per thread, instead of the shared-memory leaf
+  if (leaf_tall_enabled() && w <= 16 && ceil_div(m, (int64_t)1024) <= cap) return 16420;
   return 0;
 }
 // widest leaf the register variants take at this height (0: none)
@@ -1403,6 +1417,7 @@ int leaf_width_for(int64_t m, int max_ctas) {
   if (leaf_grid_enabled()) {
     if (ceil_div(m, (int64_t)256) <= cap) return 64;
     if (ceil_div(m, (int64_t)512) <= cap) return 32;
+    if (leaf_tall_enabled() && ceil_div(m, (int64_t)1024) <= cap) return 16;
   }
   if (rpt >= 4 && m <= (int64_t)LEAF_MAXG * 1024 && ceil_div(m, (int64_t)1024) <= cap) return 16;
   return 0;
@@ -1476,6 +1491,7 @@ int panel_leaf(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t bas
     case 1642: s = panel_leaf_launch<16, 4, 256>(pa, st); break;
     case 64120: s = panel_leaf_launch<64, 1, 256, true>(pa, st); break;
     case 32220: s = panel_leaf_launch<32, 2, 256, true>(pa, st); break;
+    case 16420: s = panel_leaf_launch<16, 4, 256, true>(pa, st); break;
     default: s = OZ_UNSUPPORTED;
   }
   prof_stop(tag, st, PROF_PANEL, (double)m * w);

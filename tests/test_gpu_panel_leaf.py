@@ -7,7 +7,8 @@ where a distributed argmax can go wrong.  Heights cover every leaf variant:
 register leaf with one cluster of 128-row CTAs (m <= 2048), 256-row CTAs
 (m <= 4096), two rows per thread (m <= 8192, 32-column windows), and the
 register leaf with the global-memory exchange beyond (256 rows per CTA up to
-the SM count, then 512 with 32-column windows)."""
+the SM count, then 512 with 32-column windows, then 1024 / 2048 with 16 / 8
+columns on capped grids)."""
 
 import numpy as np
 import pytest
@@ -36,7 +37,7 @@ def _reference_panel(a):
     return a, piv, zero
 
 
-def _device_panel(a):
+def _device_panel(a, max_ctas=0):
     import torch
 
     from paper_2509_23565_b200 import _dev, _lib
@@ -49,7 +50,7 @@ def _device_panel(a):
     info = torch.zeros((1,), dtype=torch.int32, device="cuda")
     bits = torch.zeros((2,), dtype=torch.int64, device="cuda")
     _lib.call("oz_lu_panel", d.data_ptr(), m, m, jb, 0, ipiv.data_ptr(), info.data_ptr(),
-              bits.data_ptr(), ws.data_ptr(), wsb, m, jb, 0, 0, _dev.stream())
+              bits.data_ptr(), ws.data_ptr(), wsb, m, jb, 0, max_ctas, _dev.stream())
     torch.cuda.synchronize()
     return d.cpu().numpy().T, ipiv.cpu().numpy(), int(info.item())
 
@@ -62,6 +63,19 @@ def test_leaf_ties_match_reference(m, jb):
     a = rng.integers(-4, 5, size=(m, jb)).astype(np.float64)
     want, piv, zero = _reference_panel(a)
     got, ipiv, info = _device_panel(a)
+    assert zero == 0 and info == 0
+    assert np.array_equal(ipiv, piv)
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("m,jb,ctas", [(12000, 16, 12), (5000, 16, 5)])
+def test_tall_leaf_ties_match_reference(m, jb, ctas):
+    """The tall register variants on a capped grid (look-ahead side stream):
+    1024 rows per CTA with 16-column windows, 2048 with 8-column windows."""
+    rng = np.random.default_rng(m + ctas)
+    a = rng.integers(-4, 5, size=(m, jb)).astype(np.float64)
+    want, piv, zero = _reference_panel(a)
+    got, ipiv, info = _device_panel(a, ctas)
     assert zero == 0 and info == 0
     assert np.array_equal(ipiv, piv)
     assert np.array_equal(got, want)
