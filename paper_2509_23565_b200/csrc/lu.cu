@@ -1897,13 +1897,26 @@ double panel_model(int64_t m, int64_t nb, int s) {
   return (double)nb * (a + b * (double)m / s);
 }
 
+// Panel time for sizing phase 1 once S is chosen: panels on the register
+// leaves finish ahead of the model the S search uses — ~20 % with 32/64-column
+// windows (<= 512 rows per SM), ~10 % with the tall 16-column variant
+// (OZ_LU_TRACE "p1-panel" column at n = 32768: phase 1 ran 0.6-2.5 ms past
+// the panel in steps 8-27 with the plain model, the panel's SMs idle;
+// profiles/r02bz_phase1_ab.log).
+double panel_time_p1(int64_t m, int64_t nb, int s) {
+  static const double f = getenv("OZ_LA_P1_REG") ? atof(getenv("OZ_LA_P1_REG")) : 0.8;  // tuning
+  static const double f16 = getenv("OZ_LA_P1_TALL") ? atof(getenv("OZ_LA_P1_TALL")) : 0.9;
+  const int w = leaf_width_for(m, s);
+  return panel_model(m, nb, s) * (w >= 32 ? f : w > 0 ? f16 : 1.0);
+}
+
 // phase-1 width for a given S: the columns sms - S SMs update while the panel runs
 int64_t phase1_cols(int s, int64_t m, int64_t nb, int npairs, int sms, int64_t rest) {
   if (rest <= 0 || npairs <= 0) return rest > 0 ? rest : 0;
   const double rate = emu_rate(npairs);
   const double ops_per_col = 2.0 * npairs * (double)m * (double)nb;
   const double t_lt = 0.8e-3 + 1.17e-7 * (double)rest;
-  const double tp = panel_model(m, nb, s);
+  const double tp = panel_time_p1(m, nb, s);
   const double r1 = rate * (double)(sms - s) / sms;
   double x = (tp - t_lt) * r1 / ops_per_col;
   if (x < 0) x = 0;
@@ -1930,10 +1943,11 @@ LaPlan lookahead_plan(int setting, int64_t m, int64_t nb, int npairs, int sms, i
     if (t < best_t) {
       best_t = t;
       best.sms = s;
-      // round phase 1 to whole 128-column GEMM tiles
-      best.cols1 = std::min<int64_t>(rest, ((int64_t)x + 127) / 128 * 128);
     }
   }
+  // phase 1 sized with the refined panel time at the chosen S (whole
+  // 128-column GEMM tiles)
+  best.cols1 = phase1_cols(best.sms, m, nb, npairs, sms, rest);
   return best;
 }
 
@@ -2244,6 +2258,7 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
           tr.mark_sub(st);
           tr.mark_sub(st);
           tr.mark_sub(st);
+          tr.mark_sub(st);
         } else {
           if (aux)
             OZ_CHECK_CUDA(cudaStreamWaitEvent(st, side->aux_done, 0));
@@ -2255,6 +2270,7 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
           OZ_TRY(schur_split_part(sc, false, jb2, rest, ws, st));
           tr.mark_sub(st);
           OZ_TRY(schur_cols(sc, jb2, p1_end, ws, st, sm_count() - la_sms));
+          tr.mark_sub(st);
           if (p1_end < rest) {
             OZ_CHECK_CUDA(cudaStreamWaitEvent(st, side->done, 0));
             OZ_TRY(schur_cols(sc, p1_end, rest, ws, st));
@@ -2276,20 +2292,22 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
     cudaStreamSynchronize(st);
     // 7 marks per full step: start, laswp, trsm, split, gemm_a, side_done, gemm_b
     fprintf(stderr, "step    m  laswp  trsm  split gemm_a  panel(side) gemm_b  total [ms]  sms"
-                    "  (rest: laswp trsm split gemm)\n");
+                    "  (rest: laswp trsm split gemm) p1-panel\n");
     for (size_t i = 0; i + 7 <= tr.ev.size(); i += 7) {
       float t[7];
       for (int q2 = 1; q2 < 7; ++q2) cudaEventElapsedTime(&t[q2], tr.ev[i], tr.ev[i + q2]);
       const float total = i + 7 < tr.ev.size() ? [&] { float x; cudaEventElapsedTime(&x, tr.ev[i], tr.ev[i + 7]); return x; }() : t[6];
       const size_t si = i / 7;
-      float r3[3] = {0, 0, 0};
-      if (3 * si + 2 < tr.sub.size())
-        for (int q3 = 0; q3 < 3; ++q3) cudaEventElapsedTime(&r3[q3], tr.ev[i + 4], tr.sub[3 * si + q3]);
-      fprintf(stderr, "%4zu %6lld %6.2f %5.2f %6.2f %6.2f %11.2f %6.2f %6.2f %4d  %5.2f %5.2f %5.2f %6.2f\n",
+      float r3[4] = {0, 0, 0, 0};
+      if (4 * si + 3 < tr.sub.size())
+        for (int q3 = 0; q3 < 4; ++q3) cudaEventElapsedTime(&r3[q3], tr.ev[i + 4], tr.sub[4 * si + q3]);
+      // p1-panel: end of phase 1 minus end of the panel (> 0: the panel's SMs
+      // idled; < 0: the other SMs waited for the panel)
+      fprintf(stderr, "%4zu %6lld %6.2f %5.2f %6.2f %6.2f %11.2f %6.2f %6.2f %4d  %5.2f %5.2f %5.2f %6.2f %7.2f\n",
               si, (long long)(n - (int64_t)si * nb - nb), t[1], t[2] - t[1], t[3] - t[2],
               t[4] - t[3], t[5] - t[4], t[6] - t[4], total,
               si < tr.split.size() ? tr.split[si] : 0, r3[0], r3[1] - r3[0], r3[2] - r3[1],
-              t[6] - t[4] - r3[2]);
+              t[6] - t[4] - r3[2], r3[3] - (t[5] - t[4]));
     }
     for (auto e : tr.ev) cudaEventDestroy(e);
     for (auto e : tr.sub) cudaEventDestroy(e);
