@@ -1902,12 +1902,13 @@ double panel_model(int64_t m, int64_t nb, int s) {
 // windows (<= 512 rows per SM), ~10 % with the tall 16-column variant
 // (OZ_LU_TRACE "p1-panel" column at n = 32768: phase 1 ran 0.6-2.5 ms past
 // the panel in steps 8-27 with the plain model, the panel's SMs idle;
-// profiles/r02bz_phase1_ab.log).
+// profiles/r02bz_phase1_ab.log); shared-memory leaves ~6 % behind it.
 double panel_time_p1(int64_t m, int64_t nb, int s) {
   static const double f = getenv("OZ_LA_P1_REG") ? atof(getenv("OZ_LA_P1_REG")) : 0.8;  // tuning
   static const double f16 = getenv("OZ_LA_P1_TALL") ? atof(getenv("OZ_LA_P1_TALL")) : 0.9;
+  static const double fs = getenv("OZ_LA_P1_SMEM") ? atof(getenv("OZ_LA_P1_SMEM")) : 1.06;
   const int w = leaf_width_for(m, s);
-  return panel_model(m, nb, s) * (w >= 32 ? f : w > 0 ? f16 : 1.0);
+  return panel_model(m, nb, s) * (w >= 32 ? f : w > 0 ? f16 : fs);
 }
 
 // phase-1 width for a given S: the columns sms - S SMs update while the panel runs
