@@ -1946,6 +1946,15 @@ LaPlan lookahead_plan(int setting, int64_t m, int64_t nb, int npairs, int sms, i
       best.sms = s;
     }
   }
+  // Tallest panels: where the search lands on a shared-memory leaf, take the
+  // fewest SMs that fit the 1024-row register leaf instead (up to
+  // OZ_LA_TALL_MAX): about the same SM-time, a panel ~2x shorter — which the
+  // overlapped upload needs, its first steps being a chain of panels.
+  static const int tall_max = getenv("OZ_LA_TALL_MAX") ? atoi(getenv("OZ_LA_TALL_MAX")) : 32;
+  if (tall_max > 0 && leaf_tall_enabled() && leaf_width_for(m, best.sms) == 0) {
+    const int st = (int)((ceil_div(m, (int64_t)1024) + 1) & ~1);
+    if (st > best.sms && st <= tall_max && leaf_width_for(m, st) > 0) best.sms = st;
+  }
   // phase 1 sized with the refined panel time at the chosen S (whole
   // 128-column GEMM tiles)
   best.cols1 = phase1_cols(best.sms, m, nb, npairs, sms, rest);
@@ -1989,6 +1998,7 @@ struct SideStream {
   cudaEvent_t ready = nullptr, done = nullptr;
   cudaStream_t aux = nullptr;  // early steps: the rest's row interchanges
   cudaEvent_t aux_ready = nullptr, aux_done = nullptr;
+  cudaStream_t step[8] = {};  // upload phase: one stream per wavefront step
 };
 int side_stream(SideStream** out) {
   static thread_local std::vector<SideStream> per_dev;
@@ -2007,6 +2017,7 @@ int side_stream(SideStream** out) {
     OZ_CHECK_CUDA(cudaStreamCreateWithPriority(&s.aux, cudaStreamNonBlocking, lo));
     OZ_CHECK_CUDA(cudaEventCreateWithFlags(&s.aux_ready, cudaEventDisableTiming));
     OZ_CHECK_CUDA(cudaEventCreateWithFlags(&s.aux_done, cudaEventDisableTiming));
+    for (auto& x : s.step) OZ_CHECK_CUDA(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, lo));
   }
   *out = &s;
   return OZ_OK;
@@ -2073,8 +2084,10 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
   // loop), panels 1..S factored on the side stream as soon as their columns
   // have received the earlier steps.  The loop below continues at step S.
   const int64_t nblk = ceil_div(n, nb);
-  // measured at n = 32768, nb = 1024 (wavefront): S = 0/3/4/5/6 -> 609/567/578/585/592 ms e2e
-  static const int phase_env = getenv("OZ_UPLOAD_STEPS") ? atoi(getenv("OZ_UPLOAD_STEPS")) : 3;
+  // measured at n = 32768, nb = 1024 with per-step streams and the tall-leaf
+  // panel SMs: S = 3/4/5 -> 511/497/498 ms e2e (profiles/r02ci_upload_ab.log;
+  // single stream, smem-leaf panels: 3/4/5/6 -> 567/578/585/592)
+  static const int phase_env = getenv("OZ_UPLOAD_STEPS") ? atoi(getenv("OZ_UPLOAD_STEPS")) : 4;
   const int S = (int)std::min<int64_t>(phase_env, nblk - 2);
   if (chunk_ready && side != nullptr && backend != 2 && S >= 1 && ready_cols < n &&
       chunk_cols % nb == 0) {
@@ -2100,11 +2113,47 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
                           a + (j0 + jbs) * lda + j0, lda, a + (j0 + jbs) * lda + (j0 + jbs), lda,
                           k, q, npairs, pa, pb, ps, ws.bits});
     }
-    std::vector<bool> have(S + 1, false);  // panel s ready on the main stream (A21 split)
+    // Each wavefront step runs on its own stream (OZ_UPLOAD_STREAMS=0: all on
+    // the caller's stream), so a step waiting for its panel does not hold up
+    // the earlier steps' updates of newly arrived blocks; block c's step s
+    // follows its step s - 1 through an event.  Each step stream composes its
+    // interchange lists in its own buffers.
+    static const bool step_streams_env =
+        !getenv("OZ_UPLOAD_STREAMS") || atoi(getenv("OZ_UPLOAD_STREAMS")) != 0;
+    const bool step_streams = step_streams_env && S <= 8;
+    std::vector<cudaStream_t> sst(S, st);
+    int32_t* cmp_buf = nullptr;
+    const int64_t nch = ceil_div(n, chunk_cols);
+    std::vector<cudaEvent_t> cdone;  // [s * nch + c]: block c has received step s
+    cudaEvent_t evm = nullptr;
+    uint8_t* stepb_buf = nullptr;  // per step: U12 slices + exponents of one block, split scratch
+    const size_t slabB = (size_t)planes * (size_t)chunk_cols * ws.ldK;
+    const size_t stepb = align_up(slabB) + align_up(sizeof(int32_t) * chunk_cols) + 256;
+    if (step_streams) {
+      for (int s2 = 0; s2 < S; ++s2) sst[s2] = side->step[s2];
+      const size_t per = 2 * LSWP_MAX + 4;
+      OZ_CHECK_CUDA(cudaMallocAsync(&cmp_buf, sizeof(int32_t) * per * S, st));
+      OZ_CHECK_CUDA(cudaMallocAsync(&stepb_buf, stepb * S, st));
+      for (int s2 = 0; s2 < S; ++s2) {
+        wss[s2].cdst = cmp_buf + per * s2;
+        wss[s2].csrc = wss[s2].cdst + LSWP_MAX;
+        wss[s2].ccnt = wss[s2].csrc + LSWP_MAX;
+        uint8_t* b0 = stepb_buf + stepb * s2;
+        wss[s2].slB = reinterpret_cast<int8_t*>(b0);
+        wss[s2].expB = reinterpret_cast<int32_t*>(b0 + align_up(slabB));
+        wss[s2].split_aux = b0 + align_up(slabB) + align_up(sizeof(int32_t) * chunk_cols);
+      }
+      cdone.resize((size_t)S * nch);
+      for (auto& e : cdone) OZ_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      OZ_CHECK_CUDA(cudaEventCreateWithFlags(&evm, cudaEventDisableTiming));
+      OZ_CHECK_CUDA(cudaEventRecord(evm, st));  // allocations and memsets above
+      for (int s2 = 0; s2 < S; ++s2) OZ_CHECK_CUDA(cudaStreamWaitEvent(sst[s2], evm, 0));
+    }
+    std::vector<bool> have(S + 1, false);  // panel s ready on its step stream (A21 split)
     auto ensure_panel = [&](int s2) -> int {
       if (have[s2]) return OZ_OK;
-      if (s2 > 0) OZ_CHECK_CUDA(cudaStreamWaitEvent(st, pdone[s2], 0));
-      if (s2 < S) OZ_TRY(schur_split_part(scs[s2], true, 0, 0, wss[s2], st));
+      if (s2 > 0) OZ_CHECK_CUDA(cudaStreamWaitEvent(sst[s2], pdone[s2], 0));
+      if (s2 < S) OZ_TRY(schur_split_part(scs[s2], true, 0, 0, wss[s2], sst[s2]));
       // The interchanges of step s2 on the finished L columns [0, s2*nb) are
       // deferred to the end of the phase: they reorder the A21 rows of the
       // earlier steps, whose updates of later blocks are still pending (the
@@ -2125,27 +2174,50 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
     // wavefront over (step, block): diagonal d applies step s to block d - s,
     // so step 0 keeps up with the upload while later steps wait for their
     // panels (each block still receives steps 0, 1, ... in order)
-    const int64_t nch = ceil_div(n, chunk_cols);
     for (int64_t d = 0; d < nch + S - 1; ++d) {
       for (int s2 = 0; s2 < S; ++s2) {
         const int64_t c = d - s2;
         if (c < 0 || c >= nch) continue;
         const int64_t c0 = c * chunk_cols, c1 = std::min<int64_t>(n, c0 + chunk_cols);
-        OZ_TRY(wait_until(c1));
+        const cudaStream_t ss = sst[s2];
+        OZ_TRY(wait_until(c1));  // the block's arrival (and max |A|) on the caller's stream
+        if (step_streams) {
+          if (s2 == 0) {
+            OZ_CHECK_CUDA(cudaEventRecord(evm, st));
+            OZ_CHECK_CUDA(cudaStreamWaitEvent(ss, evm, 0));
+          } else {
+            OZ_CHECK_CUDA(cudaStreamWaitEvent(ss, cdone[(size_t)(s2 - 1) * nch + c], 0));
+          }
+        }
         const int64_t j0 = s2 * nb, t0 = j0 + std::min<int64_t>(nb, n - j0);
         const int64_t r0 = std::max(c0, t0);
-        if (r0 >= c1) continue;  // this step's trailing columns start after the block
+        if (r0 >= c1) {  // this step's trailing columns start after the block
+          if (step_streams) OZ_CHECK_CUDA(cudaEventRecord(cdone[(size_t)s2 * nch + c], ss));
+          continue;
+        }
         OZ_TRY(ensure_panel(s2));
         const int jbs = (int)std::min<int64_t>(nb, n - j0);
-        OZ_TRY(laswp_ipiv(a, lda, r0, c1, 0, 0, j0, ipiv + j0, jbs, ws, st));
-        OZ_TRY(trsm_blocked(a, lda, j0, jbs, a + r0 * lda + j0, lda, c1 - r0, st));
-        OZ_TRY(schur_split_part(scs[s2], false, r0 - t0, c1 - t0, wss[s2], st));
-        OZ_TRY(schur_cols(scs[s2], r0 - t0, c1 - t0, wss[s2], st, sm_count() - la_sms));
+        OZ_TRY(laswp_ipiv(a, lda, r0, c1, 0, 0, j0, ipiv + j0, jbs, wss[s2], ss));
+        OZ_TRY(trsm_blocked(a, lda, j0, jbs, a + r0 * lda + j0, lda, c1 - r0, ss));
+        if (step_streams) {
+          // this block's columns as a Schur update of their own: the U12
+          // slices live in the step's block-sized buffer (steps run at once)
+          Schur scc = scs[s2];
+          scc.ncols = c1 - r0;
+          scc.u12 = a + r0 * lda + j0;
+          scc.a22 = a + r0 * lda + t0;
+          OZ_TRY(schur_split_part(scc, false, 0, c1 - r0, wss[s2], ss));
+          OZ_TRY(schur_cols(scc, 0, c1 - r0, wss[s2], ss, sm_count() - la_sms));
+        } else {
+          OZ_TRY(schur_split_part(scs[s2], false, r0 - t0, c1 - t0, wss[s2], ss));
+          OZ_TRY(schur_cols(scs[s2], r0 - t0, c1 - t0, wss[s2], ss, sm_count() - la_sms));
+        }
+        if (step_streams) OZ_CHECK_CUDA(cudaEventRecord(cdone[(size_t)s2 * nch + c], ss));
         // panel s2+1 has now received steps 0..s2 if its columns are in this block
         const int64_t p0 = (int64_t)(s2 + 1) * nb;
         if (next_panel == s2 + 1 && s2 + 1 <= S && p0 >= r0 &&
             p0 + std::min<int64_t>(nb, n - p0) <= c1) {
-          OZ_CHECK_CUDA(cudaEventRecord(side->ready, st));
+          OZ_CHECK_CUDA(cudaEventRecord(side->ready, ss));
           OZ_CHECK_CUDA(cudaStreamWaitEvent(side->st, side->ready, 0));
           OZ_TRY(panel_factor(a + p0 * lda + p0, lda, n - p0, std::min<int64_t>(nb, n - p0), p0,
                               ipiv + p0, info, ws.bits, ws, side->st, phase_panel_sms(p0)));
@@ -2156,6 +2228,16 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
     }
     OZ_REQUIRE(next_panel == S + 1, OZ_UNSUPPORTED, "upload phase did not reach panel %d", S);
     OZ_CHECK_CUDA(cudaStreamWaitEvent(st, pdone[S], 0));
+    if (step_streams) {
+      for (int s2 = 0; s2 < S; ++s2) {
+        OZ_CHECK_CUDA(cudaEventRecord(evm, sst[s2]));
+        OZ_CHECK_CUDA(cudaStreamWaitEvent(st, evm, 0));
+      }
+      OZ_CHECK_CUDA(cudaFreeAsync(cmp_buf, st));
+      OZ_CHECK_CUDA(cudaFreeAsync(stepb_buf, st));
+      for (auto e : cdone) cudaEventDestroy(e);
+      cudaEventDestroy(evm);
+    }
     // the deferred interchanges of steps 1..S-1 on their L columns, in step
     // order (every A21 of those steps has been consumed by now); step S's
     // follow in the loop below, before anything reads those columns again
