@@ -2149,6 +2149,21 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
       OZ_CHECK_CUDA(cudaEventRecord(evm, st));  // allocations and memsets above
       for (int s2 = 0; s2 < S; ++s2) OZ_CHECK_CUDA(cudaStreamWaitEvent(sst[s2], evm, 0));
     }
+    // OZ_LU_TRACE: timeline of the wavefront (task ends per step, panel ends)
+    const bool ptrace = getenv("OZ_LU_TRACE") != nullptr;
+    cudaEvent_t pt0 = nullptr;
+    std::vector<std::pair<std::string, cudaEvent_t>> pev;
+    auto pmark = [&](const std::string& name, cudaStream_t s3) {
+      if (!ptrace) return;
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, s3);
+      pev.emplace_back(name, e);
+    };
+    if (ptrace) {
+      cudaEventCreate(&pt0);
+      cudaEventRecord(pt0, st);
+    }
     std::vector<bool> have(S + 1, false);  // panel s ready on its step stream (A21 split)
     auto ensure_panel = [&](int s2) -> int {
       if (have[s2]) return OZ_OK;
@@ -2213,6 +2228,7 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
           OZ_TRY(schur_cols(scs[s2], r0 - t0, c1 - t0, wss[s2], ss, sm_count() - la_sms));
         }
         if (step_streams) OZ_CHECK_CUDA(cudaEventRecord(cdone[(size_t)s2 * nch + c], ss));
+        pmark("s" + std::to_string(s2) + "c" + std::to_string(c), ss);
         // panel s2+1 has now received steps 0..s2 if its columns are in this block
         const int64_t p0 = (int64_t)(s2 + 1) * nb;
         if (next_panel == s2 + 1 && s2 + 1 <= S && p0 >= r0 &&
@@ -2222,12 +2238,20 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
           OZ_TRY(panel_factor(a + p0 * lda + p0, lda, n - p0, std::min<int64_t>(nb, n - p0), p0,
                               ipiv + p0, info, ws.bits, ws, side->st, phase_panel_sms(p0)));
           OZ_CHECK_CUDA(cudaEventRecord(pdone[s2 + 1], side->st));
+          pmark("P" + std::to_string(s2 + 1), side->st);
           ++next_panel;
         }
       }
     }
     OZ_REQUIRE(next_panel == S + 1, OZ_UNSUPPORTED, "upload phase did not reach panel %d", S);
     OZ_CHECK_CUDA(cudaStreamWaitEvent(st, pdone[S], 0));
+    if (ptrace) {
+      // chunk arrivals: the caller's events (timing may be disabled on them)
+      for (int64_t c = 0; c < nch; ++c) {
+        cudaStreamWaitEvent(side->aux, chunk_ready[c], 0);
+        pmark("a" + std::to_string(c), side->aux);
+      }
+    }
     if (step_streams) {
       for (int s2 = 0; s2 < S; ++s2) {
         OZ_CHECK_CUDA(cudaEventRecord(evm, sst[s2]));
@@ -2256,6 +2280,20 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
       OZ_CHECK_CUDA(cudaFreeAsync(ex_buf, st));
     }
     for (auto e : pdone) cudaEventDestroy(e);
+    if (ptrace) {
+      pmark("phase_end", st);
+      cudaStreamSynchronize(st);
+      cudaStreamSynchronize(side->aux);
+      fprintf(stderr, "upload phase timeline [ms]:");
+      for (auto& kv : pev) {
+        float t = 0;
+        cudaEventElapsedTime(&t, pt0, kv.second);
+        fprintf(stderr, " %s=%.1f", kv.first.c_str(), t);
+        cudaEventDestroy(kv.second);
+      }
+      fprintf(stderr, "\n");
+      cudaEventDestroy(pt0);
+    }
     j_start = (int64_t)S * nb;
   }
   for (int64_t j = j_start; j < n; j += nb) {
