@@ -97,15 +97,17 @@ __device__ __forceinline__ void leaf_ll_store(unsigned long long* p, unsigned lo
   asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(t | lo), "l"(t | hi)
                : "memory");
 }
-__device__ __forceinline__ void leaf_ll_load(const unsigned long long* p, unsigned tag,
-                                             unsigned& lo, unsigned& hi) {
-  unsigned long long x, y;
-  do {
-    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(p)
-                 : "memory");
-  } while ((unsigned)(x >> 32) != tag || (unsigned)(y >> 32) != tag);
-  lo = (unsigned)x;
-  hi = (unsigned)y;
+__device__ __forceinline__ ulonglong2 leaf_ll_raw(const unsigned long long* p) {
+  ulonglong2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ bool leaf_ll_ok(ulonglong2 v, unsigned tag) {
+  return (unsigned)(v.x >> 32) == tag && (unsigned)(v.y >> 32) == tag;
+}
+__device__ __forceinline__ double leaf_ll_double(ulonglong2 v) {
+  return __longlong_as_double((long long)((v.y << 32) | (v.x & 0xffffffffull)));
 }
 __device__ __forceinline__ void leaf_ll_load2(const unsigned long long* p, unsigned tag,
                                               unsigned& w0, unsigned& w1, unsigned& w2,
@@ -327,6 +329,7 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(PanelArgs p) {
             reinterpret_cast<const unsigned long long*>(p.cand) + (size_t)b * G * LEAF_LL_STRIDE;
         double a1 = -2.0;
         int p1 = 0x7fffffff, g1 = -1;
+        long long* irw = reinterpret_cast<long long*>(sh.rec[b][0]);
         for (int gg = lane; gg < G; gg += 32) {
           const unsigned long long* r = slots + (size_t)gg * LEAF_LL_STRIDE;
           unsigned a_lo, a_hi, pv, rv;
@@ -340,14 +343,27 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(PanelArgs p) {
         }
         warp_argmax(a1, p1, g1);
         const unsigned long long* win = slots + (size_t)g1 * LEAF_LL_STRIDE;
-        long long* irw = reinterpret_cast<long long*>(sh.rec[b][0]);
-        for (int c = lane; c < 1 + W; c += 32) {
-          unsigned lo, hi;
-          leaf_ll_load(win + 2 * (c == 0 ? 1 : c + 1), tag, lo, hi);
-          if (c == 0)
-            irw[2] = (long long)(int)hi;
-          else
-            irw[3 + c] = (long long)(((unsigned long long)hi << 32) | lo);
+        // the winner's row and position: every load issued at once, then each
+        // pair re-polled only if its tags are not this step's yet (serial
+        // 16-byte polls cost a round trip per 32 values: 12288 x 1024 panel,
+        // 64-column windows on 100 SMs, leaves 3.48 -> 3.19 ms)
+        constexpr int NP = (W + 1 + 31) / 32;
+        ulonglong2 rv[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          const int c = lane + 32 * i;
+          if (c < 1 + W) rv[i] = leaf_ll_raw(win + 2 * (c == 0 ? 1 : c + 1));
+        }
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          const int c = lane + 32 * i;
+          if (c < 1 + W) {
+            while (!leaf_ll_ok(rv[i], tag)) rv[i] = leaf_ll_raw(win + 2 * (c == 0 ? 1 : c + 1));
+            if (c == 0)
+              irw[2] = (long long)(int)(unsigned)rv[i].y;
+            else
+              irw[3 + c] = (long long)((rv[i].y << 32) | (rv[i].x & 0xffffffffull));
+          }
         }
         if (lane == 0) {
           sh.rec[b][0][0] = a1;
