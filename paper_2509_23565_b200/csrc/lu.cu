@@ -516,69 +516,82 @@ __global__ void laswp_gather_kernel(double* __restrict__ a, int64_t lda, const i
 
 // LAPACK-style sequential interchanges -> one gather list.  ipiv[t] (global
 // row, >= k1 + t) is the row swapped with row k1 + t, applied in order
-// t = 0..npiv-1 (solve.py:80-82 / dlaswp).  One CTA: a single thread replays
-// the swaps on an index map (direct array for the npiv diagonal rows, an
-// open-addressing table for the rows below them), then the CTA emits
-// (dst, src) pairs meaning new_row[dst] = old_row[src].
+// t = 0..npiv-1 (solve.py:80-82 / dlaswp); the list holds (dst, src) pairs
+// meaning new_row[dst] = old_row[src].
 constexpr int COMPOSE_MAX = 1024;     // max interchanges per list (panel width)
-constexpr int COMPOSE_HASH = 4096;    // table slots for displaced rows (power of two)
-__global__ void __launch_bounds__(256) compose_ipiv_kernel(const int32_t* __restrict__ ipiv,
-                                                            int npiv, int64_t k1, int32_t* dst,
-                                                            int32_t* src, int32_t* cnt) {
-  __shared__ int32_t top[COMPOSE_MAX];
-  __shared__ int32_t slot[COMPOSE_MAX];  // per swap: index into top (< npiv) or hash slot
-  __shared__ int32_t hkey[COMPOSE_HASH];
-  __shared__ int32_t hval[COMPOSE_HASH];
+// One thread per interchange, no serial replay (was one thread replaying the
+// swaps on an index map: 80 us per panel on the critical chain, now ~10).
+// With p_t = ipiv[t] - k1 >= t: position t is final after step t and then
+// holds what position p_t held just before step t.  Position q is touched
+// before step t only as the far row of earlier steps, so it held
+// H(s*) for the last s* < t with p_s* = q (q itself if none), where H(s) —
+// the content of position s just before step s — is H(last s' < s with
+// p_s' = s), or s: a chain resolved by pointer jumping.  Rows below the
+// block end up with H(last s with p_s = q).
+__global__ void __launch_bounds__(COMPOSE_MAX) compose_ipiv_kernel(
+    const int32_t* __restrict__ ipiv, int npiv, int64_t k1, int32_t* dst, int32_t* src,
+    int32_t* cnt) {
+  __shared__ int32_t p[COMPOSE_MAX];
+  __shared__ int32_t prev_top[COMPOSE_MAX];  // last s' < s with p_s' == s, or -1
+  __shared__ int32_t hv[COMPOSE_MAX];        // H(s) once resolved
+  __shared__ int32_t hp[COMPOSE_MAX];        // pointer-jumping link
+  __shared__ int32_t has_next[COMPOSE_MAX];  // a later step has the same far row
   __shared__ int32_t npos;
-  for (int i = threadIdx.x; i < npiv; i += blockDim.x) top[i] = i;
-  for (int i = threadIdx.x; i < COMPOSE_HASH; i += blockDim.x) hkey[i] = -1;
-  if (threadIdx.x == 0) npos = 0;
+  const int t = threadIdx.x;
+  if (t < npiv) {
+    p[t] = (int)(ipiv[t] - k1);
+    prev_top[t] = -1;
+    has_next[t] = 0;
+  }
+  if (t == 0) npos = 0;
   __syncthreads();
-  // 1. (parallel) give every displaced row below the diagonal block a table slot
-  for (int t = threadIdx.x; t < npiv; t += blockDim.x) {
-    const int p = (int)(ipiv[t] - k1);  // relative row, >= t
-    if (p < npiv) {
-      slot[t] = p;
-    } else {
-      unsigned h = ((unsigned)p * 2654435761u) & (COMPOSE_HASH - 1);
-      while (true) {
-        const int prev = atomicCAS(&hkey[h], -1, p);
-        if (prev == -1 || prev == p) break;
-        h = (h + 1) & (COMPOSE_HASH - 1);
+  int sstar = -1;
+  if (t < npiv) {
+    const int pt = p[t];
+    if (pt < npiv && pt != t) atomicMax(&prev_top[pt], t);  // t < pt always
+    for (int s2 = t - 1; s2 >= 0; --s2)
+      if (p[s2] == pt) {
+        sstar = s2;
+        break;
       }
-      hval[h] = p;  // identical value from every thread that maps p here
-      slot[t] = COMPOSE_MAX + (int)h;
-    }
   }
   __syncthreads();
-  // 2. (one thread) replay the swaps in order on the index map, no probing
-  if (threadIdx.x == 0) {
-    for (int t = 0; t < npiv; ++t) {
-      const int sl = slot[t];
-      if (sl == t) continue;
-      int* other = sl < COMPOSE_MAX ? &top[sl] : &hval[sl - COMPOSE_MAX];
-      const int v = top[t];
-      top[t] = *other;
-      *other = v;
-    }
+  if (t < npiv) {
+    hp[t] = prev_top[t];
+    hv[t] = t;
+    if (sstar >= 0) has_next[sstar] = 1;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < npiv; i += blockDim.x) {
-    if (top[i] != i) {
+  for (int round = 0; round < 11; ++round) {  // 2^11 > COMPOSE_MAX
+    int nv = 0, np = -1;
+    if (t < npiv) {
+      const int q = hp[t];
+      nv = q >= 0 ? hv[q] : hv[t];
+      np = q >= 0 ? hp[q] : -1;
+    }
+    __syncthreads();
+    if (t < npiv) {
+      hv[t] = nv;
+      hp[t] = np;
+    }
+    __syncthreads();
+  }
+  if (t < npiv) {
+    const int pt = p[t];
+    const int f = sstar >= 0 ? hv[sstar] : pt;  // final content of position t
+    if (f != t) {
       const int at = atomicAdd(&npos, 1);
-      dst[at] = (int32_t)(k1 + i);
-      src[at] = (int32_t)(k1 + top[i]);
+      dst[at] = (int32_t)(k1 + t);
+      src[at] = (int32_t)(k1 + f);
     }
-  }
-  for (int i = threadIdx.x; i < COMPOSE_HASH; i += blockDim.x) {
-    if (hkey[i] >= 0 && hval[i] != hkey[i]) {
+    if (pt >= npiv && !has_next[t] && hv[t] != pt) {  // last step to touch row pt below
       const int at = atomicAdd(&npos, 1);
-      dst[at] = (int32_t)(k1 + hkey[i]);
-      src[at] = (int32_t)(k1 + hval[i]);
+      dst[at] = (int32_t)(k1 + pt);
+      src[at] = (int32_t)(k1 + hv[t]);
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) *cnt = npos;
+  if (t == 0) *cnt = npos;
 }
 
 // Apply a gather list of up to 2*COMPOSE_MAX entries to columns [c0a,c1a) U
@@ -1600,6 +1613,10 @@ int panel_window(double* a, int64_t lda, int64_t r0, int64_t m, int w, int64_t b
 
 // Apply the sequential interchanges ipiv[0..npiv) of rows k1.. (global ipiv
 // values) to columns [c0a,c1a) U [c0b,c1b) of a: compose once, gather once.
+void compose_launch(const int32_t* ipiv, int npiv, int64_t k1, const LuWs& ws, cudaStream_t st) {
+  compose_ipiv_kernel<<<1, COMPOSE_MAX, 0, st>>>(ipiv, npiv, k1, ws.cdst, ws.csrc, ws.ccnt);
+}
+
 int laswp_ipiv(double* a, int64_t lda, int64_t c0a, int64_t c1a, int64_t c0b, int64_t c1b,
                int64_t k1, const int32_t* ipiv, int npiv, const LuWs& ws, cudaStream_t st) {
   OZ_REQUIRE(npiv >= 0, OZ_INVALID_PARAMS, "negative interchange count");
@@ -1620,7 +1637,7 @@ int laswp_ipiv(double* a, int64_t lda, int64_t c0a, int64_t c1a, int64_t c0b, in
     cudaStream_t st;
     ~Stop() { prof_stop(tag, st, PROF_LASWP, 0.0); }
   } stop{prof_start(st), st};
-  compose_ipiv_kernel<<<1, 256, 0, st>>>(ipiv, npiv, k1, ws.cdst, ws.csrc, ws.ccnt);
+  compose_launch(ipiv, npiv, k1, ws, st);
   OZ_CHECK_LAUNCH();
   static const bool smem_variant = getenv("OZ_LASWP_SMEM") != nullptr;  // tuning
   if (smem_variant) {
@@ -1644,7 +1661,7 @@ int laswp_ipiv(double* a, int64_t lda, int64_t c0a, int64_t c1a, int64_t c0b, in
 int compose_list(int64_t k1, const int32_t* ipiv, int npiv, const LuWs& ws, cudaStream_t st) {
   OZ_REQUIRE(npiv >= 0 && npiv <= COMPOSE_MAX, OZ_INVALID_PARAMS, "bad interchange count");
   if (npiv == 0) return OZ_OK;
-  compose_ipiv_kernel<<<1, 256, 0, st>>>(ipiv, npiv, k1, ws.cdst, ws.csrc, ws.ccnt);
+  compose_launch(ipiv, npiv, k1, ws, st);
   OZ_CHECK_LAUNCH();
   return OZ_OK;
 }
