@@ -520,7 +520,7 @@ __global__ void laswp_gather_kernel(double* __restrict__ a, int64_t lda, const i
 // meaning new_row[dst] = old_row[src].
 constexpr int COMPOSE_MAX = 1024;     // max interchanges per list (panel width)
 // One thread per interchange, no serial replay (was one thread replaying the
-// swaps on an index map: 80 us per panel on the critical chain, now ~10).
+// swaps on an index map: 80 us per panel on the critical chain, now 11 us).
 // With p_t = ipiv[t] - k1 >= t: position t is final after step t and then
 // holds what position p_t held just before step t.  Position q is touched
 // before step t only as the far row of earlier steps, so it held
@@ -536,30 +536,47 @@ __global__ void __launch_bounds__(COMPOSE_MAX) compose_ipiv_kernel(
   __shared__ int32_t hv[COMPOSE_MAX];        // H(s) once resolved
   __shared__ int32_t hp[COMPOSE_MAX];        // pointer-jumping link
   __shared__ int32_t has_next[COMPOSE_MAX];  // a later step has the same far row
+  __shared__ int32_t prev_same[COMPOSE_MAX];  // last s < t with p_s == p_t, or -1
+  __shared__ unsigned long long key[COMPOSE_MAX];
   __shared__ int32_t npos;
   const int t = threadIdx.x;
   if (t < npiv) {
     p[t] = (int)(ipiv[t] - k1);
     prev_top[t] = -1;
     has_next[t] = 0;
+    prev_same[t] = -1;
   }
+  // (p_t, t) sorted (bitonic, padded with max keys): equal rows become
+  // neighbours in step order
+  key[t] = t < npiv ? ((unsigned long long)(ipiv[t] - k1) << 11) | (unsigned)t : ~0ull;
   if (t == 0) npos = 0;
   __syncthreads();
-  int sstar = -1;
-  if (t < npiv) {
-    const int pt = p[t];
-    if (pt < npiv && pt != t) atomicMax(&prev_top[pt], t);  // t < pt always
-    for (int s2 = t - 1; s2 >= 0; --s2)
-      if (p[s2] == pt) {
-        sstar = s2;
-        break;
+  if (t < npiv && p[t] < npiv && p[t] != t) atomicMax(&prev_top[p[t]], t);  // t < p_t
+  for (int kk = 2; kk <= COMPOSE_MAX; kk <<= 1) {
+    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+      const int u = t ^ jj;
+      if (u > t) {
+        const unsigned long long x = key[t], y = key[u];
+        if (((t & kk) == 0) == (x > y)) {
+          key[t] = y;
+          key[u] = x;
+        }
       }
+      __syncthreads();
+    }
+  }
+  if (t > 0 && t < npiv) {
+    const unsigned long long x = key[t], y = key[t - 1];
+    if ((x >> 11) == (y >> 11)) {
+      prev_same[(int)(x & 2047)] = (int)(y & 2047);
+      has_next[(int)(y & 2047)] = 1;
+    }
   }
   __syncthreads();
+  const int sstar = t < npiv ? prev_same[t] : -1;
   if (t < npiv) {
     hp[t] = prev_top[t];
     hv[t] = t;
-    if (sstar >= 0) has_next[sstar] = 1;
   }
   __syncthreads();
   for (int round = 0; round < 11; ++round) {  // 2^11 > COMPOSE_MAX
