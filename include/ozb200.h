@@ -226,7 +226,8 @@ int oz_copy2d(const double* src, int64_t rows, int64_t cols, int64_t src_rs, int
  *                 CTAs (a look-ahead panel beside a trailing update).
  * oz_laswp:       apply ipiv[0..npiv) (rows k1.., global values) as
  *                 sequential interchanges to columns [c0a,c1a) U [c0b,c1b)
- *                 (solve.py:80-82 whole-row swaps; LAPACK dlaswp); npiv <= 1024.
+ *                 (solve.py:80-82 whole-row swaps; LAPACK dlaswp); npiv <= 1024;
+ *                 fastest for getrf pivots (ipiv[t] >= k1 + t).
  * oz_trsm_lunit:  B <- L11^-1 B, L11 unit lower jb x jb (solve.py:123-127).
  * oz_schur_update: A22 -= A21 @ U12 through backend 0 (cuBLAS DGEMM) or 1
  *                 (Ozaki-INT8 emulated, pair table as oz_gemm_emu), growth

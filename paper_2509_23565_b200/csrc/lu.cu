@@ -550,7 +550,47 @@ __global__ void __launch_bounds__(COMPOSE_MAX) compose_ipiv_kernel(
   // neighbours in step order
   key[t] = t < npiv ? ((unsigned long long)(ipiv[t] - k1) << 11) | (unsigned)t : ~0ull;
   if (t == 0) npos = 0;
-  __syncthreads();
+  // General interchanges (a row above its step, p_t < t, which getrf never
+  // produces): one thread replays them on a content map instead
+  if (__syncthreads_or(t < npiv && p[t] < t)) {
+    if (t == 0) {
+      int32_t* fpos = prev_same;  // far rows touched, and their contents
+      int32_t* fval = has_next;
+      int nf = 0;
+      for (int i = 0; i < npiv; ++i) hv[i] = i;
+      for (int s2 = 0; s2 < npiv; ++s2) {
+        const int q = p[s2];
+        int* cq;
+        if (q >= 0 && q < npiv) {
+          cq = &hv[q];
+        } else {
+          int f = 0;
+          while (f < nf && fpos[f] != q) ++f;
+          if (f == nf) {
+            fpos[nf] = q;
+            fval[nf++] = q;
+          }
+          cq = &fval[f];
+        }
+        const int v = hv[s2];
+        hv[s2] = *cq;
+        *cq = v;
+      }
+      int at = 0;
+      for (int i = 0; i < npiv; ++i)
+        if (hv[i] != i) {
+          dst[at] = (int32_t)(k1 + i);
+          src[at++] = (int32_t)(k1 + hv[i]);
+        }
+      for (int f = 0; f < nf; ++f)
+        if (fval[f] != fpos[f]) {
+          dst[at] = (int32_t)(k1 + fpos[f]);
+          src[at++] = (int32_t)(k1 + fval[f]);
+        }
+      *cnt = at;
+    }
+    return;
+  }
   if (t < npiv && p[t] < npiv && p[t] != t) atomicMax(&prev_top[p[t]], t);  // t < p_t
   for (int kk = 2; kk <= COMPOSE_MAX; kk <<= 1) {
     for (int jj = kk >> 1; jj > 0; jj >>= 1) {

@@ -47,10 +47,12 @@ def _pivots(rng, kind, k1, npiv, m):
         return np.where(self_, k1 + t, far)
     if kind == "identity":
         return k1 + t
+    if kind == "general":        # rows above their step too (not getrf output; dlaswp allows it)
+        return k1 + (rng.random(npiv) * (m - k1)).astype(np.int64)
     raise ValueError(kind)
 
 
-@pytest.mark.parametrize("kind", ["random", "block", "repeat_far", "identity"])
+@pytest.mark.parametrize("kind", ["random", "block", "repeat_far", "identity", "general"])
 @pytest.mark.parametrize("npiv", [1, 37, 1024])
 def test_laswp_matches_sequential_swaps(kind, npiv):
     rng = np.random.default_rng(npiv * 7 + len(kind))
