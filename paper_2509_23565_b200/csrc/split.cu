@@ -239,7 +239,105 @@ __global__ void slices_tiled_kernel(const double* __restrict__ src, int64_t nvec
   }
 }
 
+// ---- one pass, vector-contiguous source (vs == 1, e.g. the LU's A21 panel in
+// column-major), per-vector exponents, K <= OP_K: a CTA keeps OP_R vectors x
+// K values in shared memory, reduces each vector's max, then emits its slices
+// from the tile — the FP64 source is read once instead of twice (exponent pass
+// + slice pass).  Same per-element arithmetic as the two-pass kernels.
+constexpr int OP_R = 8;      // vectors per CTA (70 KB tile: three CTAs per SM overlap load and emit)
+constexpr int OP_K = 1024;   // max K
+constexpr int OP_LD = OP_R + 1;  // tile row pitch (doubles)
+__global__ void __launch_bounds__(256) split_onepass_kernel(
+    const double* __restrict__ src, int64_t nvec, int64_t K, int64_t ts, int ksl, int q,
+    bool wide, int8_t* __restrict__ out, int64_t ld, int64_t sstride, int32_t* __restrict__ exps,
+    SplitAux* aux) {
+  extern __shared__ double tile[];  // [OP_K][OP_LD]: tile[t * OP_LD + r]
+  __shared__ double smax[8][2][32];
+  __shared__ int sexp[OP_R];
+  __shared__ int sbad;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t v0 = (int64_t)blockIdx.x * OP_R;
+  if (tid == 0) sbad = 0;
+  // load: thread -> row r = tid % OP_R of columns t = tid / OP_R + (256 / OP_R) i
+  constexpr int CS = 256 / OP_R;  // columns per pass
+  const int r = tid & (OP_R - 1), tq = tid / OP_R;
+  const int64_t v = v0 + r;
+  const bool vok = v < nvec;
+  double mx = 0.0;
+  bool bad = false;
+#pragma unroll 8
+  for (int t = tq; t < K; t += CS) {
+    const double x = vok ? __ldg(src + v + (int64_t)t * ts) : 0.0;
+    tile[t * OP_LD + r] = x;
+    note_value(x, mx, bad);
+  }
+  // the lanes of a warp that share a row (lane % OP_R), then across the 8
+  // warps (max and the non-finite flag per row)
+#pragma unroll
+  for (int o = OP_R; o < 32; o <<= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    bad = bad || __shfl_xor_sync(0xffffffffu, (int)bad, o);
+  }
+  if (lane < OP_R) {
+    smax[wid][0][lane] = mx;
+    smax[wid][1][lane] = bad ? 1.0 : 0.0;
+  }
+  if (bad) sbad = 1;
+  __syncthreads();
+  if (tid < OP_R) {
+    double m = smax[0][0][tid], b = smax[0][1][tid];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+      m = fmax(m, smax[w][0][tid]);
+      b = fmax(b, smax[w][1][tid]);
+    }
+    const int e = (m == 0.0 || b != 0.0) ? 0 : frexp_exp(m);
+    sexp[tid] = e;
+    if (v0 + tid < nvec) exps[v0 + tid] = e;
+  }
+  if (tid == 0 && sbad) aux->nonfinite = 1;
+  __syncthreads();
+  // emit: thread -> row r, 16 consecutive t per chunk
+  const double radix = (double)(1 << q);
+  const int e = sexp[r];
+  if (!vok) return;
+  for (int64_t t0 = (int64_t)tq * 16; t0 < ld; t0 += 16 * CS) {
+    double x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      x[i] = t0 + i < K ? ldexp_exact(tile[(t0 + i) * OP_LD + r], -e) : 0.0;
+    for (int s2 = 0; s2 < ksl; ++s2) {
+      uint32_t w[4], wl[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t packed = 0, packed_lo = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          double y = __dmul_rn(x[4 * i + b], radix);
+          double tr = trunc(y);
+          x[4 * i + b] = __dsub_rn(y, tr);
+          const int ti = (int)tr;
+          packed |= (uint32_t)(uint8_t)(int8_t)(wide ? (ti >> 7) : ti) << (8 * b);
+          packed_lo |= (uint32_t)(uint8_t)(ti & 127) << (8 * b);
+        }
+        w[i] = packed;
+        wl[i] = packed_lo;
+      }
+      int8_t* dst = out + (wide ? 2 * s2 : s2) * sstride + v * ld + t0;
+      *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+      if (wide) *reinterpret_cast<uint4*>(dst + sstride) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+    }
+  }
+}
+constexpr size_t OP_SMEM = sizeof(double) * OP_K * OP_LD;
+
 }  // namespace
+
+// OZ_SPLIT_ONEPASS=0: the two-pass tiled kernels for vector-contiguous sources (A/B)
+bool split_onepass_enabled() {
+  static const bool v = !getenv("OZ_SPLIT_ONEPASS") || atoi(getenv("OZ_SPLIT_ONEPASS"));
+  return v;
+}
 
 int split_launch(const double* src, int64_t rows, int64_t cols, int64_t row_stride,
                  int64_t col_stride, int orientation, int mode, int k, int q, int8_t* slices,
@@ -271,6 +369,12 @@ int split_launch(const double* src, int64_t rows, int64_t cols, int64_t row_stri
     OZ_CHECK_LAUNCH();
     slices_kcontig_kernel<16><<<(unsigned)blocks, threads, 0, st>>>(
         src, nvec, K, vs, mode, k, q, wide, slices, slice_ld, slice_stride, exps, aux);
+    OZ_CHECK_LAUNCH();
+  } else if (vs == 1 && mode == OZ_PER_VECTOR && K <= OP_K && split_onepass_enabled()) {
+    OZ_ONCE(cudaFuncSetAttribute(split_onepass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)OP_SMEM));
+    split_onepass_kernel<<<(unsigned)ceil_div(nvec, OP_R), 256, OP_SMEM, st>>>(
+        src, nvec, K, ts, k, q, wide, slices, slice_ld, slice_stride, exps, aux);
     OZ_CHECK_LAUNCH();
   } else {
     exps_tiled_kernel<<<(unsigned)ceil_div(nvec, 32), 256, 0, st>>>(src, nvec, K, vs, ts, mode,

@@ -46,6 +46,26 @@ def test_split_matches_oracle_random(shape, orient):
         assert np.array_equal(st.exponents, ref_e)
 
 
+@pytest.mark.parametrize("shape", [(1, 1), (17, 1024), (3000, 1000), (40, 1023)])
+def test_split_vector_contiguous_onepass(shape):
+    """Row-scaled split of a column-major source (the LU's A21 layout: one
+    pass through shared memory for K <= 1024) and column-scaled split of a
+    row-major one: bit-exact against the oracle, zero rows included."""
+    oz = _pkg()
+    rng = np.random.default_rng(shape[0] * 31 + shape[1])
+    a = (rng.random(shape) - 0.5) * np.ldexp(1.0, rng.integers(-70, 71, size=(shape[0], 1)))
+    a[::7] = 0.0
+    for k in (1, 7):
+        st = oz.split_matrix(np.asfortranarray(a), k, 7, oz.Orientation.ROW_SCALED)
+        ref_s, ref_e = orc.split(a, k, 7, "row")
+        assert np.array_equal(np.stack(st.slices), ref_s)
+        assert np.array_equal(st.exponents, ref_e)
+        st = oz.split_matrix(np.ascontiguousarray(a.T), k, 7, oz.Orientation.COL_SCALED)
+        ref_s, ref_e = orc.split(a.T, k, 7, "col")
+        assert np.array_equal(np.stack(st.slices), ref_s)
+        assert np.array_equal(st.exponents, ref_e)
+
+
 def test_split_nonfinite_raises():
     oz = _pkg()
     with pytest.raises(oz.NonFiniteEntryError):
