@@ -239,6 +239,82 @@ __global__ void slices_tiled_kernel(const double* __restrict__ src, int64_t nvec
   }
 }
 
+// ---- one pass, K contiguous (ts == 1), K <= 1024, per-vector exponents: one
+// warp per vector keeps its values in registers (lane l owns t = 16 l + 512 c
+// .. +15, the slice kernel's chunks), reduces the max, emits the slices — the
+// source is read once.  Same per-element arithmetic as the two-pass kernels.
+__global__ void split_kcontig_onepass_kernel(const double* __restrict__ src, int64_t nvec,
+                                             int64_t K, int64_t vs, int ksl, int q, bool wide,
+                                             int8_t* __restrict__ out, int64_t ld,
+                                             int64_t sstride, int32_t* __restrict__ exps,
+                                             SplitAux* aux) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const double radix = (double)(1 << q);
+  bool any_bad = false;
+  for (int64_t v = warp; v < nvec; v += nwarps) {
+    const double* p = src + v * vs;
+    const bool vec2 = ((reinterpret_cast<uintptr_t>(p) & 15) == 0);
+    double x[2][16];
+    double mx = 0.0;
+    bool bad = false;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int64_t t0 = (int64_t)lane * 16 + 512 * c;
+      if (t0 + 16 <= K && vec2) {
+        const double2* p2 = reinterpret_cast<const double2*>(p + t0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double2 w = __ldg(p2 + i);
+          x[c][2 * i] = w.x;
+          x[c][2 * i + 1] = w.y;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) x[c][i] = (t0 + i < K) ? __ldg(p + t0 + i) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) note_value(x[c][i], mx, bad);
+    }
+    mx = warp_max(mx);
+    bad = __any_sync(0xffffffffu, bad);
+    any_bad |= bad;
+    const int e = (mx == 0.0 || bad) ? 0 : frexp_exp(mx);
+    if (lane == 0) exps[v] = e;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int64_t t0 = (int64_t)lane * 16 + 512 * c;
+      if (t0 >= ld) continue;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[c][i] = ldexp_exact(x[c][i], -e);
+      for (int s2 = 0; s2 < ksl; ++s2) {
+        uint32_t w[4], wl[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t packed = 0, packed_lo = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            double y = __dmul_rn(x[c][4 * i + b], radix);
+            double tr = trunc(y);
+            x[c][4 * i + b] = __dsub_rn(y, tr);
+            const int ti = (int)tr;
+            packed |= (uint32_t)(uint8_t)(int8_t)(wide ? (ti >> 7) : ti) << (8 * b);
+            packed_lo |= (uint32_t)(uint8_t)(ti & 127) << (8 * b);
+          }
+          w[i] = packed;
+          wl[i] = packed_lo;
+        }
+        int8_t* dst = out + (wide ? 2 * s2 : s2) * sstride + v * ld + t0;
+        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+        if (wide)
+          *reinterpret_cast<uint4*>(dst + sstride) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+      }
+    }
+  }
+  if (lane == 0 && any_bad) aux->nonfinite = 1;
+}
+
 // ---- one pass, vector-contiguous source (vs == 1, e.g. the LU's A21 panel in
 // column-major), per-vector exponents, K <= OP_K: a CTA keeps OP_R vectors x
 // K values in shared memory, reduces each vector's max, then emits its slices
@@ -361,7 +437,15 @@ int split_launch(const double* src, int64_t rows, int64_t cols, int64_t row_stri
   SplitAux* aux = reinterpret_cast<SplitAux*>(aux_v);
   OZ_CHECK_CUDA(cudaMemsetAsync(aux, 0, sizeof(SplitAux), st));
   const int sms = sm_count();
-  if (ts == 1) {
+  if (ts == 1 && mode == OZ_PER_VECTOR && K <= 1024 && slice_ld <= 1024 &&
+      split_onepass_enabled()) {
+    const int threads = 256;
+    int64_t blocks = ceil_div(nvec, threads / 32);
+    blocks = blocks > (int64_t)sms * 16 ? (int64_t)sms * 16 : blocks;
+    split_kcontig_onepass_kernel<<<(unsigned)blocks, threads, 0, st>>>(
+        src, nvec, K, vs, k, q, wide, slices, slice_ld, slice_stride, exps, aux);
+    OZ_CHECK_LAUNCH();
+  } else if (ts == 1) {
     const int threads = 256;
     int64_t blocks = ceil_div(nvec, threads / 32);
     blocks = blocks > (int64_t)sms * 16 ? (int64_t)sms * 16 : blocks;
