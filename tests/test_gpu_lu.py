@@ -357,3 +357,43 @@ def test_solve_system_error_order():
     # the device stays usable after an exception in the overlapped path
     x, rep = oz.solve_system(np.eye(n) * 2.0, np.ones(n) * 2.0, 64)
     assert np.array_equal(x, np.ones(n))
+
+
+_LARGE_SCRIPT = r"""
+import hashlib, json, sys
+import torch
+import paper_2509_23565_b200 as oz
+from paper_2509_23565_b200.matgen import generate_device
+n, nb = int(sys.argv[1]), int(sys.argv[2])
+a = generate_device(0, n, seed=99)
+b = a.sum(1)
+x, rep = oz.solve_system(a, b, nb, oz.GemmBackend.int8(7))
+f = oz.lu_factor(a, nb, oz.GemmBackend.int8(7))
+piv = f.pivots.cpu().numpy().tobytes()
+print(json.dumps({"resid": rep.scaled_residual, "piv": hashlib.sha256(piv).hexdigest()}))
+"""
+
+
+def test_large_lu_leaf_variants_agree(tmp_path):
+    """An LU large enough for every register-leaf variant and the planner's
+    paths (grid leaves with tagged-word records, the tall 1024-row leaf on the
+    look-ahead's capped grid, two-phase look-ahead, aux-stream interchanges):
+    the same pivots and a passing residual as with the shared-memory leaf for
+    the tallest panels (OZ_PANEL_LEAF_TALL=0) — the leaf choice only moves the
+    in-panel blocking, so factors agree to rounding."""
+    import json
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "large.py"
+    script.write_text(_LARGE_SCRIPT)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = []
+    for env_extra in ({}, {"OZ_PANEL_LEAF_TALL": "0"}):
+        env = dict(os.environ, PYTHONPATH=root, **env_extra)
+        r = subprocess.run([sys.executable, str(script), "20480", "1024"], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert out[0]["piv"] == out[1]["piv"]
+    assert 0.0 < out[0]["resid"] < 1.0 and 0.0 < out[1]["resid"] < 1.0
