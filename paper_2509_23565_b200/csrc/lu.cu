@@ -1324,7 +1324,18 @@ int trsm_blocked(double* a, int64_t lda, int64_t j, int64_t jb, double* b, int64
     const int tag = prof_start(st);
     // 8 columns per CTA: measured faster than 4 or 2 (more CTAs) at every
     // panel-recursion shape and inside the LU (profiles/r02bm_trsm_nc_ab.log)
-    const int s = trsm_fused<8>(a + j * lda + j, lda, jb, b, ldb, ncols, st, max_ctas);
+    // A capped grid (SMs held by a concurrent kernel) takes a few more
+    // columns per CTA rather than a second wave of CTAs
+    const int avail = max_ctas > 0 && max_ctas < sm_count() ? max_ctas : sm_count();
+    static const bool widen = !getenv("OZ_TRSM_WIDEN") || atoi(getenv("OZ_TRSM_WIDEN"));
+    const double* l11 = a + j * lda + j;
+    const int s = !widen || ceil_div(ncols, (int64_t)8) <= avail
+                      ? trsm_fused<8>(l11, lda, jb, b, ldb, ncols, st, max_ctas)
+                  : ceil_div(ncols, (int64_t)9) <= avail
+                      ? trsm_fused<9>(l11, lda, jb, b, ldb, ncols, st, max_ctas)
+                  : ceil_div(ncols, (int64_t)10) <= avail
+                      ? trsm_fused<10>(l11, lda, jb, b, ldb, ncols, st, max_ctas)
+                      : trsm_fused<12>(l11, lda, jb, b, ldb, ncols, st, max_ctas);
     prof_stop(tag, st, PROF_TRSM, (double)jb * jb * ncols);
     return s;
   }
@@ -2417,7 +2428,8 @@ int lu_factor(double* a, int64_t n, int64_t lda, int64_t nb, int backend, int k,
     tr.mark(st);  // 1 after laswp
     if (rest > 0) {
       // trsm U12 = L11^-1 A12 (solve.py:123-127), split, Schur update (:130-134)
-      OZ_TRY(trsm_blocked(a, lda, j, jb, a12, lda, la ? jb2 : rest, st));
+      OZ_TRY(trsm_blocked(a, lda, j, jb, a12, lda, la ? jb2 : rest, st,
+                          aux ? sm_count() - aux_ctas : 0));
       tr.mark(st);  // 2 after trsm
       OZ_TRY(schur_split_part(sc, true, 0, la ? jb2 : rest, ws, st));
       tr.mark(st);  // 3 after split
